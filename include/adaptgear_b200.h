@@ -1,0 +1,233 @@
+/*
+ * adaptgear_b200.h -- C ABI of the B200-native AdaptGear aggregation path.
+ *
+ * Everything below is `extern "C"`, takes plain pointers + sizes and an opaque
+ * `void *stream` (a cudaStream_t; NULL = legacy default stream).  Pointers are
+ * DEVICE pointers unless the name ends in `_host`.  Outputs are caller-allocated
+ * unless stated otherwise.  Every entry point returns an AG_* status; on failure
+ * ag_last_error() returns a thread-local message that the Python shim maps onto
+ * the reference's exception types (ValueError / KernelError / RuntimeError).
+ *
+ * Reference interface each group replaces (paths relative to
+ * /root/reference/pkg/src/adaptgear/):
+ *   preprocessing  graph.py:47-82 (Graph.from_edges), models.py:57-73
+ *                  (gcn_normalize), reorder.py:92-228 (cluster_bfs,
+ *                  load_partition, apply_reorder), decompose.py:57-75,
+ *                  formats.py:76-140 (to_csr / to_coo / to_dense_blocks)
+ *   kernels        kernels.py:117-134 (aggregate_csr_inter),
+ *                  kernels.py:137-189 (aggregate_csr_intra_blocked),
+ *                  kernels.py:192-225 (aggregate_coo_atomic),
+ *                  kernels.py:228-250 (aggregate_dense_block),
+ *                  kernels.py:253-276 (combine), kernels.py:309-313 (backward_sum)
+ *   layers         models.py:86-112 (gcn/gin_layer_forward: agg @ W)
+ */
+#ifndef ADAPTGEAR_B200_H
+#define ADAPTGEAR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (ag_last_error() holds the message) ------------------- */
+#define AG_OK 0
+#define AG_ERR_VALUE 1  /* -> ValueError  (bad sizes / ids / block_size)     */
+#define AG_ERR_KERNEL 2 /* -> KernelError (kernel preconditions)            */
+#define AG_ERR_CUDA 3   /* -> RuntimeError (CUDA runtime failure)           */
+
+/* ---- aggregation operators: kernels.py:42-45 AggregateOp ----------------- */
+#define AG_OP_SUM 0
+#define AG_OP_MEAN 1
+#define AG_OP_MAX 2
+
+/* ---- epilogue flags of the aggregation kernels -------------------------- */
+/* AG_EPI_COMBINE: y already holds the OTHER role's partial (inter values, or
+ *   zeros for an empty partial); the kernel writes combine(this, other)
+ *   exactly as kernels.py:253-276 does (sum: a+b; mean: (a+b)/f32(max(deg,1));
+ *   max: touched-aware).  Without it the kernel stores the raw partial (rows
+ *   with no edges get 0, kernels.py:123).
+ * AG_EPI_GIN: additionally y = f32(gin_scale) * x + y  (models.py:111). */
+#define AG_EPI_COMBINE 1
+#define AG_EPI_GIN 2
+
+int ag_abi_version(void);
+const char *ag_last_error(void);
+/* Number of SMs of the current device (0 when no device is present). */
+int ag_device_sm_count(void);
+/* Kernels this library has launched since load (process-wide counter). */
+uint64_t ag_launch_count(void);
+
+/* ======================= preprocessing (device) ========================== */
+
+/* Graph.from_edges (graph.py:47-82): validate endpoints against [0, V),
+ * sort by key dst*V+src, drop duplicates, sum duplicate weights in fp64 in
+ * input order and round to fp32.  dst/src are int64[E]; w may be NULL.
+ * Outputs must hold E entries; *num_out_host receives the unique count. */
+int ag_canonicalize(int64_t num_vertices, int64_t num_edges, const int64_t *dst,
+                    const int64_t *src, const float *w, int32_t *dst_out,
+                    int32_t *src_out, float *w_out, int64_t *num_out_host,
+                    void *stream);
+
+/* apply_reorder relabel step (reorder.py:217-228): out = perm[in] as int64. */
+int ag_relabel(int64_t num_edges, const int64_t *perm, const int32_t *dst,
+               const int32_t *src, int64_t *dst_out, int64_t *src_out,
+               void *stream);
+
+/* gcn_normalize (models.py:57-73) on a canonical graph: binary union with
+ * self loops, in-degree of A+I, w = f32(1/sqrt(f64(deg[d])*f64(deg[s]))).
+ * Outputs must hold E+V entries. */
+int ag_gcn_normalize(int64_t num_vertices, int64_t num_edges,
+                     const int32_t *dst, const int32_t *src, int32_t *dst_out,
+                     int32_t *src_out, float *w_out, int64_t *num_out_host,
+                     void *stream);
+
+/* in_degrees (graph.py:94-96): int64 histogram of dst. */
+int ag_in_degrees(int64_t num_vertices, int64_t num_edges, const int32_t *dst,
+                  int64_t *deg_out, void *stream);
+
+/* decompose (decompose.py:57-75), two phases: count intra edges, then split
+ * order-preservingly (a canonical input stays canonical).  w may be NULL. */
+int ag_decompose_count(int64_t num_edges, const int32_t *dst,
+                       const int32_t *src, int64_t block_size,
+                       int64_t *num_intra_host, void *stream);
+int ag_decompose_split(int64_t num_edges, const int32_t *dst,
+                       const int32_t *src, const float *w, int64_t block_size,
+                       int32_t *intra_dst, int32_t *intra_src, float *intra_w,
+                       int32_t *inter_dst, int32_t *inter_src, float *inter_w,
+                       void *stream);
+
+/* to_csr (formats.py:76-88): row_ptr[V+1] from canonical (sorted) dst. */
+int ag_build_row_ptr(int64_t num_vertices, int64_t num_edges,
+                     const int32_t *dst, int32_t *row_ptr, void *stream);
+
+/* touched = rowlen > 0 (kernels.py:121). */
+int ag_row_touched(int64_t num_rows, const int32_t *row_ptr, uint8_t *touched,
+                   void *stream);
+
+/* First edge index whose endpoints are in different B-blocks, or -1
+ * (formats.py:115-123, kernels.py:154-161).  Uses CSR arrays only. */
+int ag_first_off_block(int64_t num_rows, const int32_t *row_ptr,
+                       const int32_t *col_idx, int64_t block_size,
+                       int64_t *first_bad_host, void *stream);
+
+/* to_dense_blocks (formats.py:105-140), two phases.  count: number k of
+ * B-blocks holding >= 1 edge.  fill: community_ids[k] (ascending),
+ * comm_slot[ceil(V/B)] (slot or -1), blocks[k*B*B] (zero-filled here),
+ * row_touched[k*B].  Edges must be block-local (checked by the caller). */
+int ag_blocks_count(int64_t num_vertices, int64_t num_edges,
+                    const int32_t *dst, int64_t block_size, int64_t *k_host,
+                    void *stream);
+int ag_blocks_fill(int64_t num_vertices, int64_t num_edges, const int32_t *dst,
+                   const int32_t *src, const float *w, int64_t block_size,
+                   int64_t k, int32_t *community_ids, int32_t *comm_slot,
+                   float *blocks, uint8_t *row_touched, void *stream);
+
+/* ================== aggregation kernels (the hot path) =================== */
+
+/* K1 aggregate_csr_inter (kernels.py:87-134).  Y[r] = sum_e val[e]*X[col[e]]
+ * reduced in EXACTLY numpy's np.add.reduceat order (first term + pairwise
+ * 8-accumulator blocked sum, block 128) so values are bitwise equal to the
+ * reference; max reduces raw X rows.  val may be NULL (implicit 1.0).
+ * x, y: fp32 [V, F] row-major.  See AG_EPI_* for the epilogue. */
+int ag_csr_spmm(int64_t num_rows, int64_t feat, const int32_t *row_ptr,
+                const int32_t *col_idx, const float *val, const float *x,
+                float *y, int32_t op, int32_t epi_flags,
+                const uint8_t *other_touched, const int64_t *deg,
+                float gin_scale, void *stream);
+
+/* K2 aggregate_csr_intra_blocked (kernels.py:137-189): one CTA per B-row
+ * community; the community's B x F_tile source slab is staged in shared
+ * memory once and every row of the block gathers from it.  F is tiled so
+ * that B*F_tile*4 <= tile_budget_bytes (kernels.py:169-171).  Values are
+ * bitwise identical to ag_csr_spmm. */
+int ag_csr_intra_spmm(int64_t num_rows, int64_t feat, int64_t block_size,
+                      int64_t tile_budget_bytes, const int32_t *row_ptr,
+                      const int32_t *col_idx, const float *val, const float *x,
+                      float *y, int32_t op, int32_t epi_flags,
+                      const uint8_t *other_touched, const int64_t *deg,
+                      float gin_scale, void *stream);
+
+/* K3 aggregate_coo_atomic (kernels.py:192-225): edge-parallel over a
+ * (row, col)-sorted COO; warps fold runs of equal rows in registers and
+ * flush with vector atomics.  ACCUMULATES into y: the caller initialises
+ * y to 0 (sum/mean) or -inf (max). */
+int ag_coo_spmm(int64_t num_rows, int64_t feat, int64_t num_edges,
+                const int32_t *row, const int32_t *col, const float *val,
+                const float *x, float *y, int32_t op, void *stream);
+
+/* K4 aggregate_dense_block (kernels.py:228-250): for every B-row community c
+ * with slot k = comm_slot[c] >= 0: Y[cB:cB+B] = blocks[k] @ X[cB:cB+B]
+ * (ragged last block zero-padded).  Communities without a block produce an
+ * untouched (zero) partial.  Rejects max (kernels.py:234-235). */
+int ag_dense_block_spmm(int64_t num_rows, int64_t feat, int64_t block_size,
+                        const int32_t *comm_slot, const float *blocks,
+                        const uint8_t *row_touched, const float *x, float *y,
+                        int32_t op, int32_t epi_flags,
+                        const uint8_t *other_touched, const int64_t *deg,
+                        float gin_scale, void *stream);
+
+/* K5 combine (kernels.py:253-276) as a standalone pass. out may alias a. */
+int ag_combine(int64_t num_rows, int64_t feat, const float *a,
+               const uint8_t *touched_a, const float *b,
+               const uint8_t *touched_b, const int64_t *deg, int32_t op,
+               float *out, void *stream);
+
+/* ======================== dense update (K7) ============================== */
+
+/* C = alpha * op(A) @ op(B) + beta * C, fp32 row-major, optional ReLU on
+ * the result (epilogue 1).  op(A) is [M,K], op(B) is [K,N]. */
+#define AG_GEMM_RELU 1
+int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
+                float *C, int64_t ldc, float alpha, float beta,
+                int32_t epilogue, void *stream);
+
+/* ===================== training helpers (composed) ======================= */
+
+/* Mean softmax cross-entropy over rows with mask[r] != 0 (mask may be NULL =
+ * all rows).  Writes the loss (fp32 scalar, device) and dlogits =
+ * (softmax - onehot) / n_masked (0 for unmasked rows). */
+int ag_softmax_xent(int64_t num_rows, int64_t num_classes, const float *logits,
+                    const int32_t *labels, const uint8_t *mask,
+                    int64_t num_masked, float *loss_out, float *dlogits,
+                    void *stream);
+/* g = g * (h > 0) in place (ReLU backward). */
+int ag_relu_backward(int64_t n, const float *h, float *g, void *stream);
+/* w -= lr * dw. */
+int ag_sgd_step(int64_t n, float *w, const float *dw, float lr, void *stream);
+
+/* ====================== host-side preprocessing ========================== */
+
+/* cluster_bfs (reorder.py:92-153) bit-exact, sequential, HOST arrays.
+ * dst_host/src_host: canonical int32 edges.  Outputs int64[V]. */
+int ag_cluster_bfs(int64_t num_vertices, int64_t num_edges,
+                   const int32_t *dst_host, const int32_t *src_host,
+                   int64_t comm_size, int64_t *community_out_host,
+                   int64_t *permutation_out_host);
+
+/* load_partition core (reorder.py:156-203): stable sort of community ids,
+ * chunking into <= comm_size runs, renumbering.  HOST arrays. */
+int ag_partition_from_ids(int64_t num_vertices, const int64_t *ids_host,
+                          int64_t comm_size, int64_t *community_out_host,
+                          int64_t *permutation_out_host);
+
+/* ====================== synthetic generator (device) ===================== */
+
+/* Candidate edges of the seeded community generator:
+ * candidate i in [first, first+count) -> (dst, src) int64 in PRE-shuffle id
+ * space.  Pure function of (params, i): identical to oracle/synth.py. */
+int ag_synth_candidates(int64_t num_vertices, int64_t block_gen,
+                        double p_intra, double p_global, int64_t window,
+                        int64_t skew, uint64_t seed, int64_t first,
+                        int64_t count, int64_t *dst_out, int64_t *src_out,
+                        void *stream);
+/* 64-bit vertex shuffle keys: key[v] = hash(seed, v). */
+int ag_synth_vertex_keys(int64_t num_vertices, uint64_t seed, uint64_t *keys,
+                         void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADAPTGEAR_B200_H */

@@ -1,0 +1,281 @@
+// Dense update and training helpers of the GCN/GIN layers.
+//   ag_gemm_f32      the (agg @ W) update of models.py:99/:112 and its two
+//                    backward products (H^T G, G W^T); fp32 SIMT, 128x128x8
+//                    CTA tiles, 8x8 register micro-tiles, register-prefetched
+//                    double buffering, deterministic split-K for the skinny
+//                    H^T G case (K = V, M,N <= a few hundred).
+//   ag_softmax_xent  composed loss of SURVEY.md §8c (mean masked softmax CE)
+//   ag_relu_backward, ag_sgd_step
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "ag_common.cuh"
+
+namespace ag {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 8, TM = 8, TN = 8, NT = 256;
+
+struct GemmArgs {
+  int64_t M, N, K;
+  const float *A;
+  int64_t lda;
+  int ta;
+  const float *B;
+  int64_t ldb;
+  int tb;
+  float *C;  // final output (splits == 1) or partial buffer [splits][M][N]
+  int64_t ldc;
+  float alpha, beta;
+  int epi;
+  int64_t k_per_split;
+};
+
+// A(m, k) of op(A) and B(k, n) of op(B)
+__device__ __forceinline__ float ldA(const GemmArgs &g, int64_t m, int64_t k) {
+  if (m >= g.M || k >= g.K) return 0.0f;
+  return g.ta ? __ldg(g.A + k * g.lda + m) : __ldg(g.A + m * g.lda + k);
+}
+__device__ __forceinline__ float ldB(const GemmArgs &g, int64_t k, int64_t n) {
+  if (k >= g.K || n >= g.N) return 0.0f;
+  return g.tb ? __ldg(g.B + n * g.ldb + k) : __ldg(g.B + k * g.ldb + n);
+}
+
+__global__ void __launch_bounds__(NT, 2) sgemm_kernel(GemmArgs g, int partial) {
+  __shared__ __align__(16) float As[2][BK][BM];
+  __shared__ __align__(16) float Bs[2][BK][BN];
+  const int tid = threadIdx.x;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM;
+  const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
+  const int64_t kbeg = static_cast<int64_t>(blockIdx.z) * g.k_per_split;
+  const int64_t kend = min(g.K, kbeg + g.k_per_split);
+  // loader mapping: 1024 elements of each tile, 4 per thread
+  // non-transposed A: row-major [m][k]  -> thread loads (m = tid/2, k = (tid%2)*4 .. +4)
+  // transposed A:     stored [k][m]     -> thread loads (k = tid/32, m = (tid%32)*4 .. +4)
+  float ra[4], rb[4];
+  auto load_regs = [&](int64_t k0) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (!g.ta) ra[t] = ldA(g, m0 + tid / 2, k0 + (tid % 2) * 4 + t);
+      else ra[t] = ldA(g, m0 + (tid % 32) * 4 + t, k0 + tid / 32);
+      if (!g.tb) rb[t] = ldB(g, k0 + tid / 32, n0 + (tid % 32) * 4 + t);
+      else rb[t] = ldB(g, k0 + (tid % 2) * 4 + t, n0 + tid / 2);
+    }
+  };
+  auto store_smem = [&](int buf) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (!g.ta) As[buf][(tid % 2) * 4 + t][tid / 2] = ra[t];
+      else As[buf][tid / 32][(tid % 32) * 4 + t] = ra[t];
+      if (!g.tb) Bs[buf][tid / 32][(tid % 32) * 4 + t] = rb[t];
+      else Bs[buf][(tid % 2) * 4 + t][tid / 2] = rb[t];
+    }
+  };
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
+  const int ty = tid / 16, tx = tid % 16;
+  int buf = 0;
+  if (kbeg < kend) {
+    load_regs(kbeg);
+    store_smem(0);
+    __syncthreads();
+  }
+  for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
+    const bool more = k0 + BK < kend;
+    if (more) load_regs(k0 + BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[TM], b[TN];
+      const float4 a0 = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4 *>(&As[buf][kk][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][64 + tx * 4]);
+      a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+      a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+      b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (more) {
+      store_smem(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  // epilogue: rows ty*4+{0..3} and 64+ty*4+{0..3}; cols tx*4+{0..3}, 64+tx*4+{0..3}
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    if (m >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+      if (n >= g.N) continue;
+      if (partial) {
+        g.C[(static_cast<int64_t>(blockIdx.z) * g.M + m) * g.N + n] = acc[i][j];
+      } else {
+        float v = g.alpha * acc[i][j];
+        if (g.beta != 0.0f) v = fmaf(g.beta, g.C[m * g.ldc + n], v);
+        if (g.epi & AG_GEMM_RELU) v = fmaxf(v, 0.0f);
+        g.C[m * g.ldc + n] = v;
+      }
+    }
+  }
+}
+
+__global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const float *part, float *C,
+                                     int64_t ldc, float alpha, float beta, int epi) {
+  const int64_t n = M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.0f;
+    for (int p = 0; p < splits; ++p) s += part[p * n + i];  // fixed order: deterministic
+    const int64_t m = i / N, c = i % N;
+    float v = alpha * s;
+    if (beta != 0.0f) v = fmaf(beta, C[m * ldc + c], v);
+    if (epi & AG_GEMM_RELU) v = fmaxf(v, 0.0f);
+    C[m * ldc + c] = v;
+  }
+}
+
+// One warp per row: mean softmax cross-entropy over the masked rows.
+__global__ void xent_rows_kernel(int64_t rows, int64_t C, const float *logits,
+                                 const int32_t *labels, const uint8_t *mask, float inv_n,
+                                 float *row_loss, float *dlogits) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const float *z = logits + r * C;
+    float *dz = dlogits + r * C;
+    const bool on = mask ? mask[r] != 0 : true;
+    if (!on) {
+      for (int64_t c = lane; c < C; c += 32) dz[c] = 0.0f;
+      if (lane == 0) row_loss[r] = 0.0f;
+      continue;
+    }
+    float mx = -INFINITY;
+    for (int64_t c = lane; c < C; c += 32) mx = fmaxf(mx, z[c]);
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float se = 0.0f;
+    for (int64_t c = lane; c < C; c += 32) se += expf(z[c] - mx);
+    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const int32_t y = labels[r];
+    const float lse = mx + logf(se);
+    for (int64_t c = lane; c < C; c += 32) {
+      const float p = expf(z[c] - mx) / se;
+      dz[c] = (p - (c == y ? 1.0f : 0.0f)) * inv_n;
+    }
+    if (lane == 0) row_loss[r] = lse - z[y];
+  }
+}
+
+// Deterministic single-CTA reduction of the per-row losses.
+__global__ void loss_reduce_kernel(int64_t rows, const float *row_loss, float inv_n, float *out) {
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) s += row_loss[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = static_cast<float>(sh[0] * inv_n);
+}
+
+__global__ void relu_bwd_kernel(int64_t n, const float *h, float *g) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (!(h[i] > 0.0f)) g[i] = 0.0f;
+}
+
+__global__ void sgd_kernel(int64_t n, float *w, const float *dw, float lr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    w[i] = w[i] - lr * dw[i];
+}
+
+}  // namespace
+}  // namespace ag
+
+using namespace ag;
+
+extern "C" int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                           int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
+                           float *C, int64_t ldc, float alpha, float beta, int32_t epilogue,
+                           void *stream) {
+  if (M < 0 || N < 0 || K < 0) return fail(AG_ERR_VALUE, "negative GEMM sizes");
+  if (M == 0 || N == 0) return AG_OK;
+  cudaStream_t st = as_stream(stream);
+  const int64_t tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  if (tiles_m > 65535) return fail(AG_ERR_VALUE, "GEMM M too large (%lld)", (long long)M);
+  const int64_t tiles = tiles_m * tiles_n;
+  const int64_t target = 2LL * sm_count();
+  int splits = 1;
+  if (tiles < target && K >= 4 * 512) {
+    splits = static_cast<int>(std::min<int64_t>((target + tiles - 1) / tiles, K / 512));
+    splits = std::max(1, std::min(splits, 256));
+  }
+  int64_t kps = (K + splits - 1) / splits;
+  kps = (kps + BK - 1) / BK * BK;
+  splits = static_cast<int>((K + kps - 1) / kps);
+  if (splits < 1) splits = 1;
+  GemmArgs g{M, N, K, A, lda, trans_a, B, ldb, trans_b, C, ldc, alpha, beta, epilogue, kps};
+  dim3 grid(static_cast<unsigned>(tiles_n), static_cast<unsigned>(tiles_m), splits);
+  if (splits == 1) {
+    sgemm_kernel<<<grid, NT, 0, st>>>(g, 0);
+    AG_LAUNCH_CHECK("sgemm_kernel");
+    return AG_OK;
+  }
+  Scratch part;
+  AG_CUDA(part.alloc(static_cast<size_t>(splits) * M * N * sizeof(float), st));
+  g.C = part.as<float>();
+  sgemm_kernel<<<grid, NT, 0, st>>>(g, 1);
+  AG_LAUNCH_CHECK("sgemm_kernel(split)");
+  splitk_reduce_kernel<<<grid_for(M * N, 256), 256, 0, st>>>(M, N, splits, part.as<float>(), C,
+                                                            ldc, alpha, beta, epilogue);
+  AG_LAUNCH_CHECK("splitk_reduce_kernel");
+  return AG_OK;
+}
+
+extern "C" int ag_softmax_xent(int64_t rows, int64_t C, const float *logits, const int32_t *labels,
+                               const uint8_t *mask, int64_t num_masked, float *loss_out,
+                               float *dlogits, void *stream) {
+  if (rows < 0 || C < 1) return fail(AG_ERR_VALUE, "bad loss sizes");
+  cudaStream_t st = as_stream(stream);
+  const float inv_n = num_masked > 0 ? 1.0f / static_cast<float>(num_masked) : 0.0f;
+  Scratch rl;
+  AG_CUDA(rl.alloc(std::max<int64_t>(rows, 1) * sizeof(float), st));
+  if (rows > 0) {
+    xent_rows_kernel<<<grid_for(rows * 32, 256), 256, 0, st>>>(rows, C, logits, labels, mask,
+                                                               inv_n, rl.as<float>(), dlogits);
+    AG_LAUNCH_CHECK("xent_rows_kernel");
+  }
+  loss_reduce_kernel<<<1, 1024, 0, st>>>(rows, rl.as<float>(),
+                                         num_masked > 0 ? 1.0 / num_masked : 0.0, loss_out);
+  AG_LAUNCH_CHECK("loss_reduce_kernel");
+  return AG_OK;
+}
+
+extern "C" int ag_relu_backward(int64_t n, const float *h, float *g, void *stream) {
+  if (n == 0) return AG_OK;
+  relu_bwd_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, h, g);
+  AG_LAUNCH_CHECK("relu_bwd_kernel");
+  return AG_OK;
+}
+
+extern "C" int ag_sgd_step(int64_t n, float *w, const float *dw, float lr, void *stream) {
+  if (n == 0) return AG_OK;
+  sgd_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, w, dw, lr);
+  AG_LAUNCH_CHECK("sgd_kernel");
+  return AG_OK;
+}

@@ -1,0 +1,200 @@
+"""Device-resident physical formats (reference formats.py:16-161).
+
+CSR over destinations (row_ptr int32[V+1], col_idx int32[E], val f32[E]),
+canonical COO (row, col, val) and per-community dense diagonal blocks.  All
+are built on the device once per graph and cached (the reference rebuilds
+them on every aggregate_decomposed call).  For unweighted
+graphs the value array is implicit (the kernels take val=NULL, i.e. 1.0),
+so GIN aggregation never reads a ones vector from HBM; `.val` materialises
+it lazily for API compatibility.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .graph import Graph, as_device
+
+
+class CooMatrix:
+    """Coordinate-format adjacency sorted by (row, col)."""
+
+    __slots__ = ("num_vertices", "row", "col", "_val", "_ones")
+
+    def __init__(self, num_vertices: int, row: torch.Tensor, col: torch.Tensor,
+                 val: torch.Tensor | None):
+        self.num_vertices = int(num_vertices)
+        self.row, self.col, self._val, self._ones = row, col, val, None
+
+    @property
+    def val(self) -> torch.Tensor:
+        if self._val is not None:
+            return self._val
+        if self._ones is None:
+            self._ones = torch.ones(self.num_edges, dtype=torch.float32, device=self.row.device)
+        return self._ones
+
+    @property
+    def kernel_val(self) -> torch.Tensor | None:
+        return self._val
+
+    @property
+    def num_edges(self) -> int:
+        return int(self.row.numel())
+
+
+class CsrMatrix:
+    """Compressed sparse rows over destination vertices."""
+
+    __slots__ = ("num_vertices", "row_ptr", "col_idx", "_val", "_ones", "_rows", "_touched",
+                 "_off_block")
+
+    def __init__(self, num_vertices: int, row_ptr: torch.Tensor, col_idx: torch.Tensor,
+                 val: torch.Tensor | None, rows: torch.Tensor | None = None):
+        self.num_vertices = int(num_vertices)
+        self.row_ptr, self.col_idx, self._val, self._ones = row_ptr, col_idx, val, None
+        self._rows = rows
+        self._touched = None
+        self._off_block: dict[int, int] = {}
+
+    @property
+    def val(self) -> torch.Tensor:
+        if self._val is not None:
+            return self._val
+        if self._ones is None:
+            self._ones = torch.ones(self.num_edges, dtype=torch.float32,
+                                    device=self.col_idx.device)
+        return self._ones
+
+    @property
+    def kernel_val(self) -> torch.Tensor | None:
+        return self._val
+
+    @property
+    def num_edges(self) -> int:
+        return int(self.col_idx.numel())
+
+    def touched(self) -> torch.Tensor:
+        """bool[V]: row has >= 1 edge (kernels.py:121)."""
+        if self._touched is None:
+            # torch.bool is one byte holding 0/1: the kernel writes it as uint8
+            t = torch.empty(self.num_vertices, dtype=torch.bool, device=self.row_ptr.device)
+            _lib.call("ag_row_touched", self.num_vertices, _lib.ptr(self.row_ptr), _lib.ptr(t),
+                      _lib.stream())
+            self._touched = t
+        return self._touched
+
+    def first_off_block(self, block_size: int) -> int:
+        """Index of the first edge crossing a B-block boundary, or -1."""
+        if block_size not in self._off_block:
+            out = _lib.out_i64()
+            _lib.call("ag_first_off_block", self.num_vertices, _lib.ptr(self.row_ptr),
+                      _lib.ptr(self.col_idx), int(block_size), _lib.byref(out), _lib.stream())
+            self._off_block[block_size] = out.value
+        return self._off_block[block_size]
+
+    def rows(self) -> torch.Tensor:
+        """Destination of every edge (the COO row array)."""
+        if self._rows is None:
+            counts = (self.row_ptr[1:] - self.row_ptr[:-1]).to(torch.int64)
+            self._rows = torch.repeat_interleave(
+                torch.arange(self.num_vertices, dtype=torch.int32, device=self.row_ptr.device),
+                counts)
+        return self._rows
+
+
+class DenseBlockSet:
+    """Diagonal B x B blocks of an intra-community adjacency (formats.py:48-73).
+
+    Only communities with >= 1 edge are stored; `comm_slot[c]` maps every
+    community to its slot or -1 (device-side lookup for the block kernel).
+    """
+
+    __slots__ = ("num_vertices", "block_size", "community_ids", "blocks", "row_touched",
+                 "comm_slot")
+
+    def __init__(self, num_vertices, block_size, community_ids, blocks, row_touched, comm_slot):
+        self.num_vertices = int(num_vertices)
+        self.block_size = int(block_size)
+        self.community_ids = community_ids
+        self.blocks = blocks
+        self.row_touched = row_touched
+        self.comm_slot = comm_slot
+
+    def nonzero_count(self) -> int:
+        return int(torch.count_nonzero(self.blocks).item())
+
+
+def to_csr(g: Graph) -> CsrMatrix:
+    """CSR of a canonical graph (formats.py:76-88); cached on the graph."""
+    a = g._cache.get("csr")
+    if a is None:
+        row_ptr = torch.empty(g.num_vertices + 1, dtype=torch.int32, device=g.dst.device)
+        _lib.call("ag_build_row_ptr", g.num_vertices, g.num_edges, _lib.ptr(g.dst),
+                  _lib.ptr(row_ptr), _lib.stream())
+        a = CsrMatrix(g.num_vertices, row_ptr, g.src, g.weights, rows=g.dst)
+        g._cache["csr"] = a
+    return a
+
+
+def to_coo(g) -> CooMatrix:
+    """Canonical COO of a graph or of a CSR matrix (formats.py:91-102)."""
+    if isinstance(g, CsrMatrix):
+        return CooMatrix(g.num_vertices, g.rows(), g.col_idx, g.kernel_val)
+    m = g._cache.get("coo")
+    if m is None:
+        m = CooMatrix(g.num_vertices, g.dst, g.src, g.weights)
+        g._cache["coo"] = m
+    return m
+
+
+def to_dense_blocks(g: Graph, block_size: int) -> DenseBlockSet:
+    """Pack a block-local (intra) graph into dense B x B blocks (formats.py:105-140)."""
+    if block_size < 1:
+        raise ValueError("block_size must be >= 1")
+    key = ("blocks", int(block_size))
+    d = g._cache.get(key)
+    if d is not None:
+        return d
+    b = int(block_size)
+    bad = to_csr(g).first_off_block(b)
+    if bad >= 0:
+        dd = int(g.dst[bad].item())
+        ss = int(g.src[bad].item())
+        raise ValueError(f"off-diagonal edge (dst={dd}, src={ss}) "
+                         f"is not block-local for block_size={b}")
+    k = _lib.out_i64()
+    _lib.call("ag_blocks_count", g.num_vertices, g.num_edges, _lib.ptr(g.dst), b, _lib.byref(k),
+              _lib.stream())
+    k = k.value
+    dev = g.dst.device
+    ncomm = (g.num_vertices + b - 1) // b
+    community_ids = torch.empty(k, dtype=torch.int32, device=dev)
+    comm_slot = torch.empty(ncomm, dtype=torch.int32, device=dev)
+    blocks = torch.empty((k, b, b), dtype=torch.float32, device=dev)
+    touched = torch.empty((k, b), dtype=torch.bool, device=dev)
+    _lib.call("ag_blocks_fill", g.num_vertices, g.num_edges, _lib.ptr(g.dst), _lib.ptr(g.src),
+              _lib.ptr(g.weights), b, k, _lib.ptr(community_ids), _lib.ptr(comm_slot),
+              _lib.ptr(blocks), _lib.ptr(touched), _lib.stream())
+    d = DenseBlockSet(g.num_vertices, b, community_ids, blocks, touched, comm_slot)
+    g._cache[key] = d
+    return d
+
+
+def feature_matrix(data, num_vertices: int | None = None) -> torch.Tensor:
+    """Validated C-contiguous fp32 [V, F] device feature matrix."""
+    x = as_device(data, torch.float32)
+    if x.dim() != 2:
+        raise ValueError(f"features must be 2-d, got shape {tuple(x.shape)}")
+    if num_vertices is not None and x.shape[0] != num_vertices:
+        raise ValueError(f"feature rows {x.shape[0]} != num_vertices {num_vertices}")
+    if not bool(torch.isfinite(x).all()):
+        raise ValueError("features contain NaN or Inf")
+    return x
+
+
+def random_features(num_vertices: int, dim: int, seed: int = 0) -> torch.Tensor:
+    """default_rng(seed).standard_normal((V, F)).astype(f32) (formats.py:158-161)."""
+    rng = np.random.default_rng(seed)
+    return as_device(rng.standard_normal((num_vertices, dim)).astype(np.float32), torch.float32)

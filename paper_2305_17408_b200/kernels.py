@@ -1,0 +1,388 @@
+"""Density-specialised aggregation kernels (reference kernels.py:31-376).
+
+Same operator API as the reference; every kernel is a hand-written sm_100a
+kernel behind the C ABI:
+
+  csr_inter          K1 ag_csr_spmm        row-parallel CSR gather; values
+                                           bitwise equal to the reference's
+                                           np.add.reduceat order
+  csr_intra_blocked  K2 ag_csr_intra_spmm  per-community smem-staged slab
+  coo_atomic         K3 ag_coo_spmm        edge-parallel, vector atomics
+  dense_block        K4 ag_dense_block_spmm batched B x B block products
+  dense_reference    dense adjacency @ X on the device (ag_gemm_f32), V <= cap
+
+The decomposed path runs the inter role first (raw partial, or atomics into
+a zero / -inf buffer) and the intra role second with combine() fused into
+its epilogue (AG_EPI_COMBINE), so no separate merge pass or second V x F
+buffer is needed.  Outputs are fresh CUDA tensors; `threads` is accepted for
+signature compatibility and ignored.
+"""
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .decompose import DecomposedGraph
+from .errors import KernelError
+from .formats import CooMatrix, CsrMatrix, DenseBlockSet, to_coo, to_csr, to_dense_blocks
+from .graph import Graph, as_device
+
+DEFAULT_TILE_BUDGET_BYTES = 48 * 1024
+DENSE_ORACLE_CAP = 4096
+
+
+class AggregateOp(enum.Enum):
+    SUM = "sum"
+    MEAN = "mean"
+    MAX = "max"
+
+
+class KernelKind(enum.Enum):
+    CSR_INTER = "csr_inter"
+    CSR_INTRA_BLOCKED = "csr_intra_blocked"
+    COO_ATOMIC = "coo_atomic"
+    DENSE_BLOCK = "dense_block"
+    DENSE_REFERENCE = "dense_reference"
+
+
+@dataclass
+class PartialResult:
+    """One subgraph's aggregation before combination; untouched rows hold 0."""
+
+    values: torch.Tensor
+    touched: torch.Tensor
+    op: AggregateOp
+    note: str | None = None
+
+
+def _opcode(op: AggregateOp) -> int:
+    return _lib.AG_OP[op.value]
+
+
+def _check_features(num_vertices: int, x) -> torch.Tensor:
+    x = as_device(x, torch.float32)
+    if x.dim() != 2 or x.shape[0] != num_vertices:
+        raise KernelError(
+            f"feature matrix shape {tuple(x.shape)} does not match {num_vertices} vertices")
+    return x
+
+
+def empty_partial(num_vertices: int, dim: int, op: AggregateOp) -> PartialResult:
+    dev = _lib.device()
+    return PartialResult(values=torch.zeros((num_vertices, dim), dtype=torch.float32, device=dev),
+                         touched=torch.zeros(num_vertices, dtype=torch.bool, device=dev), op=op)
+
+
+# ------------------------------------------------------------ raw launches --
+def launch_csr(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp, flags: int = 0,
+               other_touched: torch.Tensor | None = None, deg: torch.Tensor | None = None,
+               gin_scale: float = 0.0) -> None:
+    _lib.call("ag_csr_spmm", a.num_vertices, x.shape[1], _lib.ptr(a.row_ptr),
+              _lib.ptr(a.col_idx), _lib.ptr(a.kernel_val), _lib.ptr(x), _lib.ptr(y),
+              _opcode(op), flags, _lib.ptr(other_touched), _lib.ptr(deg), float(gin_scale),
+              _lib.stream())
+
+
+def _check_block_local(a: CsrMatrix, block_size: int) -> None:
+    bad = a.first_off_block(block_size)
+    if bad >= 0:
+        r = int(a.rows()[bad].item())
+        c = int(a.col_idx[bad].item())
+        raise KernelError(f"off-diagonal edge (dst={r}, src={c}) for block_size={block_size}")
+
+
+def launch_csr_intra(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp,
+                     block_size: int, tile_budget_bytes: int = DEFAULT_TILE_BUDGET_BYTES,
+                     flags: int = 0, other_touched=None, deg=None, gin_scale: float = 0.0):
+    if block_size < 1:
+        raise KernelError("block_size must be >= 1")
+    _check_block_local(a, block_size)
+    _lib.call("ag_csr_intra_spmm", a.num_vertices, x.shape[1], int(block_size),
+              int(tile_budget_bytes), _lib.ptr(a.row_ptr), _lib.ptr(a.col_idx),
+              _lib.ptr(a.kernel_val), _lib.ptr(x), _lib.ptr(y), _opcode(op), flags,
+              _lib.ptr(other_touched), _lib.ptr(deg), float(gin_scale), _lib.stream())
+
+
+def launch_coo(a: CooMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp) -> None:
+    """Accumulate into y (caller initialises 0 / -inf)."""
+    _lib.call("ag_coo_spmm", a.num_vertices, x.shape[1], a.num_edges, _lib.ptr(a.row),
+              _lib.ptr(a.col), _lib.ptr(a.kernel_val), _lib.ptr(x), _lib.ptr(y), _opcode(op),
+              _lib.stream())
+
+
+def coo_init(y: torch.Tensor, op: AggregateOp) -> None:
+    y.fill_(float("-inf") if op is AggregateOp.MAX else 0.0)
+
+
+def launch_dense_block(d: DenseBlockSet, x: torch.Tensor, y: torch.Tensor, op: AggregateOp,
+                       flags: int = 0, other_touched=None, deg=None, gin_scale: float = 0.0):
+    _lib.call("ag_dense_block_spmm", d.num_vertices, x.shape[1], d.block_size,
+              _lib.ptr(d.comm_slot), _lib.ptr(d.blocks), _lib.ptr(d.row_touched), _lib.ptr(x),
+              _lib.ptr(y), _opcode(op), flags, _lib.ptr(other_touched), _lib.ptr(deg),
+              float(gin_scale), _lib.stream())
+
+
+def _coo_touched(a: CooMatrix) -> torch.Tensor:
+    t = torch.zeros(a.num_vertices, dtype=torch.bool, device=a.row.device)
+    if a.num_edges:
+        t[a.row.long()] = True
+    return t
+
+
+def _block_touched(d: DenseBlockSet) -> torch.Tensor:
+    dev = d.blocks.device
+    t = torch.zeros(d.num_vertices, dtype=torch.bool, device=dev)
+    if d.community_ids.numel():
+        idx = (d.community_ids.long()[:, None] * d.block_size
+               + torch.arange(d.block_size, device=dev)[None, :])
+        valid = idx < d.num_vertices
+        t[idx[valid]] = d.row_touched[valid]
+    return t
+
+
+# -------------------------------------------------------------- public API --
+def aggregate_csr_inter(a: CsrMatrix, x, op: AggregateOp, threads: int = 1) -> PartialResult:
+    """Row-parallel CSR aggregation (the inter-subgraph kernel), kernels.py:117-134."""
+    del threads
+    x = _check_features(a.num_vertices, x)
+    y = torch.empty((a.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
+    launch_csr(a, x, y, op)
+    return PartialResult(values=y, touched=a.touched().clone(), op=op)
+
+
+def aggregate_csr_intra_blocked(a: CsrMatrix, x, op: AggregateOp, block_size: int,
+                                tile_budget_bytes: int = DEFAULT_TILE_BUDGET_BYTES,
+                                threads: int = 1) -> PartialResult:
+    """CSR aggregation with per-community smem staging, kernels.py:137-189.
+
+    Bitwise identical to aggregate_csr_inter for any tile budget.
+    """
+    del threads
+    if block_size < 1:
+        raise KernelError("block_size must be >= 1")
+    x = _check_features(a.num_vertices, x)
+    y = torch.empty((a.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
+    launch_csr_intra(a, x, y, op, block_size, tile_budget_bytes)
+    return PartialResult(values=y, touched=a.touched().clone(), op=op)
+
+
+def aggregate_coo_atomic(a: CooMatrix, x, op: AggregateOp) -> PartialResult:
+    """Edge-parallel aggregation with atomic accumulation, kernels.py:192-225."""
+    x = _check_features(a.num_vertices, x)
+    y = torch.empty((a.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
+    coo_init(y, op)
+    launch_coo(a, x, y, op)
+    touched = _coo_touched(a)
+    note = None
+    if op is AggregateOp.MAX:
+        note = "max via atomic compare-exchange emulation"
+        y.masked_fill_(~touched[:, None], 0.0)
+    return PartialResult(values=y, touched=touched, op=op, note=note)
+
+
+def aggregate_dense_block(d: DenseBlockSet, x, op: AggregateOp) -> PartialResult:
+    """Batched dense products over diagonal blocks, kernels.py:228-250 (no max)."""
+    if op is AggregateOp.MAX:
+        raise KernelError("dense_block kernel does not support max aggregation")
+    x = _check_features(d.num_vertices, x)
+    y = torch.empty((d.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
+    launch_dense_block(d, x, y, op)
+    return PartialResult(values=y, touched=_block_touched(d), op=op)
+
+
+def combine(intra: PartialResult, inter: PartialResult, op: AggregateOp,
+            full_in_degree=None) -> torch.Tensor:
+    """Merge intra and inter partial results, kernels.py:253-276."""
+    if intra.op is not op or inter.op is not op:
+        raise KernelError(f"op mismatch: combine({intra.op}, {inter.op}) as {op}")
+    if intra.values.shape != inter.values.shape:
+        raise KernelError("partial result shapes differ")
+    deg = None
+    if op is AggregateOp.MEAN:
+        if full_in_degree is None:
+            raise KernelError("mean combine requires the full-graph degree vector")
+        deg = as_device(full_in_degree, torch.int64)
+    a = as_device(intra.values, torch.float32)
+    b = as_device(inter.values, torch.float32)
+    ta = as_device(intra.touched, torch.bool) if op is AggregateOp.MAX else None
+    tb = as_device(inter.touched, torch.bool) if op is AggregateOp.MAX else None
+    out = torch.empty_like(a)
+    _lib.call("ag_combine", a.shape[0], a.shape[1], _lib.ptr(a), _lib.ptr(ta), _lib.ptr(b),
+              _lib.ptr(tb), _lib.ptr(deg), _opcode(op), _lib.ptr(out), _lib.stream())
+    return out
+
+
+def dense_adjacency(g: Graph) -> torch.Tensor:
+    """V x V fp32 adjacency on the device."""
+    a = torch.zeros((g.num_vertices, g.num_vertices), dtype=torch.float32, device=g.dst.device)
+    if g.num_edges:
+        a[g.dst.long(), g.src.long()] = g.edge_weights()
+    return a
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
+         trans_a: bool = False, trans_b: bool = False, alpha: float = 1.0, beta: float = 0.0,
+         relu: bool = False) -> torch.Tensor:
+    """out = alpha * op(a) @ op(b) + beta * out on the hand-written fp32 GEMM."""
+    M = a.shape[1] if trans_a else a.shape[0]
+    K = a.shape[0] if trans_a else a.shape[1]
+    N = b.shape[0] if trans_b else b.shape[1]
+    Kb = b.shape[1] if trans_b else b.shape[0]
+    if K != Kb:
+        raise KernelError(f"gemm inner dimensions differ: {K} vs {Kb}")
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=a.device)
+    _lib.call("ag_gemm_f32", M, N, K, _lib.ptr(a), a.stride(0), int(trans_a), _lib.ptr(b),
+              b.stride(0), int(trans_b), _lib.ptr(out), out.stride(0), float(alpha), float(beta),
+              _lib.AG_GEMM_RELU if relu else 0, _lib.stream())
+    return out
+
+
+def aggregate_dense_reference(g: Graph, x, op: AggregateOp,
+                              cap: int = DENSE_ORACLE_CAP) -> torch.Tensor:
+    """Dense-adjacency aggregation on the device (kernels.py:286-306), V <= cap."""
+    if g.num_vertices > cap:
+        raise KernelError(f"dense oracle capped at {cap} vertices, got {g.num_vertices}")
+    x = _check_features(g.num_vertices, x)
+    if op is AggregateOp.MAX:
+        y = torch.zeros((g.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
+        launch_csr(to_csr(g), x, y, op, flags=_lib.AG_EPI_COMBINE)
+        return y
+    out = gemm(dense_adjacency(g), x)
+    if op is AggregateOp.MEAN:
+        zeros = torch.zeros_like(out)
+        _lib.call("ag_combine", out.shape[0], out.shape[1], _lib.ptr(out), None, _lib.ptr(zeros),
+                  None, _lib.ptr(g.in_degrees()), _opcode(op), _lib.ptr(out), _lib.stream())
+    return out
+
+
+def backward_sum(g_transposed: Graph, d_y, threads: int = 1) -> torch.Tensor:
+    """dX = A^T dY: sum-aggregation over the edge-reversed graph (kernels.py:309-313)."""
+    return aggregate_csr_inter(to_csr(g_transposed), d_y, AggregateOp.SUM, threads).values
+
+
+@dataclass
+class SubgraphExec:
+    """Pre-built device formats of one subgraph, reused across iterations."""
+
+    graph: Graph
+    block_size: int
+    csr: CsrMatrix
+    coo: CooMatrix
+    blocks: DenseBlockSet | None = None
+
+    @classmethod
+    def for_intra(cls, g: Graph, block_size: int) -> "SubgraphExec":
+        return cls(graph=g, block_size=block_size, csr=to_csr(g), coo=to_coo(g),
+                   blocks=to_dense_blocks(g, block_size))
+
+    @classmethod
+    def for_inter(cls, g: Graph, block_size: int) -> "SubgraphExec":
+        return cls(graph=g, block_size=block_size, csr=to_csr(g), coo=to_coo(g))
+
+    def run(self, kind: KernelKind, x, op: AggregateOp,
+            tile_budget_bytes: int = DEFAULT_TILE_BUDGET_BYTES, threads: int = 1) -> PartialResult:
+        if kind is KernelKind.CSR_INTER:
+            return aggregate_csr_inter(self.csr, x, op)
+        if kind is KernelKind.CSR_INTRA_BLOCKED:
+            return aggregate_csr_intra_blocked(self.csr, x, op, self.block_size,
+                                               tile_budget_bytes=tile_budget_bytes)
+        if kind is KernelKind.COO_ATOMIC:
+            return aggregate_coo_atomic(self.coo, x, op)
+        if kind is KernelKind.DENSE_BLOCK:
+            if self.blocks is None:
+                raise KernelError("dense_block kernel requires an intra subgraph")
+            return aggregate_dense_block(self.blocks, x, op)
+        if kind is KernelKind.DENSE_REFERENCE:
+            values = aggregate_dense_reference(self.graph, x, op)
+            return PartialResult(values=values, touched=self.csr.touched().clone(), op=op)
+        raise KernelError(f"unknown kernel {kind}")
+
+    # ---- fused two-role execution (used by the decomposed path) ----------
+    def run_raw_into(self, kind: KernelKind, x: torch.Tensor, y: torch.Tensor,
+                     op: AggregateOp, tile_budget_bytes: int) -> None:
+        """First role: write this subgraph's raw partial into y.
+
+        COO leaves untouched max rows at -inf; the second role's epilogue only
+        reads y where this subgraph's `touched` is set.
+        """
+        if kind is KernelKind.CSR_INTER:
+            launch_csr(self.csr, x, y, op)
+        elif kind is KernelKind.COO_ATOMIC:
+            coo_init(y, op)
+            launch_coo(self.coo, x, y, op)
+        else:
+            y.copy_(self.run(kind, x, op, tile_budget_bytes).values)
+
+    def run_combine_into(self, kind: KernelKind, x: torch.Tensor, y: torch.Tensor,
+                         op: AggregateOp, other_touched: torch.Tensor, deg: torch.Tensor,
+                         tile_budget_bytes: int, gin_scale: float | None = None) -> None:
+        """Second role: y = combine(this, y) [+ gin_scale * x], fused when possible."""
+        flags = _lib.AG_EPI_COMBINE | (_lib.AG_EPI_GIN if gin_scale is not None else 0)
+        g = 0.0 if gin_scale is None else gin_scale
+        if kind is KernelKind.CSR_INTRA_BLOCKED:
+            launch_csr_intra(self.csr, x, y, op, self.block_size, tile_budget_bytes, flags,
+                             other_touched, deg, g)
+        elif kind is KernelKind.CSR_INTER:
+            launch_csr(self.csr, x, y, op, flags, other_touched, deg, g)
+        elif kind is KernelKind.DENSE_BLOCK:
+            if self.blocks is None:
+                raise KernelError("dense_block kernel requires an intra subgraph")
+            if op is AggregateOp.MAX:
+                raise KernelError("dense_block kernel does not support max aggregation")
+            launch_dense_block(self.blocks, x, y, op, flags, other_touched, deg, g)
+        else:
+            mine = self.run(kind, x, op, tile_budget_bytes)
+            other = PartialResult(values=y, touched=other_touched, op=op)
+            y.copy_(combine(mine, other, op, full_in_degree=deg))
+            if gin_scale is not None:
+                y.copy_(np.float32(gin_scale) * x + y)
+
+
+def decomposed_execs(d: DecomposedGraph) -> tuple[SubgraphExec, SubgraphExec]:
+    """Formats of both roles, built once per DecomposedGraph and cached."""
+    ex = d._cache.get("execs")
+    if ex is None:
+        ex = (SubgraphExec.for_intra(d.intra, d.block_size),
+              SubgraphExec.for_inter(d.inter, d.block_size))
+        d._cache["execs"] = ex
+    return ex
+
+
+def aggregate_full(g: Graph, x, op: AggregateOp, kernel: KernelKind = KernelKind.CSR_INTER,
+                   threads: int = 1) -> torch.Tensor:
+    """One kernel over the full graph, finalised as combine(partial, empty)."""
+    del threads
+    x = _check_features(g.num_vertices, x)
+    if kernel is KernelKind.CSR_INTER:
+        y = torch.zeros((g.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
+        launch_csr(to_csr(g), x, y, op, _lib.AG_EPI_COMBINE, None, g.in_degrees())
+        return y
+    ex = SubgraphExec.for_inter(g, block_size=max(g.num_vertices, 1))
+    partial = ex.run(kernel, x, op)
+    other = empty_partial(g.num_vertices, x.shape[1], op)
+    return combine(partial, other, op, full_in_degree=g.in_degrees())
+
+
+def aggregate_decomposed(d: DecomposedGraph, x, op: AggregateOp,
+                         kernel_intra: KernelKind = KernelKind.CSR_INTRA_BLOCKED,
+                         kernel_inter: KernelKind = KernelKind.COO_ATOMIC,
+                         tile_budget_bytes: int = DEFAULT_TILE_BUDGET_BYTES,
+                         threads: int = 1, gin_scale: float | None = None) -> torch.Tensor:
+    """Aggregate a decomposed graph with one kernel per role (kernels.py:365-376).
+
+    The inter kernel writes its raw partial, the intra kernel combines into
+    it in its epilogue (and adds gin_scale * x when given, models.py:111).
+    """
+    del threads
+    x = _check_features(d.num_vertices, x)
+    intra, inter = decomposed_execs(d)
+    y = torch.empty((d.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
+    inter.run_raw_into(kernel_inter, x, y, op, tile_budget_bytes)
+    intra.run_combine_into(kernel_intra, x, y, op, inter.csr.touched(), d.full_in_degree,
+                           tile_budget_bytes, gin_scale)
+    return y

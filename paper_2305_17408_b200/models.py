@@ -1,0 +1,313 @@
+"""GCN / GIN layers and the composed training step (reference models.py:25-112).
+
+Forward entry points keep the reference signatures: (A_hat X) W for GCN and
+((1+eps) X + A X) W for GIN, aggregation first at the input width.  The
+backward entry points (`gcn_layer_backward`, `gin_layer_backward`) and the
+multi-layer `GNN` with its loss / SGD step are the builder-defined
+composition of SURVEY.md §8c (the reference has forward layers only):
+
+  GCN  H_{l+1} = ReLU((A_hat H_l) W_l)          (no ReLU after the last layer)
+  GIN  H_{l+1} = ReLU(((1+eps) H_l + A H_l) W_l)
+  loss = mean softmax cross-entropy over the train mask
+  dW_l = agg_l^T G_l ;  dH_l = A_hat^T (G_l W_l^T) [+ (1+eps) G_l W_l^T for GIN]
+
+Every product is a hand-written kernel: aggregation through the decomposed
+(or full CSR) kernels, the update through ag_gemm_f32 with the ReLU fused
+into its epilogue, the (1+eps) X term fused into the aggregation epilogue.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .decompose import DecomposedGraph, decompose
+from .graph import Graph, as_device
+from .kernels import (
+    DEFAULT_TILE_BUDGET_BYTES,
+    AggregateOp,
+    KernelKind,
+    _check_features,
+    aggregate_decomposed,
+    aggregate_full,
+    gemm,
+)
+
+MODELS = ("gcn", "gin", "agg_only")
+
+
+@dataclass(frozen=True)
+class LayerParams:
+    model: str
+    in_dim: int
+    out_dim: int
+    weight: np.ndarray | None
+    gin_eps: float = 0.0
+
+    def __post_init__(self):
+        if self.model not in MODELS:
+            raise ValueError(f"unknown model {self.model!r}")
+        if self.weight is not None:
+            if self.weight.shape != (self.in_dim, self.out_dim):
+                raise ValueError(
+                    f"weight shape {self.weight.shape} != ({self.in_dim}, {self.out_dim})")
+            self.weight.setflags(write=False)
+
+    @classmethod
+    def seeded(cls, model: str, in_dim: int, out_dim: int, seed: int = 0,
+               gin_eps: float = 0.0) -> "LayerParams":
+        """W = default_rng(seed).uniform(-0.1, 0.1, (in, out)).astype(f32) (models.py:46-54)."""
+        if model == "agg_only":
+            return cls(model=model, in_dim=in_dim, out_dim=in_dim, weight=None)
+        rng = np.random.default_rng(seed)
+        w = rng.uniform(-0.1, 0.1, size=(in_dim, out_dim)).astype(np.float32)
+        return cls(model=model, in_dim=in_dim, out_dim=out_dim, weight=w, gin_eps=gin_eps)
+
+    def gin_scale(self) -> float:
+        """np.float32(1.0 + eps) as used by models.py:111."""
+        return float(np.float32(1.0 + self.gin_eps))
+
+
+def gcn_normalize(g: Graph) -> Graph:
+    """A + I with w = 1/sqrt(deg(d) deg(s)) from in-degrees of A+I (models.py:57-73)."""
+    E, V = g.num_edges, g.num_vertices
+    dev = _lib.device()
+    dst = torch.empty(E + V, dtype=torch.int32, device=dev)
+    src = torch.empty(E + V, dtype=torch.int32, device=dev)
+    w = torch.empty(E + V, dtype=torch.float32, device=dev)
+    nu = _lib.out_i64()
+    _lib.call("ag_gcn_normalize", V, E, _lib.ptr(g.dst), _lib.ptr(g.src), _lib.ptr(dst),
+              _lib.ptr(src), _lib.ptr(w), _lib.byref(nu), _lib.stream())
+    n = nu.value
+    if n != E + V:
+        dst, src, w = dst[:n].clone(), src[:n].clone(), w[:n].clone()
+    return Graph(num_vertices=V, dst=dst, src=src, weights=w)
+
+
+def _aggregate(subject, x, op: AggregateOp, *, kernel_intra, kernel_inter,
+               gin_scale: float | None = None,
+               tile_budget_bytes: int = DEFAULT_TILE_BUDGET_BYTES) -> torch.Tensor:
+    if isinstance(subject, DecomposedGraph):
+        return aggregate_decomposed(subject, x, op, kernel_intra=kernel_intra,
+                                    kernel_inter=kernel_inter,
+                                    tile_budget_bytes=tile_budget_bytes, gin_scale=gin_scale)
+    if isinstance(subject, Graph):
+        agg = aggregate_full(subject, x, op)
+        if gin_scale is not None:
+            x = _check_features(subject.num_vertices, x)
+            agg = np.float32(gin_scale) * x + agg
+        return agg
+    raise TypeError(f"expected Graph or DecomposedGraph, got {type(subject)!r}")
+
+
+def _weight(params: LayerParams) -> torch.Tensor:
+    return as_device(params.weight, torch.float32)
+
+
+def gcn_layer_forward(subject, x, params: LayerParams,
+                      kernel_intra: KernelKind = KernelKind.CSR_INTRA_BLOCKED,
+                      kernel_inter: KernelKind = KernelKind.COO_ATOMIC,
+                      threads: int = 1) -> torch.Tensor:
+    """One GCN layer: (normalized-A @ X) @ W (models.py:86-99)."""
+    del threads
+    if params.model != "gcn":
+        raise ValueError(f"gcn_layer_forward called with model {params.model!r}")
+    agg = _aggregate(subject, x, AggregateOp.SUM, kernel_intra=kernel_intra,
+                     kernel_inter=kernel_inter)
+    return gemm(agg, _weight(params))
+
+
+def gin_layer_forward(subject, x, params: LayerParams,
+                      kernel_intra: KernelKind = KernelKind.CSR_INTRA_BLOCKED,
+                      kernel_inter: KernelKind = KernelKind.COO_ATOMIC,
+                      threads: int = 1) -> torch.Tensor:
+    """One GIN layer: ((1 + eps) * X + A @ X) @ W (models.py:102-112)."""
+    del threads
+    if params.model != "gin":
+        raise ValueError(f"gin_layer_forward called with model {params.model!r}")
+    h = _aggregate(subject, x, AggregateOp.SUM, kernel_intra=kernel_intra,
+                   kernel_inter=kernel_inter, gin_scale=params.gin_scale())
+    return gemm(h, _weight(params))
+
+
+def gcn_layer_backward(subject_t, x, agg, params: LayerParams, d_out,
+                       kernel_intra: KernelKind = KernelKind.CSR_INTRA_BLOCKED,
+                       kernel_inter: KernelKind = KernelKind.CSR_INTER,
+                       need_dx: bool = True):
+    """Gradients of out = (A_hat X) W: returns (d_x, d_w).
+
+    subject_t is the transposed topology (Graph.reverse(), optionally
+    decomposed).  d_w = agg^T d_out;  d_x = A_hat^T (d_out W^T)
+    (backward_sum, kernels.py:309-313, applied to d_out W^T).
+    """
+    agg = as_device(agg, torch.float32)
+    d_out = as_device(d_out, torch.float32)
+    w = _weight(params)
+    d_w = gemm(agg, d_out, trans_a=True)
+    if not need_dx:
+        return None, d_w
+    d_agg = gemm(d_out, w, trans_b=True)
+    d_x = _aggregate(subject_t, d_agg, AggregateOp.SUM, kernel_intra=kernel_intra,
+                     kernel_inter=kernel_inter)
+    return d_x, d_w
+
+
+def gin_layer_backward(subject_t, x, h, params: LayerParams, d_out,
+                       kernel_intra: KernelKind = KernelKind.CSR_INTRA_BLOCKED,
+                       kernel_inter: KernelKind = KernelKind.CSR_INTER,
+                       need_dx: bool = True):
+    """Gradients of out = ((1+eps) X + A X) W: returns (d_x, d_w).
+
+    d_w = h^T d_out;  d_x = (1+eps) d_h + A^T d_h with d_h = d_out W^T, the
+    (1+eps) term fused into the transposed aggregation's epilogue.
+    """
+    h = as_device(h, torch.float32)
+    d_out = as_device(d_out, torch.float32)
+    w = _weight(params)
+    d_w = gemm(h, d_out, trans_a=True)
+    if not need_dx:
+        return None, d_w
+    d_h = gemm(d_out, w, trans_b=True)
+    d_x = _aggregate(subject_t, d_h, AggregateOp.SUM, kernel_intra=kernel_intra,
+                     kernel_inter=kernel_inter, gin_scale=params.gin_scale())
+    return d_x, d_w
+
+
+@dataclass
+class GNN:
+    """Multi-layer GCN / GIN over a decomposed (reordered) graph.
+
+    `subject` is the decomposed forward topology, `subject_t` the decomposed
+    transpose (built once).  `kernels[(direction, F)] = (intra, inter)` holds
+    the per-width kernel pair; `autotune` fills it with the adaptive selector.
+    """
+
+    model: str
+    dims: list
+    subject: DecomposedGraph
+    subject_t: DecomposedGraph
+    weights: list = field(default_factory=list)
+    gin_eps: float = 0.0
+    kernels: dict = field(default_factory=dict)
+    default_pair: tuple = (KernelKind.CSR_INTRA_BLOCKED, KernelKind.CSR_INTER)
+    # when a list, every aggregation appends (start_event, end_event, F, subject)
+    events: list | None = None
+
+    @classmethod
+    def build(cls, model: str, dims, subject: DecomposedGraph, seed: int = 0,
+              gin_eps: float = 0.0, subject_t: DecomposedGraph | None = None) -> "GNN":
+        if model not in ("gcn", "gin"):
+            raise ValueError(f"unknown model {model!r}")
+        if subject_t is None:
+            full = _reassemble(subject)
+            subject_t = decompose(full.reverse(), subject.block_size)
+        ws = [as_device(LayerParams.seeded(model, dims[i], dims[i + 1], seed=seed + i,
+                                           gin_eps=gin_eps).weight, torch.float32).clone()
+              for i in range(len(dims) - 1)]
+        return cls(model=model, dims=list(dims), subject=subject, subject_t=subject_t,
+                   weights=ws, gin_eps=gin_eps)
+
+    @property
+    def num_layers(self) -> int:
+        return len(self.dims) - 1
+
+    def pair(self, direction: str, feat: int) -> tuple:
+        return self.kernels.get((direction, feat), self.default_pair)
+
+    def gin_scale(self) -> float | None:
+        return float(np.float32(1.0 + self.gin_eps)) if self.model == "gin" else None
+
+    def autotune(self, profile_iters: int = 3) -> dict:
+        """Run the adaptive selector once per (direction, width); cache the pairs."""
+        from .selector import SelectorState, run_training_loop
+        for direction, subj in (("fwd", self.subject), ("bwd", self.subject_t)):
+            widths = self.dims[:-1] if direction == "fwd" else self.dims[1:-1]
+            for f in sorted(set(widths)):
+                if (direction, f) in self.kernels:
+                    continue
+                x = torch.randn((subj.num_vertices, f), device=_lib.device())
+                s = SelectorState.fresh(AggregateOp.SUM, profile_iters_per_candidate=profile_iters)
+                _, s, _ = run_training_loop(subj, x, AggregateOp.SUM, s.total_profiling_iters, s)
+                self.kernels[(direction, f)] = (s.choice_intra, s.choice_inter)
+        return dict(self.kernels)
+
+    def _aggregate(self, subj: DecomposedGraph, h: torch.Tensor, direction: str):
+        ki, ke = self.pair(direction, h.shape[1])
+        if self.events is None:
+            return aggregate_decomposed(subj, h, AggregateOp.SUM, kernel_intra=ki,
+                                        kernel_inter=ke, gin_scale=self.gin_scale())
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = aggregate_decomposed(subj, h, AggregateOp.SUM, kernel_intra=ki, kernel_inter=ke,
+                                   gin_scale=self.gin_scale())
+        e1.record()
+        self.events.append((e0, e1, h.shape[1], subj))
+        return out
+
+    def forward(self, x: torch.Tensor):
+        """Returns (logits, saved) with saved = per-layer (agg/h input, output)."""
+        saved = []
+        h = x
+        for l in range(self.num_layers):
+            agg = self._aggregate(self.subject, h, "fwd")
+            last = l == self.num_layers - 1
+            out = gemm(agg, self.weights[l], relu=not last)
+            saved.append((agg, out))
+            h = out
+        return h, saved
+
+    def backward(self, saved, d_logits: torch.Tensor):
+        """Returns the list of dW (layer order)."""
+        grads = [None] * self.num_layers
+        g = d_logits
+        for l in range(self.num_layers - 1, -1, -1):
+            agg, _ = saved[l]
+            grads[l] = gemm(agg, g, trans_a=True)
+            if l == 0:
+                break
+            d_in = gemm(g, self.weights[l], trans_b=True)
+            d_h = self._aggregate(self.subject_t, d_in, "bwd")
+            _, h_prev = saved[l - 1]
+            _lib.call("ag_relu_backward", d_h.numel(), _lib.ptr(h_prev), _lib.ptr(d_h),
+                      _lib.stream())
+            g = d_h
+        return grads
+
+    def loss_and_grad(self, logits, labels, mask, num_masked: int):
+        loss = torch.empty(1, dtype=torch.float32, device=logits.device)
+        d_logits = torch.empty_like(logits)
+        _lib.call("ag_softmax_xent", logits.shape[0], logits.shape[1], _lib.ptr(logits),
+                  _lib.ptr(labels), _lib.ptr(mask), int(num_masked), _lib.ptr(loss),
+                  _lib.ptr(d_logits), _lib.stream())
+        return loss, d_logits
+
+    def sgd(self, grads, lr: float) -> None:
+        for w, dw in zip(self.weights, grads):
+            _lib.call("ag_sgd_step", w.numel(), _lib.ptr(w), _lib.ptr(dw), float(lr),
+                      _lib.stream())
+
+    def train_step(self, x, labels, mask, num_masked: int, lr: float = 0.01):
+        """One epoch: forward, loss, backward, SGD.  Returns (loss tensor, grads)."""
+        logits, saved = self.forward(x)
+        loss, d_logits = self.loss_and_grad(logits, labels, mask, num_masked)
+        grads = self.backward(saved, d_logits)
+        self.sgd(grads, lr)
+        return loss, grads
+
+
+def _reassemble(d: DecomposedGraph) -> Graph:
+    """The full (reordered) graph of a decomposition (union of both halves)."""
+    full = d._cache.get("full")
+    if full is None:
+        dst = torch.cat([d.intra.dst, d.inter.dst]).to(torch.int64)
+        src = torch.cat([d.intra.src, d.inter.src]).to(torch.int64)
+        w = None
+        if d.intra.weights is not None:
+            w = torch.cat([d.intra.weights, d.inter.weights])
+        from .graph import _canonical
+        full = _canonical(d.num_vertices, dst, src, w)
+        d._cache["full"] = full
+    return full
