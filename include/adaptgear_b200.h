@@ -48,9 +48,13 @@ extern "C" {
  *   exactly as kernels.py:253-276 does (sum: a+b; mean: (a+b)/f32(max(deg,1));
  *   max: touched-aware).  Without it the kernel stores the raw partial (rows
  *   with no edges get 0, kernels.py:123).
- * AG_EPI_GIN: additionally y = f32(gin_scale) * x + y  (models.py:111). */
+ * AG_EPI_GIN: additionally y = f32(gin_scale) * x + y  (models.py:111).
+ * AG_EPI_EMPTY_OTHER (with COMBINE, ag_fused_spmm only): the other partial is
+ *   the empty one (zeros, untouched) -- combine(partial, empty_partial) of
+ *   aggregate_full (kernels.py:355-362) without reading y. */
 #define AG_EPI_COMBINE 1
 #define AG_EPI_GIN 2
+#define AG_EPI_EMPTY_OTHER 4
 
 int ag_abi_version(void);
 const char *ag_last_error(void);
@@ -167,6 +171,47 @@ int ag_dense_block_spmm(int64_t num_rows, int64_t feat, int64_t block_size,
                         int32_t op, int32_t epi_flags,
                         const uint8_t *other_touched, const int64_t *deg,
                         float gin_scale, void *stream);
+
+/* Stage-aligned CSR ("SA-CSR"), the layout of the fused aggregation kernel,
+ * built once per (topology, B, role_mask).  Every row's edges are listed in
+ * role order -- the intra run (cols in [floor(r/B)B, +B)), then the inter
+ * edges (prefix ++ suffix of the sorted row) -- and cut into 9-slot stages
+ * aligned with numpy's pairwise reduction: slot 0 = a role's first term
+ * (first stage of the role only), slots 1..8 = one 8-wide accumulator group;
+ * empty slots hold col -1.  count: counts[2r..2r+1] = items of the (intra,
+ * inter) role with role_mask applied, stage_ptr[V+1] = first stage of each
+ * row (exclusive scan), *num_stages_host = total.  fill: stage_col /
+ * stage_val [num_stages * 9] (val NULL -> 1.0).  block_size 0 = no split
+ * (role_mask must be 2: the whole row is one role). */
+int ag_stage_layout_count(int64_t num_rows, const int32_t *row_ptr,
+                          const int32_t *col_idx, int64_t block_size,
+                          int32_t role_mask, int32_t *stage_ptr, int32_t *counts,
+                          int64_t *num_stages_host, void *stream);
+int ag_stage_layout_fill(int64_t num_rows, const int32_t *row_ptr,
+                         const int32_t *col_idx, const float *val,
+                         int64_t block_size, const int32_t *stage_ptr,
+                         const int32_t *counts, int32_t *stage_col,
+                         float *stage_val, void *stream);
+
+/* Fused decomposed aggregation (one launch) over the full reordered CSR and
+ * its SA-CSR layout: for every row, I = intra-role value and O = inter-role
+ * value, each in the reference's reduceat order, then
+ *   role_mask 3: y = combine(I, O) (kernels.py:253-276)   [+ gin term]
+ *   role_mask 1/2: a single role with the AG_EPI_* epilogue of ag_csr_spmm.
+ * Bitwise equal to two ag_csr_spmm launches over the intra / inter CSRs plus
+ * ag_combine, with a single output write.  Source rows are gathered by TMA
+ * (cp.async.bulk, one per row) into a per-warp shared-memory stage ring with
+ * mbarrier completion; chunks of 16 rows are scheduled dynamically.  Needs
+ * F % 4 == 0, F <= 256 and the layout; otherwise (layout pointers NULL) a
+ * register-gather kernel over the CSR computes identical values. */
+int ag_fused_spmm(int64_t num_rows, int64_t feat, int64_t block_size,
+                  int32_t role_mask, const int32_t *row_ptr,
+                  const int32_t *col_idx, const float *val,
+                  const int32_t *stage_ptr, const int32_t *counts,
+                  const int32_t *stage_col, const float *stage_val,
+                  const float *x, float *y, int32_t op, int32_t epi_flags,
+                  const uint8_t *other_touched, const int64_t *deg,
+                  float gin_scale, void *stream);
 
 /* K5 combine (kernels.py:253-276) as a standalone pass. out may alias a. */
 int ag_combine(int64_t num_rows, int64_t feat, const float *a,

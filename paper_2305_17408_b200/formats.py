@@ -48,7 +48,7 @@ class CsrMatrix:
     """Compressed sparse rows over destination vertices."""
 
     __slots__ = ("num_vertices", "row_ptr", "col_idx", "_val", "_ones", "_rows", "_touched",
-                 "_off_block")
+                 "_off_block", "_long")
 
     def __init__(self, num_vertices: int, row_ptr: torch.Tensor, col_idx: torch.Tensor,
                  val: torch.Tensor | None, rows: torch.Tensor | None = None):
@@ -57,6 +57,7 @@ class CsrMatrix:
         self._rows = rows
         self._touched = None
         self._off_block: dict[int, int] = {}
+        self._long = None
 
     @property
     def val(self) -> torch.Tensor:
@@ -93,6 +94,35 @@ class CsrMatrix:
                       _lib.ptr(self.col_idx), int(block_size), _lib.byref(out), _lib.stream())
             self._off_block[block_size] = out.value
         return self._off_block[block_size]
+
+    def stage_layout(self, block_size: int, role_mask: int):
+        """Stage-aligned CSR for the fused kernel, cached per (B, role_mask).
+
+        Returns (stage_ptr int32[V+1], counts int32[V, 2], stage_col int32[S, 9],
+        stage_val f32[S, 9]); see ag_stage_layout_* in include/adaptgear_b200.h.
+        """
+        if self._long is None:
+            self._long = {}
+        key = (int(block_size), int(role_mask))
+        lay = self._long.get(key)
+        if lay is None:
+            dev = self.row_ptr.device
+            V = self.num_vertices
+            stage_ptr = torch.empty(V + 1, dtype=torch.int32, device=dev)
+            counts = torch.empty((V, 2), dtype=torch.int32, device=dev)
+            ns = _lib.out_i64()
+            _lib.call("ag_stage_layout_count", V, _lib.ptr(self.row_ptr), _lib.ptr(self.col_idx),
+                      key[0], key[1], _lib.ptr(stage_ptr), _lib.ptr(counts), _lib.byref(ns),
+                      _lib.stream())
+            S = ns.value
+            scol = torch.empty((S, 9), dtype=torch.int32, device=dev)
+            sval = torch.empty((S, 9), dtype=torch.float32, device=dev)
+            _lib.call("ag_stage_layout_fill", V, _lib.ptr(self.row_ptr), _lib.ptr(self.col_idx),
+                      _lib.ptr(self._val), key[0], _lib.ptr(stage_ptr), _lib.ptr(counts),
+                      _lib.ptr(scol), _lib.ptr(sval), _lib.stream())
+            lay = (stage_ptr, counts, scol, sval)
+            self._long[key] = lay
+        return lay
 
     def rows(self) -> torch.Tensor:
         """Destination of every edge (the COO row array)."""

@@ -3,18 +3,22 @@
 Same operator API as the reference; every kernel is a hand-written sm_100a
 kernel behind the C ABI:
 
-  csr_inter          K1 ag_csr_spmm        row-parallel CSR gather; values
-                                           bitwise equal to the reference's
-                                           np.add.reduceat order
-  csr_intra_blocked  K2 ag_csr_intra_spmm  per-community smem-staged slab
-  coo_atomic         K3 ag_coo_spmm        edge-parallel, vector atomics
-  dense_block        K4 ag_dense_block_spmm batched B x B block products
+  csr_inter          ag_fused_spmm          TMA-ring row gather, values bitwise
+                                            equal to the reference's
+                                            np.add.reduceat order
+  csr_intra_blocked  ag_csr_intra_spmm      per-community smem-staged slab (the
+                                            public call, honouring the tile
+                                            budget); ag_fused_spmm inside the
+                                            decomposed runtime (same bits)
+  coo_atomic         ag_coo_spmm            edge-parallel, vector atomics
+  dense_block        ag_dense_block_spmm    batched B x B block products
   dense_reference    dense adjacency @ X on the device (ag_gemm_f32), V <= cap
 
-The decomposed path runs the inter role first (raw partial, or atomics into
-a zero / -inf buffer) and the intra role second with combine() fused into
-its epilogue (AG_EPI_COMBINE), so no separate merge pass or second V x F
-buffer is needed.  Outputs are fresh CUDA tensors; `threads` is accepted for
+The decomposed path with a CSR x CSR pair is ONE launch of ag_fused_spmm over
+the full reordered CSR: both role sums in the reference's order and
+combine() in the epilogue, one output write.  Other pairs run the inter role
+first (raw partial, or atomics into a zero / -inf buffer) and the intra role
+second with combine() fused into its epilogue (AG_EPI_COMBINE).  Outputs are fresh CUDA tensors; `threads` is accepted for
 signature compatibility and ignored.
 """
 from __future__ import annotations
@@ -26,7 +30,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .decompose import DecomposedGraph
+from .decompose import DecomposedGraph, full_graph
 from .errors import KernelError
 from .formats import CooMatrix, CsrMatrix, DenseBlockSet, to_coo, to_csr, to_dense_blocks
 from .graph import Graph, as_device
@@ -83,6 +87,23 @@ def launch_csr(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp, 
                gin_scale: float = 0.0) -> None:
     _lib.call("ag_csr_spmm", a.num_vertices, x.shape[1], _lib.ptr(a.row_ptr),
               _lib.ptr(a.col_idx), _lib.ptr(a.kernel_val), _lib.ptr(x), _lib.ptr(y),
+              _opcode(op), flags, _lib.ptr(other_touched), _lib.ptr(deg), float(gin_scale),
+              _lib.stream())
+
+
+def launch_fused(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp,
+                 block: int = 0, mask: int = 2, flags: int = 0,
+                 other_touched: torch.Tensor | None = None, deg: torch.Tensor | None = None,
+                 gin_scale: float = 0.0) -> None:
+    """ag_fused_spmm: TMA-ring gather + reduceat-order reduction (+ role split)."""
+    F = x.shape[1]
+    if F % 4 == 0 and F <= 256:
+        sp, cnt, scol, sval = a.stage_layout(block, mask)
+    else:  # the register-gather path needs only the CSR
+        sp = cnt = scol = sval = None
+    _lib.call("ag_fused_spmm", a.num_vertices, F, int(block), int(mask),
+              _lib.ptr(a.row_ptr), _lib.ptr(a.col_idx), _lib.ptr(a.kernel_val), _lib.ptr(sp),
+              _lib.ptr(cnt), _lib.ptr(scol), _lib.ptr(sval), _lib.ptr(x), _lib.ptr(y),
               _opcode(op), flags, _lib.ptr(other_touched), _lib.ptr(deg), float(gin_scale),
               _lib.stream())
 
@@ -150,7 +171,7 @@ def aggregate_csr_inter(a: CsrMatrix, x, op: AggregateOp, threads: int = 1) -> P
     del threads
     x = _check_features(a.num_vertices, x)
     y = torch.empty((a.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
-    launch_csr(a, x, y, op)
+    launch_fused(a, x, y, op)
     return PartialResult(values=y, touched=a.touched().clone(), op=op)
 
 
@@ -310,8 +331,8 @@ class SubgraphExec:
         COO leaves untouched max rows at -inf; the second role's epilogue only
         reads y where this subgraph's `touched` is set.
         """
-        if kind is KernelKind.CSR_INTER:
-            launch_csr(self.csr, x, y, op)
+        if kind in (KernelKind.CSR_INTER, KernelKind.CSR_INTRA_BLOCKED):
+            launch_fused(self.csr, x, y, op)
         elif kind is KernelKind.COO_ATOMIC:
             coo_init(y, op)
             launch_coo(self.coo, x, y, op)
@@ -324,11 +345,11 @@ class SubgraphExec:
         """Second role: y = combine(this, y) [+ gin_scale * x], fused when possible."""
         flags = _lib.AG_EPI_COMBINE | (_lib.AG_EPI_GIN if gin_scale is not None else 0)
         g = 0.0 if gin_scale is None else gin_scale
-        if kind is KernelKind.CSR_INTRA_BLOCKED:
-            launch_csr_intra(self.csr, x, y, op, self.block_size, tile_budget_bytes, flags,
-                             other_touched, deg, g)
-        elif kind is KernelKind.CSR_INTER:
-            launch_csr(self.csr, x, y, op, flags, other_touched, deg, g)
+        if kind in (KernelKind.CSR_INTRA_BLOCKED, KernelKind.CSR_INTER):
+            if kind is KernelKind.CSR_INTRA_BLOCKED:
+                _check_block_local(self.csr, self.block_size)
+            launch_fused(self.csr, x, y, op, flags=flags, other_touched=other_touched, deg=deg,
+                         gin_scale=g)
         elif kind is KernelKind.DENSE_BLOCK:
             if self.blocks is None:
                 raise KernelError("dense_block kernel requires an intra subgraph")
@@ -353,14 +374,32 @@ def decomposed_execs(d: DecomposedGraph) -> tuple[SubgraphExec, SubgraphExec]:
     return ex
 
 
+CSR_KINDS = (KernelKind.CSR_INTRA_BLOCKED, KernelKind.CSR_INTER)
+
+
+def fusable(kernel_intra: KernelKind, kernel_inter: KernelKind) -> bool:
+    """A CSR x CSR pair runs as ONE fused launch over the full CSR (same bits)."""
+    return kernel_intra in CSR_KINDS and kernel_inter is KernelKind.CSR_INTER
+
+
+def run_fused_pair(d: DecomposedGraph, x: torch.Tensor, y: torch.Tensor, op: AggregateOp,
+                   gin_scale: float | None = None) -> None:
+    """y = combine(intra, inter) [+ gin] in one pass over the full reordered CSR."""
+    full = full_graph(d)
+    flags = _lib.AG_EPI_GIN if gin_scale is not None else 0
+    launch_fused(to_csr(full), x, y, op, block=d.block_size, mask=3, flags=flags,
+                 deg=d.full_in_degree, gin_scale=0.0 if gin_scale is None else gin_scale)
+
+
 def aggregate_full(g: Graph, x, op: AggregateOp, kernel: KernelKind = KernelKind.CSR_INTER,
                    threads: int = 1) -> torch.Tensor:
     """One kernel over the full graph, finalised as combine(partial, empty)."""
     del threads
     x = _check_features(g.num_vertices, x)
     if kernel is KernelKind.CSR_INTER:
-        y = torch.zeros((g.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
-        launch_csr(to_csr(g), x, y, op, _lib.AG_EPI_COMBINE, None, g.in_degrees())
+        y = torch.empty((g.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
+        launch_fused(to_csr(g), x, y, op, flags=_lib.AG_EPI_COMBINE | _lib.AG_EPI_EMPTY_OTHER,
+                     deg=g.in_degrees())
         return y
     ex = SubgraphExec.for_inter(g, block_size=max(g.num_vertices, 1))
     partial = ex.run(kernel, x, op)
@@ -380,8 +419,11 @@ def aggregate_decomposed(d: DecomposedGraph, x, op: AggregateOp,
     """
     del threads
     x = _check_features(d.num_vertices, x)
-    intra, inter = decomposed_execs(d)
     y = torch.empty((d.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
+    if fusable(kernel_intra, kernel_inter):
+        run_fused_pair(d, x, y, op, gin_scale)
+        return y
+    intra, inter = decomposed_execs(d)
     inter.run_raw_into(kernel_inter, x, y, op, tile_budget_bytes)
     intra.run_combine_into(kernel_intra, x, y, op, inter.csr.touched(), d.full_in_degree,
                            tile_budget_bytes, gin_scale)

@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .decompose import DecomposedGraph, decompose
+from .decompose import DecomposedGraph, decompose, full_graph
 from .graph import Graph, as_device
 from .kernels import (
     DEFAULT_TILE_BUDGET_BYTES,
@@ -201,8 +201,7 @@ class GNN:
         if model not in ("gcn", "gin"):
             raise ValueError(f"unknown model {model!r}")
         if subject_t is None:
-            full = _reassemble(subject)
-            subject_t = decompose(full.reverse(), subject.block_size)
+            subject_t = decompose(full_graph(subject).reverse(), subject.block_size)
         ws = [as_device(LayerParams.seeded(model, dims[i], dims[i + 1], seed=seed + i,
                                            gin_eps=gin_eps).weight, torch.float32).clone()
               for i in range(len(dims) - 1)]
@@ -296,18 +295,3 @@ class GNN:
         grads = self.backward(saved, d_logits)
         self.sgd(grads, lr)
         return loss, grads
-
-
-def _reassemble(d: DecomposedGraph) -> Graph:
-    """The full (reordered) graph of a decomposition (union of both halves)."""
-    full = d._cache.get("full")
-    if full is None:
-        dst = torch.cat([d.intra.dst, d.inter.dst]).to(torch.int64)
-        src = torch.cat([d.intra.src, d.inter.src]).to(torch.int64)
-        w = None
-        if d.intra.weights is not None:
-            w = torch.cat([d.intra.weights, d.inter.weights])
-        from .graph import _canonical
-        full = _canonical(d.num_vertices, dst, src, w)
-        d._cache["full"] = full
-    return full

@@ -1,0 +1,81 @@
+"""Per-kernel timing on a bench config (CUDA events, warm), for development.
+
+    python scripts/kbench.py [--config C5] [--feat 256]
+"""
+import argparse
+import json
+import pathlib
+import sys
+
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2305_17408_b200 as ag  # noqa: E402
+from paper_2305_17408_b200 import kernels as K  # noqa: E402
+from paper_2305_17408_b200.decompose import full_graph  # noqa: E402
+
+
+def timeit(fn, reps=5):
+    fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--feat", type=int, nargs="+", default=[256, 100])
+    ap.add_argument("--only", default=None, help="run just this kernel once (for ncu)")
+    args = ap.parse_args()
+    cfg = bench.CONFIGS[args.config]
+    g, rg, dec, net, prep = bench.build_workload(cfg)
+    V = cfg["V"]
+    E = rg.num_edges
+    out = {"V": V, "E": E, "intra": dec.intra.num_edges, "prep_s": prep}
+    intra, inter = K.decomposed_execs(dec)
+    full = K.to_csr(full_graph(dec))
+    lens = (full.row_ptr[1:] - full.row_ptr[:-1]).float()
+    out["deg_mean"] = float(lens.mean())
+    out["deg_max"] = float(lens.max())
+    out["rows_over_128"] = int((lens > 128).sum())
+    for F in args.feat:
+        x = torch.randn((V, F), device="cuda")
+        y = torch.empty_like(x)
+        if args.only == "fused_pair":
+            K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM)
+            torch.cuda.synchronize()
+            continue
+        ba = bench.bytes_alg(V, E, F, rg.weights is not None)
+        res = {}
+        res["fused_pair"] = timeit(lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM))
+        res["fused_full_O1"] = timeit(lambda: K.launch_fused(full, x, y, ag.AggregateOp.SUM))
+        res["inter_csr_fused_raw"] = timeit(lambda: K.launch_fused(inter.csr, x, y,
+                                                                   ag.AggregateOp.SUM))
+        res["intra_csr_fused"] = timeit(lambda: K.launch_fused(intra.csr, x, y,
+                                                               ag.AggregateOp.SUM))
+        res["inter_coo"] = timeit(lambda: (K.coo_init(y, ag.AggregateOp.SUM),
+                                           K.launch_coo(inter.coo, x, y, ag.AggregateOp.SUM)))
+        res["intra_dense_block"] = timeit(lambda: K.launch_dense_block(intra.blocks, x, y,
+                                                                       ag.AggregateOp.SUM))
+        res["full_csr_old"] = timeit(lambda: K.launch_csr(full, x, y, ag.AggregateOp.SUM))
+        res["copy_xy"] = timeit(lambda: y.copy_(x))
+        w = torch.randn((F, 256), device="cuda")
+        res["gemm_Fx256"] = timeit(lambda: K.gemm(x, w))
+        res["gemm_TN_dW"] = timeit(lambda: K.gemm(x, x, trans_a=True))
+        gbs = {k: round(ba / (v / 1e3) / 1e9, 1) for k, v in res.items() if "gemm" not in k}
+        out[f"F{F}"] = {"ms": {k: round(v, 4) for k, v in res.items()}, "alg_GBps": gbs,
+                        "bytes_alg": ba}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
