@@ -55,6 +55,11 @@ extern "C" {
 #define AG_EPI_COMBINE 1
 #define AG_EPI_GIN 2
 #define AG_EPI_EMPTY_OTHER 4
+/* AG_EPI_RELU_MASK (ag_fused_spmm only): after everything else,
+ * y = relu_src > 0 ? y : 0 -- the ReLU backward of the layer below, fused
+ * into the transposed aggregation (relu_src = that layer's output, same
+ * shape and row stride as y). */
+#define AG_EPI_RELU_MASK 8
 
 int ag_abi_version(void);
 const char *ag_last_error(void);
@@ -172,46 +177,36 @@ int ag_dense_block_spmm(int64_t num_rows, int64_t feat, int64_t block_size,
                         const uint8_t *other_touched, const int64_t *deg,
                         float gin_scale, void *stream);
 
-/* Stage-aligned CSR ("SA-CSR"), the layout of the fused aggregation kernel,
- * built once per (topology, B, role_mask).  Every row's edges are listed in
- * role order -- the intra run (cols in [floor(r/B)B, +B)), then the inter
- * edges (prefix ++ suffix of the sorted row) -- and cut into 9-slot stages
- * aligned with numpy's pairwise reduction: slot 0 = a role's first term
- * (first stage of the role only), slots 1..8 = one 8-wide accumulator group;
- * empty slots hold col -1.  count: counts[2r..2r+1] = items of the (intra,
- * inter) role with role_mask applied, stage_ptr[V+1] = first stage of each
- * row (exclusive scan), *num_stages_host = total.  fill: stage_col /
- * stage_val [num_stages * 9] (val NULL -> 1.0).  block_size 0 = no split
- * (role_mask must be 2: the whole row is one role). */
-int ag_stage_layout_count(int64_t num_rows, const int32_t *row_ptr,
-                          const int32_t *col_idx, int64_t block_size,
-                          int32_t role_mask, int32_t *stage_ptr, int32_t *counts,
-                          int64_t *num_stages_host, void *stream);
-int ag_stage_layout_fill(int64_t num_rows, const int32_t *row_ptr,
-                         const int32_t *col_idx, const float *val,
-                         int64_t block_size, const int32_t *stage_ptr,
-                         const int32_t *counts, int32_t *stage_col,
-                         float *stage_val, void *stream);
+/* Role-ordered CSR of the fused kernel, built once per (topology, B):
+ * every row's edges re-listed as its intra run (cols in [floor(r/B)B, +B),
+ * ascending) followed by its inter edges (the sorted row's prefix ++ suffix,
+ * ascending) -- the two operand lists of the reference's intra / inter CSR
+ * kernels (decompose.py:63, kernels.py:117-189).  role_col / role_val hold E
+ * entries (role_val may be NULL iff val is NULL); role_mid[r] = row_ptr[r] +
+ * (intra edges of row r). */
+int ag_role_csr_build(int64_t num_rows, const int32_t *row_ptr,
+                      const int32_t *col_idx, const float *val,
+                      int64_t block_size, int32_t *role_col, float *role_val,
+                      int32_t *role_mid, void *stream);
 
-/* Fused decomposed aggregation (one launch) over the full reordered CSR and
- * its SA-CSR layout: for every row, I = intra-role value and O = inter-role
- * value, each in the reference's reduceat order, then
+/* Fused decomposed aggregation (one launch).  For every row r,
+ *   I = intra-role value over edges [row_ptr[r], role_mid[r])
+ *   O = inter-role value over edges [role_mid[r], row_ptr[r+1])
+ * each in the reference's np.add.reduceat order (bitwise), then
  *   role_mask 3: y = combine(I, O) (kernels.py:253-276)   [+ gin term]
  *   role_mask 1/2: a single role with the AG_EPI_* epilogue of ag_csr_spmm.
- * Bitwise equal to two ag_csr_spmm launches over the intra / inter CSRs plus
- * ag_combine, with a single output write.  Source rows are gathered by TMA
- * (cp.async.bulk, one per row) into a per-warp shared-memory stage ring with
- * mbarrier completion; chunks of 16 rows are scheduled dynamically.  Needs
- * F % 4 == 0, F <= 256 and the layout; otherwise (layout pointers NULL) a
- * register-gather kernel over the CSR computes identical values. */
-int ag_fused_spmm(int64_t num_rows, int64_t feat, int64_t block_size,
-                  int32_t role_mask, const int32_t *row_ptr,
-                  const int32_t *col_idx, const float *val,
-                  const int32_t *stage_ptr, const int32_t *counts,
-                  const int32_t *stage_col, const float *stage_val,
+ * role_mid NULL: the whole row is the single role of role_mask 1 or 2, and
+ * col_idx / val are the plain CSR -- this is aggregate_csr_inter
+ * (kernels.py:117-134).  num_edges = row_ptr[num_rows] (used to balance the
+ * row ranges).  One warp per row, 32-column tiles swept over nnz-balanced
+ * row ranges so re-used source rows hit L1; any F (float4 path when F % 4
+ * == 0 and x, y are 16-byte aligned). */
+int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
+                  const int32_t *row_ptr, const int32_t *role_mid,
+                  const int32_t *col_idx, const float *val, int64_t num_edges,
                   const float *x, float *y, int32_t op, int32_t epi_flags,
                   const uint8_t *other_touched, const int64_t *deg,
-                  float gin_scale, void *stream);
+                  float gin_scale, const float *relu_src, void *stream);
 
 /* K5 combine (kernels.py:253-276) as a standalone pass. out may alias a. */
 int ag_combine(int64_t num_rows, int64_t feat, const float *a,
@@ -229,15 +224,29 @@ int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                 float *C, int64_t ldc, float alpha, float beta,
                 int32_t epilogue, void *stream);
 
+/* The same GEMM on the tensor cores: tcgen05.mma kind::tf32 with TMA-fed,
+ * 128-byte-swizzled shared-memory operands, TMEM accumulators and 3xTF32
+ * operand splitting (hi*hi + hi*lo + lo*hi, fp32 accumulation) -- fp32-faithful
+ * to a few ulp.  Needs 16-byte aligned A, B and lda, ldb multiples of 4 and
+ * K >= 1; any M, N, K otherwise (TMA zero-fills the ragged edges).  Skinny
+ * outputs (dW = H^T G, K = V) are split over K with a deterministic fixed-order
+ * reduction. */
+int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                   int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
+                   float *C, int64_t ldc, float alpha, float beta,
+                   int32_t epilogue, void *stream);
+
 /* ===================== training helpers (composed) ======================= */
 
 /* Mean softmax cross-entropy over rows with mask[r] != 0 (mask may be NULL =
- * all rows).  Writes the loss (fp32 scalar, device) and dlogits =
- * (softmax - onehot) / n_masked (0 for unmasked rows). */
-int ag_softmax_xent(int64_t num_rows, int64_t num_classes, const float *logits,
-                    const int32_t *labels, const uint8_t *mask,
-                    int64_t num_masked, float *loss_out, float *dlogits,
-                    void *stream);
+ * all rows).  logits / dlogits are [num_rows] x [num_classes] with row stride
+ * ld >= num_classes.  Writes the loss (fp32 scalar, device; per-CTA fp64
+ * partials summed in a fixed order) and dlogits = (softmax - onehot) /
+ * n_masked (0 for unmasked rows; columns >= num_classes untouched). */
+int ag_softmax_xent(int64_t num_rows, int64_t num_classes, int64_t ld,
+                    const float *logits, const int32_t *labels,
+                    const uint8_t *mask, int64_t num_masked, float *loss_out,
+                    float *dlogits, void *stream);
 /* g = g * (h > 0) in place (ReLU backward). */
 int ag_relu_backward(int64_t n, const float *h, float *g, void *stream);
 /* w -= lr * dw. */

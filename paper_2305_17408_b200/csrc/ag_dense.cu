@@ -146,50 +146,60 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const flo
   }
 }
 
-// One warp per row: mean softmax cross-entropy over the masked rows.
-__global__ void xent_rows_kernel(int64_t rows, int64_t C, const float *logits,
-                                 const int32_t *labels, const uint8_t *mask, float inv_n,
-                                 float *row_loss, float *dlogits) {
-  const int lane = threadIdx.x % 32;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
-  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
-  for (int64_t r = warp; r < rows; r += nwarps) {
-    const float *z = logits + r * C;
-    float *dz = dlogits + r * C;
+// Mean softmax cross-entropy over the masked rows.  CTA b owns
+// the contiguous row block [b*R, (b+1)*R); a warp per row; lane c holds
+// logits c, c+32, ...  Each CTA reduces its rows' losses in fp64 in a fixed
+// order and writes one partial; loss_final_kernel adds the partials in order,
+// so the loss is deterministic for a given grid.
+constexpr int kXentThreads = 256;
+
+__global__ void __launch_bounds__(kXentThreads) xent_kernel(
+    int64_t rows, int64_t C, int64_t ld, const float *logits, const int32_t *labels,
+    const uint8_t *mask, float inv_n, int64_t rows_per_cta, double *partial, float *dlogits) {
+  __shared__ double warp_sum[kXentThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(rows, r0 + rows_per_cta);
+  double acc = 0.0;
+  for (int64_t r = r0 + warp; r < r1; r += kXentThreads / 32) {
+    const float *z = logits + r * ld;
+    float *dz = dlogits + r * ld;
     const bool on = mask ? mask[r] != 0 : true;
     if (!on) {
       for (int64_t c = lane; c < C; c += 32) dz[c] = 0.0f;
-      if (lane == 0) row_loss[r] = 0.0f;
       continue;
     }
     float mx = -INFINITY;
     for (int64_t c = lane; c < C; c += 32) mx = fmaxf(mx, z[c]);
+#pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     float se = 0.0f;
     for (int64_t c = lane; c < C; c += 32) se += expf(z[c] - mx);
+#pragma unroll
     for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
     const int32_t y = labels[r];
-    const float lse = mx + logf(se);
+    const float inv_se = 1.0f / se;
     for (int64_t c = lane; c < C; c += 32) {
-      const float p = expf(z[c] - mx) / se;
+      const float p = expf(z[c] - mx) * inv_se;
       dz[c] = (p - (c == y ? 1.0f : 0.0f)) * inv_n;
     }
-    if (lane == 0) row_loss[r] = lse - z[y];
+    if (lane == 0) acc += static_cast<double>(mx + logf(se) - z[y]);
+  }
+  if (lane == 0) warp_sum[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kXentThreads / 32; ++w) t += warp_sum[w];
+    partial[blockIdx.x] = t;
   }
 }
 
-// Deterministic single-CTA reduction of the per-row losses.
-__global__ void loss_reduce_kernel(int64_t rows, const float *row_loss, float inv_n, float *out) {
-  __shared__ double sh[1024];
-  double s = 0.0;
-  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) s += row_loss[i];
-  sh[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-    __syncthreads();
+__global__ void loss_final_kernel(int n, const double *partial, double inv_n, float *out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += partial[i];
+    *out = static_cast<float>(t * inv_n);
   }
-  if (threadIdx.x == 0) *out = static_cast<float>(sh[0] * inv_n);
 }
 
 __global__ void relu_bwd_kernel(int64_t n, const float *h, float *g) {
@@ -247,22 +257,24 @@ extern "C" int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int6
   return AG_OK;
 }
 
-extern "C" int ag_softmax_xent(int64_t rows, int64_t C, const float *logits, const int32_t *labels,
-                               const uint8_t *mask, int64_t num_masked, float *loss_out,
-                               float *dlogits, void *stream) {
-  if (rows < 0 || C < 1) return fail(AG_ERR_VALUE, "bad loss sizes");
+extern "C" int ag_softmax_xent(int64_t rows, int64_t C, int64_t ld, const float *logits,
+                               const int32_t *labels, const uint8_t *mask, int64_t num_masked,
+                               float *loss_out, float *dlogits, void *stream) {
+  if (rows < 0 || C < 1 || ld < C) return fail(AG_ERR_VALUE, "bad loss sizes");
   cudaStream_t st = as_stream(stream);
   const float inv_n = num_masked > 0 ? 1.0f / static_cast<float>(num_masked) : 0.0f;
-  Scratch rl;
-  AG_CUDA(rl.alloc(std::max<int64_t>(rows, 1) * sizeof(float), st));
-  if (rows > 0) {
-    xent_rows_kernel<<<grid_for(rows * 32, 256), 256, 0, st>>>(rows, C, logits, labels, mask,
-                                                               inv_n, rl.as<float>(), dlogits);
-    AG_LAUNCH_CHECK("xent_rows_kernel");
-  }
-  loss_reduce_kernel<<<1, 1024, 0, st>>>(rows, rl.as<float>(),
-                                         num_masked > 0 ? 1.0 / num_masked : 0.0, loss_out);
-  AG_LAUNCH_CHECK("loss_reduce_kernel");
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64,
+                                                              static_cast<int64_t>(sm_count()) * 8));
+  const int64_t per = (rows + ctas - 1) / ctas;
+  Scratch part;
+  AG_CUDA(part.alloc(ctas * sizeof(double), st));
+  xent_kernel<<<static_cast<unsigned>(ctas), kXentThreads, 0, st>>>(
+      rows, C, ld, logits, labels, mask, inv_n, std::max<int64_t>(per, 1), part.as<double>(),
+      dlogits);
+  AG_LAUNCH_CHECK("xent_kernel");
+  loss_final_kernel<<<1, 32, 0, st>>>(static_cast<int>(ctas), part.as<double>(),
+                                      num_masked > 0 ? 1.0 / num_masked : 0.0, loss_out);
+  AG_LAUNCH_CHECK("loss_final_kernel");
   return AG_OK;
 }
 

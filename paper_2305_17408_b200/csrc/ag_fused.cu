@@ -1,44 +1,40 @@
-// Fused single-pass decomposed aggregation (the hot path of every GCN/GIN layer).
+// Decomposed aggregation in one pass (the hot path of every GCN/GIN layer).
 //
-// One launch computes, for every destination row r of the FULL reordered CSR,
-//   I = intra-role value over the row's block-local edges (cols in [cB, cB+B))
-//   O = inter-role value over the remaining edges (prefix ++ suffix of the row)
+// For every destination row r of a CSR whose edges are stored in ROLE ORDER
+// (intra run first, then the inter edges; ag_role_csr_build), one launch
+// computes
+//   I = intra-role value over edges [row_ptr[r], mid[r])
+//   O = inter-role value over edges [mid[r], row_ptr[r+1])
 //   y[r] = combine(I, O)  [+ (1+eps) x[r] for GIN]
-// which is bit-for-bit what the reference computes with two separate CSR
-// kernels and combine() (kernels.py:87-189, :253-276): both role sums follow
-// np.add.reduceat's order (first term + numpy pairwise, see ag_spmm.cu), the
-// intra edges of a sorted row are one contiguous run, and the inter role is
-// the ordered concatenation of what is left.  Compared with two launches it
-// saves one full write + read of the V x F partial (2VF*4 bytes): HBM traffic
-// is topology once, X once (modulo L2 misses), Y once.
+// bit-for-bit what the reference computes with two CSR kernels and combine()
+// (kernels.py:87-189, :253-276).  Each role is reduced in np.add.reduceat's
+// order: c0 + P(c1..c_{n-1}) with c = fl(val * x[col]) and P numpy's pairwise
+// sum (n < 8: sequential from -0.0; n <= 128: 8 strided accumulators, the
+// tree ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8 tail in order;
+// n > 128: split at n/2 rounded down to a multiple of 8 and recurse).
 //
-// Layout: the "stage-aligned CSR" (built once per topology, ag_stage_layout_*)
-// lists every row's edges in role order (intra run, then inter = prefix ++
-// suffix) cut into 9-slot stages aligned with numpy's pairwise structure:
-// slot 0 holds a role's first term c0 (only in the role's first stage), slots
-// 1..8 hold one 8-wide accumulator group, empty slots hold col = -1.  The
-// reduction is then branch-free per stage: the 8 accumulators start at -0.0
-// (x + -0.0 == x bitwise) and take one group per stage, leaves of the >128
-// recursion start on stage boundaries (split points are multiples of 8), and
-// the n%8 tail is the role's last stage.
-//
-// Data movement (sm_100a).  Warps pull chunks of 16 consecutive rows from a
-// global atomic counter, so the whole grid sweeps the row space as one tight
-// wavefront and the reorder's locality keeps gathered X rows L2-resident.
-// Each warp runs a producer/consumer pipeline on itself: the producer reads a
-// stage's 9 (col, val) slots with one coalesced load and issues one
-// cp.async.bulk (TMA) per source row into a shared-memory ring of stages,
-// completing on the stage's mbarrier; the consumer reduces stage by stage.
-// Products and sums use packed FMUL2 / FFMA2(acc, 1.0, c) (exact: acc*1 is
-// exact, so the only rounding is that of the sum) -- half the FP issue slots.
-// Feature widths the bulk path cannot serve (F % 4 != 0, F > 256) take the
-// register-gather long-row kernel below.
+// Work decomposition (sm_100a, HBM/L2-bound gather):
+//  * The feature dimension is cut into column tiles of T = 32 floats (one
+//    128-byte L1 line per source row).  A CTA owns one column tile of one
+//    contiguous, nnz-balanced range of rows and sweeps it front to back, so
+//    the source rows of a reordered graph (the 16-row community block and its
+//    neighbourhood) are re-read from the SM's L1 instead of L2.  The CTAs of
+//    the ntiles column tiles of a range are adjacent in launch order and share
+//    the range's topology through L2.
+//  * One warp per row.  The warp is split into NG groups of 32/NG lanes; every
+//    group covers the SAME T columns (float4 per lane) and owns 8/NG of the
+//    8 pairwise accumulators, so a warp has NG independent row gathers in
+//    flight per round and the accumulator tree's upper levels are two
+//    xor-shuffles -- the exact numpy tree, no re-association.
+//  * Column indices and weights are streamed 32 edges at a time into lane
+//    registers (one coalesced load each) and broadcast with shuffles.
+//  * Products / sums are packed FMUL2 / FADD2 (fp32x2, round-to-nearest, no
+//    FMA contraction), so results stay bitwise equal to the reference.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
-
-#include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "ag_common.cuh"
 #include "ag_vec.cuh"
@@ -47,54 +43,31 @@ namespace ag {
 namespace {
 using namespace vec;
 
-constexpr int kChunk = 16;   // rows per chunk (consecutive)
-constexpr int kSlots = 9;    // slot 0: first term, slots 1..8: one pairwise group
 constexpr int kLeafN = 128;  // numpy PW_BLOCKSIZE
 constexpr int kDepth = 40;
+constexpr int kThreads = 256;
+constexpr unsigned kFull = 0xffffffffu;
 
-// ------------------------------------------------------------ PTX helpers --
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile(
-      "{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
-          smem_u32(bar)),
-      "r"(bytes)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  uint32_t done = 0;
-  const uint32_t addr = smem_u32(bar);
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(addr), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
-                                         uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
+struct GArgs {
+  int64_t rows;
+  int feat;
+  int mask;                 // 1 intra only, 2 inter only, 3 both (combine)
+  const int32_t *row_ptr;   // [rows + 1]
+  const int32_t *mid;       // [rows] end of the intra run; nullptr: single role
+  const int32_t *col;       // role-ordered column indices
+  const float *val;         // role-ordered weights; nullptr = implicit 1.0
+  const float *x;
+  float *y;
+  Epi ep;
+  int ntiles;               // column tiles
+  int ranges;               // row ranges
+  int64_t cost_total;       // nnz + kRowCost * rows
+  float one;                // 1.0f, passed at run time (see add2)
+};
 
-// packed fp32x2: p = fl(a * s) per lane pair (FMUL2)
+constexpr int64_t kRowCost = 4;  // a row's fixed cost in edge units (epilogue, topology)
+
+// ---------------------------------------------------------- packed fp32x2 --
 __device__ __forceinline__ uint64_t pk(float a, float b) {
   uint64_t r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
@@ -103,241 +76,238 @@ __device__ __forceinline__ uint64_t pk(float a, float b) {
 __device__ __forceinline__ void upk(uint64_t r, float &a, float &b) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
 }
-__device__ __forceinline__ uint64_t pmul(uint64_t a, uint64_t s) {
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
   uint64_t d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(s));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
-// acc + c as FFMA2(acc, 1.0, c) with a run-time 1.0 (one): exact fl(acc + c),
-// and not contractible with the preceding FMUL2
-__device__ __forceinline__ uint64_t padd(uint64_t acc, uint64_t one, uint64_t c) {
+// fl(a + b) as FFMA2(a, one, b) with a RUN-TIME one = {1.0f, 1.0f}: exact
+// (a * 1 is exact, so the only rounding is the sum's), and opaque to ptxas,
+// which otherwise contracts mul.rn.f32x2 + add.rn.f32x2 into one FFMA2 and
+// changes the rounding of c = fl(val * x).
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b, uint64_t one) {
   uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(acc), "l"(one), "l"(c));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(one), "l"(b));
   return d;
 }
 
-// ------------------------------------------------------------ arguments ----
-struct FusedArgs {
-  int64_t rows;
-  int feat;
-  int block;      // B (0: no role split, the whole row is one role)
-  int mask;       // 1 intra only, 2 inter only, 3 both (combine)
-  const int32_t *row_ptr;  // CSR (register-gather fallback)
-  const int32_t *col;
-  const float *val;        // nullptr: implicit 1.0
-  const float *x;
-  float *y;
-  Epi ep;
-  // stage-aligned layout
-  const int32_t *stage_ptr;  // [rows + 1] first stage of each row
-  const int2 *counts;        // [rows] items of the (intra, inter) role, mask applied
-  const int32_t *scol;       // [stages * 9]; -1 = empty slot
-  const float *sval;         // [stages * 9]
-  unsigned int *chunk_ctr;   // dynamic chunk scheduler (zeroed per launch)
-  int warps;                 // warps per CTA
-  int warp_bytes;            // dynamic smem per warp
-  int stages;                // ring depth (power of two)
-  float one;                 // 1.0f at run time (keeps FFMA2(acc, 1, c) opaque)
+// Predicated packed add: acc = on ? fl(acc + c) : acc (no select, no branch).
+__device__ __forceinline__ uint64_t add2_if(uint64_t acc, uint64_t c, uint64_t one, bool on) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q fma.rn.f32x2 %0, %0, %1, %2;\n\t}"
+      : "+l"(acc)
+      : "l"(one), "l"(c), "r"(static_cast<int>(on)));
+  return acc;
+}
+
+// A lane's slice of one row: VEC consecutive columns as packed fp32 pairs.
+template <int VEC>
+struct Lv {
+  static constexpr int NP = VEC / 2;
+  uint64_t p[NP];
+};
+template <>
+struct Lv<1> {
+  static constexpr int NP = 0;
+  float s;
 };
 
-__device__ __forceinline__ int role_stages(int n) {
-  return n <= 0 ? 0 : (n == 1 ? 1 : (n - 1 + 7) >> 3);
+template <int VEC>
+__device__ __forceinline__ Lv<VEC> lv_splat(float v) {
+  Lv<VEC> r;
+  if constexpr (VEC == 1) {
+    r.s = v;
+  } else {
+#pragma unroll
+    for (int i = 0; i < Lv<VEC>::NP; ++i) r.p[i] = pk(v, v);
+  }
+  return r;
+}
+template <int VEC>
+__device__ __forceinline__ Lv<VEC> lv_add(const Lv<VEC> &a, const Lv<VEC> &b, uint64_t one) {
+  Lv<VEC> r;
+  if constexpr (VEC == 1) {
+    r.s = __fadd_rn(a.s, b.s);
+  } else {
+#pragma unroll
+    for (int i = 0; i < Lv<VEC>::NP; ++i) r.p[i] = add2(a.p[i], b.p[i], one);
+  }
+  return r;
+}
+template <int VEC>
+__device__ __forceinline__ Lv<VEC> lv_add_if(const Lv<VEC> &a, const Lv<VEC> &b, uint64_t one,
+                                             bool on) {
+  Lv<VEC> r;
+  if constexpr (VEC == 1) {
+    r.s = on ? __fadd_rn(a.s, b.s) : a.s;
+  } else {
+#pragma unroll
+    for (int i = 0; i < Lv<VEC>::NP; ++i) r.p[i] = add2_if(a.p[i], b.p[i], one, on);
+  }
+  return r;
+}
+template <int VEC>
+__device__ __forceinline__ Lv<VEC> lv_scale(const Lv<VEC> &a, uint64_t vv) {
+  Lv<VEC> r;
+  if constexpr (VEC == 1) {
+    float v, v2;
+    upk(vv, v, v2);
+    r.s = __fmul_rn(a.s, v);
+  } else {
+#pragma unroll
+    for (int i = 0; i < Lv<VEC>::NP; ++i) r.p[i] = mul2(a.p[i], vv);
+  }
+  return r;
+}
+template <int VEC>
+__device__ __forceinline__ Lv<VEC> lv_max(const Lv<VEC> &a, const Lv<VEC> &b) {
+  Lv<VEC> r;
+  if constexpr (VEC == 1) {
+    r.s = fmaxf(a.s, b.s);
+  } else {
+#pragma unroll
+    for (int i = 0; i < Lv<VEC>::NP; ++i) {
+      float a0, a1, b0, b1;
+      upk(a.p[i], a0, a1);
+      upk(b.p[i], b0, b1);
+      r.p[i] = pk(fmaxf(a0, b0), fmaxf(a1, b1));
+    }
+  }
+  return r;
+}
+// Unconditional non-coherent 16-byte loads straight into packed pairs.  Every
+// caller passes a valid address (inactive lanes / discarded tail items read a
+// clamped, in-bounds row), so no predicate or branch surrounds the load.
+template <int VEC>
+__device__ __forceinline__ Lv<VEC> lv_load(const float *p) {
+  Lv<VEC> r;
+  if constexpr (VEC == 1) {
+    r.s = __ldg(p);
+  } else {
+#pragma unroll
+    for (int i = 0; i < Lv<VEC>::NP; i += 2)
+      asm("ld.global.nc.v2.b64 {%0, %1}, [%2];"
+          : "=l"(r.p[i]), "=l"(r.p[i + 1])
+          : "l"(p + 2 * i));
+  }
+  return r;
+}
+template <int VEC>
+__device__ __forceinline__ Vf<VEC> lv_out(const Lv<VEC> &a) {
+  Vf<VEC> r;
+  if constexpr (VEC == 1) {
+    r.v[0] = a.s;
+  } else {
+#pragma unroll
+    for (int i = 0; i < Lv<VEC>::NP; ++i) upk(a.p[i], r.v[2 * i], r.v[2 * i + 1]);
+  }
+  return r;
 }
 
-__device__ __forceinline__ void lds_v2u64(uint32_t addr, uint64_t &a, uint64_t &b) {
-  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr));
+// One entry of a warp's topology window (16 bytes): the source row's offset
+// into x in floats, and its weight duplicated as an fp32 pair (the FMUL2
+// operand), so one broadcast LDS.128 yields everything an item needs.
+constexpr int kWin = 32;  // items per window refill
+
+__device__ __forceinline__ void win_st(uint32_t addr, uint64_t a, uint64_t b) {
+  asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(addr), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void win_ld(uint32_t addr, uint32_t &off, uint64_t &vv) {
+  uint64_t a;
+  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(vv) : "r"(addr) : "memory");
+  off = static_cast<uint32_t>(a);
 }
 
-template <int FV>
-struct Warp {
-  static constexpr int W = 4 * FV;
-  static constexpr int P = W / 2;  // fp32x2 pairs per lane
-  const FusedArgs *a;
-  uint64_t *bar;
-  float *vals;        // [stages][kSlots]
-  int *fifo;          // [4] chunk ids, producer -> consumer
-  uint32_t ring_u32;  // shared address of the ring
-  uint32_t vals_u32;
-  uint32_t rowbytes;
+// ------------------------------------------------------------ the warp ----
+// Per-warp state, passed by value (never by address: it must stay in
+// registers).  Edge indices are int32 (E < 2^31 is checked on the host).
+template <int VEC, bool W>
+struct RowWarp {
+  uint32_t win;        // shared address of this warp's window (kWin entries)
+  const int32_t *col;  // role-ordered topology
+  const float *val;    // nullptr = 1.0
+  const float *xl;     // x + this lane's first column (clamped in-bounds)
+  uint32_t feat;
   int lane;
-  int smask;
-  int64_t nchunks;
-  bool act[FV];       // this lane holds feature columns in half h
-  // producer
-  int64_t pt;         // stages issued
-  int64_t ps, pe;     // next stage to issue / end of the producer's chunk
-  int pcount;         // chunk ids pushed
-  bool pdone;
-  // consumer
-  int64_t ct;         // stages consumed
-  int ccount;         // chunk ids popped
-  uint32_t phase;
-  int cur;
-  uint32_t cur_base;  // ring address of the acquired stage's slot 0, this lane
-  uint64_t one2;
+  uint64_t one;    // {1.0f, 1.0f} loaded at run time (see add2)
+  int32_t p, end;  // window holds items [p, p + kWin)
 
-  // pull the next chunk from the scheduler into the FIFO
-  __device__ __forceinline__ bool prod_next_chunk() {
-    if (pdone || pcount - ccount >= 4) return false;
-    int c = 0;
-    if (lane == 0) c = static_cast<int>(atomicAdd(a->chunk_ctr, 1u));
-    c = __shfl_sync(0xffffffffu, c, 0);
-    if (c >= nchunks) {
-      c = -1;
-      pdone = true;
-    }
-    if (lane == 0) fifo[pcount & 3] = c;
+  __device__ __forceinline__ void fill(int32_t at) {
     __syncwarp();
-    ++pcount;
-    if (c < 0) return false;
-    const int64_t r0 = static_cast<int64_t>(c) * kChunk;
-    const int64_t r1 = r0 + kChunk < a->rows ? r0 + kChunk : a->rows;
-    ps = a->stage_ptr[r0];
-    pe = a->stage_ptr[r1];
-    return true;
-  }
-
-  __device__ __forceinline__ bool prod_seek() {
-    while (ps >= pe)
-      if (!prod_next_chunk()) return false;
-    return true;
-  }
-
-  __device__ __forceinline__ void issue() {
-    const int slot = static_cast<int>(pt) & smask;
-    int32_t c = -1;
-    float v = 0.0f;
-    if (lane < kSlots) {
-      c = __ldg(a->scol + ps * kSlots + lane);
-      v = __ldg(a->sval + ps * kSlots + lane);
-      vals[slot * kSlots + lane] = v;
+    p = at;
+    const int32_t e = at + lane;
+    if (e < end) {
+      const uint32_t off = static_cast<uint32_t>(__ldg(col + e)) * feat;
+      const float v = W ? __ldg(val + e) : 1.0f;
+      win_st(win + lane * 16, off, pk(v, v));
     }
-    const bool valid = c >= 0;
-    const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, valid));
-    if (lane == 0) mbar_expect_tx(&bar[slot], rowbytes * cnt);
     __syncwarp();
-    if (valid) {
-      fence_proxy_async();
-      bulk_g2s(reinterpret_cast<char *>(ring_ptr()) + (slot * kSlots + lane) * rowbytes,
-               a->x + static_cast<int64_t>(c) * a->feat, rowbytes, &bar[slot]);
-    }
-    ++pt;
-    ++ps;
+  }
+  __device__ __forceinline__ void ensure(int32_t lo, int n) {
+    if (lo + n > p + kWin) fill(lo);
+  }
+  template <bool RAW>
+  __device__ __forceinline__ Lv<VEC> item(int32_t e) const {
+    uint32_t off;
+    uint64_t vv;
+    win_ld(win + static_cast<uint32_t>(e - p) * 16u, off, vv);
+    const float *ptr;  // xl + off as one IMAD.WIDE.U32
+    asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(ptr) : "r"(off), "l"(xl));
+    const Lv<VEC> xv = lv_load<VEC>(ptr);
+    if (RAW || !W) return xv;
+    return lv_scale<VEC>(xv, vv);
   }
 
-  float *ring_base;
-  __device__ __forceinline__ float *ring_ptr() const { return ring_base; }
-
-  __device__ __forceinline__ void fill() {
-    while (pt - ct < smask + 1 && prod_seek()) issue();
-  }
-
-  // consumer side ---------------------------------------------------------
-  __device__ __forceinline__ int next_chunk() {
-    if (ccount == pcount) prod_next_chunk();
-    const int c = fifo[ccount & 3];
-    ++ccount;
-    fill();
-    return c;
-  }
-
-  __device__ __forceinline__ void acquire() {
-    cur = static_cast<int>(ct) & smask;
-    mbar_wait(&bar[cur], (phase >> cur) & 1u);
-    phase ^= 1u << cur;
-    cur_base = ring_u32 + cur * kSlots * rowbytes + lane * 16;
-  }
-
-  __device__ __forceinline__ void release() {
-    ++ct;
-    __syncwarp();
-    fill();
-  }
-
-  // packed contribution fl(val * x) of slot j of the acquired stage
-  __device__ __forceinline__ void contrib(int j, uint64_t (&c)[P]) const {
-    const float v = vals[cur * kSlots + j];
-    const uint64_t v2 = pk(v, v);
-    const uint32_t addr = cur_base + j * rowbytes;
+  // res + c_e0 + ... + c_{e0+t-1} in order, t < 8 (warp-uniform)
+  __device__ __forceinline__ Lv<VEC> seq(Lv<VEC> res, int32_t e0, int t) {
+    if (t <= 0) return res;
+    ensure(e0, t);
+    Lv<VEC> c[7];
 #pragma unroll
-    for (int h = 0; h < FV; ++h) {
-      uint64_t lo = 0, hi = 0;
-      if (act[h]) lds_v2u64(addr + h * 512, lo, hi);
-      c[2 * h] = pmul(lo, v2);
-      c[2 * h + 1] = pmul(hi, v2);
-    }
+    for (int i = 0; i < 7; ++i) c[i] = item<false>(e0 + (i < t ? i : 0));
+#pragma unroll
+    for (int i = 0; i < 7; ++i) res = lv_add_if<VEC>(res, c[i], one, i < t);
+    return res;
   }
 
-  __device__ __forceinline__ Vf<W> raw(int j) const {
-    const uint32_t addr = cur_base + j * rowbytes;
-    Vf<W> v;
+  // numpy pairwise leaf over items [e0, e0 + n), 8 <= n <= 128
+  __device__ __forceinline__ Lv<VEC> leaf(int32_t e0, int n) {
+    const int q = n >> 3;
+    Lv<VEC> r[8];
+    ensure(e0, 8);
 #pragma unroll
-    for (int h = 0; h < FV; ++h) {
-      uint64_t lo = 0, hi = 0;
-      if (act[h]) lds_v2u64(addr + h * 512, lo, hi);
-      upk(lo, v.v[4 * h], v.v[4 * h + 1]);
-      upk(hi, v.v[4 * h + 2], v.v[4 * h + 3]);
-    }
-    return v;
-  }
-
-  // numpy pairwise leaf over the next nl items (stage aligned)
-  __device__ __forceinline__ void leaf(int nl, bool first_in_cur, uint64_t (&res)[P]) {
-    const int q = nl >> 3, tail = nl & 7;
-    const uint64_t nz = pk(-0.0f, -0.0f);
-#pragma unroll
-    for (int i = 0; i < P; ++i) res[i] = nz;
-    if (q > 0) {
-      uint64_t r[8][P];
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-#pragma unroll
-        for (int i = 0; i < P; ++i) r[j][i] = nz;
+    for (int j = 0; j < 8; ++j) r[j] = item<false>(e0 + j);
 #pragma unroll 1
-      for (int g = 0; g < q; ++g) {
-        if (g > 0 || !first_in_cur) { release(); acquire(); }
+    for (int g = 1; g < q; ++g) {
+      const int32_t b = e0 + 8 * g;
+      ensure(b, 8);
+      Lv<VEC> c[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          uint64_t c[P];
-          contrib(1 + j, c);
+      for (int j = 0; j < 8; ++j) c[j] = item<false>(b + j);
 #pragma unroll
-          for (int i = 0; i < P; ++i) r[j][i] = padd(r[j][i], one2, c[i]);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < P; ++i)
-        res[i] = padd(padd(padd(r[0][i], one2, r[1][i]), one2, padd(r[2][i], one2, r[3][i])),
-                      one2,
-                      padd(padd(r[4][i], one2, r[5][i]), one2, padd(r[6][i], one2, r[7][i])));
+      for (int j = 0; j < 8; ++j) r[j] = lv_add<VEC>(r[j], c[j], one);
     }
-    if (tail > 0) {
-      if (q > 0 || !first_in_cur) { release(); acquire(); }
-#pragma unroll 1
-      for (int j = 0; j < tail; ++j) {
-        uint64_t c[P];
-        contrib(1 + j, c);
-#pragma unroll
-        for (int i = 0; i < P; ++i) res[i] = padd(res[i], one2, c[i]);
-      }
-    }
+    const Lv<VEC> s = lv_add<VEC>(
+        lv_add<VEC>(lv_add<VEC>(r[0], r[1], one), lv_add<VEC>(r[2], r[3], one), one),
+        lv_add<VEC>(lv_add<VEC>(r[4], r[5], one), lv_add<VEC>(r[6], r[7], one), one), one);
+    return seq(s, e0 + 8 * q, n & 7);
   }
 
-  // P over the next m items: post-order walk of numpy's recursion (a single
-  // leaf when m <= 128); the first leaf shares the role's first stage with c0
-  __device__ __forceinline__ void pairwise(int m, uint64_t (&out)[P]) {
+  // recursion of numpy's pairwise sum (n > 128), post-order, explicit stack
+  __device__ __forceinline__ Lv<VEC> pairwise_long(int32_t e0, int n) {
+    int32_t st_e[kDepth];
     int st_n[kDepth];
     int st_stage[kDepth];
-    uint64_t st_left[kDepth][P];
+    Lv<VEC> st_left[kDepth];
     int sp = 0;
-    bool first = true;
-    st_n[0] = m;
+    st_e[0] = e0;
+    st_n[0] = n;
     st_stage[0] = 0;
+    Lv<VEC> ret = lv_splat<VEC>(0.0f);
 #pragma unroll 1
     while (sp >= 0) {
       const int cn = st_n[sp];
       if (cn <= kLeafN) {
-        leaf(cn, first, out);
-        first = false;
+        ret = leaf(st_e[sp], cn);
         --sp;
         continue;
       }
@@ -345,474 +315,204 @@ struct Warp {
       n2 -= n2 & 7;
       if (st_stage[sp] == 0) {
         st_stage[sp] = 1;
+        st_e[sp + 1] = st_e[sp];
         st_n[sp + 1] = n2;
         st_stage[sp + 1] = 0;
         ++sp;
       } else if (st_stage[sp] == 1) {
-#pragma unroll
-        for (int i = 0; i < P; ++i) st_left[sp][i] = out[i];
+        st_left[sp] = ret;
         st_stage[sp] = 2;
+        st_e[sp + 1] = st_e[sp] + n2;
         st_n[sp + 1] = cn - n2;
         st_stage[sp + 1] = 0;
         ++sp;
       } else {
-#pragma unroll
-        for (int i = 0; i < P; ++i) out[i] = padd(st_left[sp][i], one2, out[i]);
+        ret = lv_add<VEC>(st_left[sp], ret, one);
         --sp;
       }
     }
+    return ret;
   }
 
+  // one role over items [e0, e0 + n)
   template <bool IS_MAX>
-  __device__ __forceinline__ Vf<W> role(int n) {
-    Vf<W> out = splat<W>(0.0f);
-    if (n <= 0) return out;
-    acquire();
-    if constexpr (IS_MAX) {
-      out = raw(0);
-      int left = n - 1, k = 0;
-#pragma unroll 1
-      while (left > 0) {
-        if (k > 0) { release(); acquire(); }
-        const int cnt = left < 8 ? left : 8;
-#pragma unroll 1
-        for (int j = 0; j < cnt; ++j) out = vmax<W>(out, raw(1 + j));
-        left -= cnt;
-        ++k;
-      }
-      release();
-      return out;
-    } else {
-      uint64_t c0[P];
-      contrib(0, c0);
-      if (n > 1) {
-        uint64_t p[P];
-        pairwise(n - 1, p);
-#pragma unroll
-        for (int i = 0; i < P; ++i) c0[i] = padd(c0[i], one2, p[i]);
-      }
-      release();
-#pragma unroll
-      for (int i = 0; i < P; ++i) upk(c0[i], out.v[2 * i], out.v[2 * i + 1]);
-      return out;
-    }
-  }
+  __device__ __forceinline__ Lv<VEC> role(int32_t e0, int32_t n);
 };
 
-template <int W>
-__device__ __forceinline__ Vf<W> combine2(int op, const Vf<W> &I, bool ti, const Vf<W> &O,
-                                          bool to, int64_t deg) {
-  if (op == AG_OP_SUM) return vadd<W>(I, O);
-  if (op == AG_OP_MEAN) {
-    const float d = static_cast<float>(deg < 1 ? 1 : deg);
-    Vf<W> s = vadd<W>(I, O), r;
-#pragma unroll
-    for (int i = 0; i < W; ++i) r.v[i] = __fdiv_rn(s.v[i], d);
-    return r;
-  }
-  if (ti && to) return vmax<W>(I, O);
-  if (ti) return I;
-  if (to) return O;
-  return splat<W>(0.0f);
+// Roles longer than kLeafN + 1 items take the recursion out of line; the
+// warp state travels by value so the hot path keeps it in registers.
+template <int VEC, bool W>
+__device__ __noinline__ Lv<VEC> pairwise_long_fn(RowWarp<VEC, W> w, int32_t e0, int n) {
+  w.fill(e0);
+  return w.pairwise_long(e0, n);
 }
 
-template <int FV>
-__device__ __forceinline__ Vf<4 * FV> load_row(const float *base, int feat, int lane) {
-  Vf<4 * FV> v = splat<4 * FV>(0.0f);
-#pragma unroll
-  for (int h = 0; h < FV; ++h) {
-    const int f = h * 128 + lane * 4;
-    if (f < feat) {
-      const float4 t = *reinterpret_cast<const float4 *>(base + f);
-      v.v[h * 4 + 0] = t.x; v.v[h * 4 + 1] = t.y; v.v[h * 4 + 2] = t.z; v.v[h * 4 + 3] = t.w;
-    }
-  }
-  return v;
-}
-
-template <int FV, bool IS_MAX>
-__global__ void __launch_bounds__(FV == 1 ? 512 : 384) fused_kernel(FusedArgs a) {
-  constexpr int W = 4 * FV;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  unsigned char *base = smem_raw + static_cast<size_t>(warp) * a.warp_bytes;
-  Warp<FV> w;
-  w.a = &a;
-  w.bar = reinterpret_cast<uint64_t *>(base);
-  w.vals = reinterpret_cast<float *>(base + 8 * a.stages);
-  w.fifo = reinterpret_cast<int *>(base + 8 * a.stages + 4 * kSlots * a.stages);
-  const int hdr = (8 * a.stages + 4 * kSlots * a.stages + 16 + 127) / 128 * 128;
-  w.ring_base = reinterpret_cast<float *>(base + hdr);
-  w.ring_u32 = smem_u32(w.ring_base);
-  w.vals_u32 = smem_u32(w.vals);
-  w.rowbytes = static_cast<uint32_t>(a.feat) * 4u;
-  w.lane = lane;
-  w.smask = a.stages - 1;
-  w.nchunks = (a.rows + kChunk - 1) / kChunk;
-#pragma unroll
-  for (int h = 0; h < FV; ++h) w.act[h] = h * 128 + lane * 4 < a.feat;
-  w.pt = 0; w.ps = 0; w.pe = 0; w.pcount = 0; w.pdone = false;
-  w.ct = 0; w.ccount = 0; w.phase = 0; w.cur = 0; w.cur_base = 0;
-  w.one2 = pk(a.one, a.one);
-  if (lane == 0) {
-    for (int i = 0; i < a.stages; ++i) mbar_init(&w.bar[i], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  const int64_t ld = a.feat;
-  const bool need_y = a.mask != 3 && (a.ep.flags & AG_EPI_COMBINE) &&
-                      !(a.ep.flags & AG_EPI_EMPTY_OTHER);
-  const bool need_x = (a.ep.flags & AG_EPI_GIN) != 0;
-  const bool need_ot = need_y && a.ep.other_touched != nullptr;
-  const bool need_deg = a.ep.op == AG_OP_MEAN && a.ep.deg != nullptr;
-#pragma unroll 1
-  for (;;) {
-    const int c = w.next_chunk();
-    if (c < 0) break;
-    const int64_t r0 = static_cast<int64_t>(c) * kChunk;
-    const int nr = static_cast<int>(a.rows - r0 < kChunk ? a.rows - r0 : kChunk);
-    int2 cnt = make_int2(0, 0);
-    long long dg = 1;
-    int ot = 0;
-    if (lane < nr) {
-      cnt = a.counts[r0 + lane];
-      if (need_deg) dg = a.ep.deg[r0 + lane];
-      if (need_ot) ot = a.ep.other_touched[r0 + lane];
-    }
-#pragma unroll 1
-    for (int l = 0; l < nr; ++l) {
-      const int64_t r = r0 + l;
-      const int ni = __shfl_sync(0xffffffffu, cnt.x, l);
-      const int no = __shfl_sync(0xffffffffu, cnt.y, l);
-      const long long d = __shfl_sync(0xffffffffu, dg, l);
-      const bool other_t = __shfl_sync(0xffffffffu, ot, l) != 0;
-      Vf<W> side_y = splat<W>(0.0f), side_x = splat<W>(0.0f);
-      if (need_y) side_y = load_row<FV>(a.y + r * ld, a.feat, lane);
-      if (need_x) side_x = load_row<FV>(a.x + r * ld, a.feat, lane);
-      Vf<W> I = splat<W>(0.0f), O = splat<W>(0.0f);
-#pragma unroll 1
-      for (int role = 0; role < 2; ++role) {
-        const Vf<W> v = w.template role<IS_MAX>(role == 0 ? ni : no);
-        if (role == 0) I = v; else O = v;
-      }
-      Vf<W> out;
-      if (a.mask == 3) {
-        out = combine2<W>(a.ep.op, I, ni > 0, O, no > 0, d);
-      } else {
-        const Vf<W> v = (a.mask == 1) ? I : O;
-        const bool t = (a.mask == 1) ? ni > 0 : no > 0;
-        if (!(a.ep.flags & AG_EPI_COMBINE)) out = t ? v : splat<W>(0.0f);
-        else out = combine2<W>(a.ep.op, v, t, side_y, other_t, d);
-      }
-      if (need_x) out = vadd<W>(vscale<W>(a.ep.gin_scale, side_x), out);
-#pragma unroll
-      for (int h = 0; h < FV; ++h) {
-        const int f = h * 128 + lane * 4;
-        if (f < a.feat)
-          *reinterpret_cast<float4 *>(a.y + r * ld + f) = make_float4(
-              out.v[h * 4 + 0], out.v[h * 4 + 1], out.v[h * 4 + 2], out.v[h * 4 + 3]);
-      }
-    }
-  }
-}
-
-// ---------------------------------------------- stage-aligned layout build --
-__device__ __forceinline__ void intra_run(const int32_t *col, int64_t s, int64_t e, int64_t r,
-                                          int64_t B, int64_t &ia, int64_t &ib) {
-  if (B <= 0) { ia = ib = 0; return; }
-  const int64_t cb = (r / B) * B;
-  int64_t lo = s, hi = e;
-  while (lo < hi) { const int64_t m = (lo + hi) >> 1; if (col[m] < cb) lo = m + 1; else hi = m; }
-  ia = lo - s;
-  hi = e;
-  while (lo < hi) { const int64_t m = (lo + hi) >> 1; if (col[m] < cb + B) lo = m + 1; else hi = m; }
-  ib = lo - s;
-}
-
-__global__ void layout_count_kernel(int64_t rows, const int32_t *row_ptr, const int32_t *col,
-                                    int64_t B, int mask, int2 *counts, int32_t *nstages) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = row_ptr[r], e = row_ptr[r + 1];
-    int64_t ia, ib;
-    intra_run(col, s, e, r, B, ia, ib);
-    const int n1 = static_cast<int>(ib - ia);
-    const int ni = (mask & 1) ? n1 : 0;
-    const int no = (mask & 2) ? static_cast<int>(e - s) - n1 : 0;
-    counts[r] = make_int2(ni, no);
-    nstages[r] = role_stages(ni) + role_stages(no);
-  }
-}
-
-__global__ void layout_fill_kernel(int64_t rows, const int32_t *row_ptr, const int32_t *col,
-                                   const float *val, int64_t B, const int32_t *stage_ptr,
-                                   const int2 *counts, int32_t *scol, float *sval) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = row_ptr[r], e = row_ptr[r + 1];
-    int64_t ia, ib;
-    intra_run(col, s, e, r, B, ia, ib);
-    int64_t t = stage_ptr[r];
-    const int2 cn = counts[r];
-    for (int role = 0; role < 2; ++role) {
-      const int n = role == 0 ? cn.x : cn.y;
-      const int ns = role_stages(n);
-      for (int k = 0; k < ns; ++k, ++t) {
-        for (int j = 0; j < kSlots; ++j) {
-          const int item = (j == 0) ? (k == 0 ? 0 : -1) : 8 * k + j;
-          int32_t c = -1;
-          float v = 0.0f;
-          if (item >= 0 && item < n) {
-            int64_t ed;
-            if (role == 0) ed = s + ia + item;
-            else ed = (item < ia) ? s + item : s + ib + (item - ia);
-            c = col[ed];
-            v = val ? val[ed] : 1.0f;
-          }
-          scol[t * kSlots + j] = c;
-          sval[t * kSlots + j] = v;
-        }
-      }
-    }
-  }
-}
-
-// ------------------------------------------------------ long-row kernel ----
-// One warp per row (from a row list, or every row), register gathers straight
-// from global memory, the same role split / order / epilogue.  Serves rows
-// longer than kLong and feature widths the bulk path does not cover.
-struct LongArgs {
-  FusedArgs f;
-  const int32_t *list;  // nullptr: all rows
-  int64_t count;
-};
-
-// role item k -> edge id
-struct RoleMap {
-  int64_t s, a, b;
-  bool intra;
-  __device__ __forceinline__ int64_t edge(int64_t k) const {
-    if (intra) return a + k;
-    return (k < a - s) ? s + k : b + (k - (a - s));
-  }
-};
-
-template <int VEC>
-__device__ __forceinline__ Vf<VEC> g_contrib(const LongArgs &la, const RoleMap &m, int64_t k,
-                                             int f, bool raw) {
-  const int64_t e = m.edge(k);
-  const int32_t c = __ldg(la.f.col + e);
-  Vf<VEC> v = ldv<VEC>(la.f.x + static_cast<int64_t>(c) * la.f.feat + f);
-  if (!raw && la.f.val) v = vscale<VEC>(__ldg(la.f.val + e), v);
-  return v;
-}
-
-template <int VEC>
-__device__ __forceinline__ Vf<VEC> g_leaf(const LongArgs &la, const RoleMap &m, int64_t start,
-                                          int n, int f) {
-  Vf<VEC> res = splat<VEC>(-0.0f);
-  int i = 0;
-  if (n >= 8) {
-    Vf<VEC> r[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = g_contrib<VEC>(la, m, start + j, f, false);
-    const int mm = n - (n & 7);
-    for (i = 8; i < mm; i += 8) {
-      Vf<VEC> c[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) c[j] = g_contrib<VEC>(la, m, start + i + j, f, false);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = vadd<VEC>(r[j], c[j]);
-    }
-    res = vadd<VEC>(vadd<VEC>(vadd<VEC>(r[0], r[1]), vadd<VEC>(r[2], r[3])),
-                    vadd<VEC>(vadd<VEC>(r[4], r[5]), vadd<VEC>(r[6], r[7])));
-    i = mm;
-  }
-  Vf<VEC> c[7];
-#pragma unroll
-  for (int t = 0; t < 7; ++t)
-    if (i + t < n) c[t] = g_contrib<VEC>(la, m, start + i + t, f, false);
-#pragma unroll
-  for (int t = 0; t < 7; ++t)
-    if (i + t < n) res = vadd<VEC>(res, c[t]);
-  return res;
-}
-
-template <int VEC>
-__device__ __noinline__ Vf<VEC> g_pairwise(const LongArgs la, const RoleMap m, int64_t start,
-                                           int n, int f) {
-  int64_t st_start[kDepth];
-  int st_n[kDepth];
-  int st_stage[kDepth];
-  Vf<VEC> st_left[kDepth];
-  int sp = 0;
-  st_start[0] = start;
-  st_n[0] = n;
-  st_stage[0] = 0;
-  Vf<VEC> ret = splat<VEC>(0.0f);
-  while (sp >= 0) {
-    const int cn = st_n[sp];
-    if (cn <= kLeafN) {
-      ret = g_leaf<VEC>(la, m, st_start[sp], cn, f);
-      --sp;
-      continue;
-    }
-    int n2 = cn / 2;
-    n2 -= n2 & 7;
-    if (st_stage[sp] == 0) {
-      st_stage[sp] = 1;
-      st_start[sp + 1] = st_start[sp];
-      st_n[sp + 1] = n2;
-      st_stage[sp + 1] = 0;
-      ++sp;
-    } else if (st_stage[sp] == 1) {
-      st_left[sp] = ret;
-      st_stage[sp] = 2;
-      st_start[sp + 1] = st_start[sp] + n2;
-      st_n[sp + 1] = cn - n2;
-      st_stage[sp + 1] = 0;
-      ++sp;
-    } else {
-      ret = vadd<VEC>(st_left[sp], ret);
-      --sp;
-    }
-  }
-  return ret;
-}
-
-template <int VEC, bool IS_MAX>
-__device__ __forceinline__ Vf<VEC> g_role(const LongArgs &la, const RoleMap &m, int64_t n,
-                                          int f) {
-  if (n <= 0) return splat<VEC>(0.0f);
+template <int VEC, bool W>
+template <bool IS_MAX>
+__device__ __forceinline__ Lv<VEC> RowWarp<VEC, W>::role(int32_t e0, int32_t n) {
+  if (n <= 0) return lv_splat<VEC>(0.0f);
+  end = e0 + n;
+  fill(e0);
   if constexpr (IS_MAX) {
-    Vf<VEC> acc = g_contrib<VEC>(la, m, 0, f, true);
-    int64_t k = 1;
-    for (; k + 4 <= n; k += 4) {
-      Vf<VEC> c[4];
+    Lv<VEC> acc = item<true>(e0);
+#pragma unroll 1
+    for (int32_t b = e0 + 1; b < end; b += 8) {
+      const int cnt = end - b < 8 ? end - b : 8;
+      ensure(b, cnt);
+      Lv<VEC> c[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) c[j] = g_contrib<VEC>(la, m, k + j, f, true);
+      for (int j = 0; j < 8; ++j) c[j] = item<true>(b + (j < cnt ? j : 0));
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc = vmax<VEC>(acc, c[j]);
+      for (int j = 0; j < 8; ++j) acc = lv_max<VEC>(acc, c[j]);  // duplicates are harmless
     }
-    for (; k < n; ++k) acc = vmax<VEC>(acc, g_contrib<VEC>(la, m, k, f, true));
     return acc;
   } else {
-    Vf<VEC> c0 = g_contrib<VEC>(la, m, 0, f, false);
-    if (n == 1) return c0;
-    return vadd<VEC>(c0, g_pairwise<VEC>(la, m, 1, static_cast<int>(n - 1), f));
+    const Lv<VEC> c0 = item<false>(e0);
+    const int32_t m = n - 1;
+    if (m == 0) return c0;
+    if (m < 8) return lv_add<VEC>(c0, seq(lv_splat<VEC>(-0.0f), e0 + 1, m), one);
+    if (m <= kLeafN) return lv_add<VEC>(c0, leaf(e0 + 1, m), one);
+    return lv_add<VEC>(c0, pairwise_long_fn<VEC, W>(*this, e0 + 1, m), one);
   }
 }
 
-template <int VEC, bool IS_MAX>
-__global__ void __launch_bounds__(256) long_row_kernel(LongArgs la) {
-  const FusedArgs &a = la.f;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const int64_t n_items = la.list ? la.count : a.rows;
-  for (int64_t it = gw; it < n_items; it += nw) {
-    const int64_t r = la.list ? la.list[it] : it;
-    const int64_t s = a.row_ptr[r], e = a.row_ptr[r + 1];
-    int64_t ra = s, rb = s;
-    if (a.block > 0) {  // intra run: binary search of [cB, cB+B) in the sorted row
-      const int64_t cb = (r / a.block) * a.block;
-      int64_t lo = s, hi = e;
-      while (lo < hi) { const int64_t m = (lo + hi) >> 1; if (a.col[m] < cb) lo = m + 1; else hi = m; }
-      ra = lo;
-      hi = e;
-      while (lo < hi) {
-        const int64_t m = (lo + hi) >> 1;
-        if (a.col[m] < cb + a.block) lo = m + 1; else hi = m;
-      }
-      rb = lo;
-    }
-    const int64_t ni = (a.mask & 1) ? rb - ra : 0;
-    const int64_t no = (a.mask & 2) ? (e - s) - (rb - ra) : 0;
-    const RoleMap mi{s, ra, rb, true}, mo{s, ra, rb, false};
-    for (int f0 = 0; f0 < a.feat; f0 += 32 * VEC) {
-      const int f = f0 + lane * VEC;
-      if (f >= a.feat) continue;
-      Vf<VEC> I = g_role<VEC, IS_MAX>(la, mi, ni, f);
-      Vf<VEC> O = g_role<VEC, IS_MAX>(la, mo, no, f);
-      Vf<VEC> out;
-      if (a.mask == 3) {
-        const int64_t d = (a.ep.op == AG_OP_MEAN && a.ep.deg) ? a.ep.deg[r] : 1;
-        out = combine2<VEC>(a.ep.op, I, ni > 0, O, no > 0, d);
-        if (a.ep.flags & AG_EPI_GIN)
-          out = vadd<VEC>(vscale<VEC>(a.ep.gin_scale, ldv<VEC>(a.x + r * a.feat + f)), out);
-        stv<VEC>(a.y + r * a.feat + f, out);
-      } else {
-        const bool t = (a.mask == 1) ? ni > 0 : no > 0;
-        if (a.ep.flags & AG_EPI_EMPTY_OTHER) {
-          const int64_t d = (a.ep.op == AG_OP_MEAN && a.ep.deg) ? a.ep.deg[r] : 1;
-          out = combine2<VEC>(a.ep.op, (a.mask == 1) ? I : O, t, splat<VEC>(0.0f), false, d);
-          if (a.ep.flags & AG_EPI_GIN)
-            out = vadd<VEC>(vscale<VEC>(a.ep.gin_scale, ldv<VEC>(a.x + r * a.feat + f)), out);
-          stv<VEC>(a.y + r * a.feat + f, out);
-        } else {
-          epilogue_store<VEC>(a.ep, a.y, r, f, (a.mask == 1) ? I : O, t);
-        }
-      }
-    }
+__device__ __forceinline__ int64_t range_start(const GArgs &a, int k) {
+  if (k <= 0) return 0;
+  if (k >= a.ranges) return a.rows;
+  const int64_t target = a.cost_total / a.ranges * k + (a.cost_total % a.ranges) * k / a.ranges;
+  int64_t lo = 0, hi = a.rows;  // first r with cost(r) >= target
+  while (lo < hi) {
+    const int64_t m = (lo + hi) >> 1;
+    if (static_cast<int64_t>(a.row_ptr[m]) + kRowCost * m < target) lo = m + 1;
+    else hi = m;
   }
-}
-
-inline int pick_vec(int64_t feat, const void *x, const void *y) {
-  auto al = [](const void *p, int b) { return (reinterpret_cast<uintptr_t>(p) % b) == 0; };
-  if (feat % 4 == 0 && al(x, 16) && al(y, 16)) return 4;
-  if (feat % 2 == 0 && al(x, 8) && al(y, 8)) return 2;
-  return 1;
+  return lo;
 }
 
 template <int VEC>
-int launch_long(const LongArgs &la, bool is_max, cudaStream_t st) {
-  const int64_t n = la.list ? la.count : la.f.rows;
-  if (n == 0) return AG_OK;
-  int64_t blocks = (n * 32 + 255) / 256;
-  const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
-  if (blocks > cap) blocks = cap;
-  if (is_max) long_row_kernel<VEC, true><<<(int)blocks, 256, 0, st>>>(la);
-  else long_row_kernel<VEC, false><<<(int)blocks, 256, 0, st>>>(la);
-  AG_LAUNCH_CHECK("long_row_kernel");
-  return AG_OK;
+__device__ __forceinline__ Vf<VEC> combine2(int op, const Vf<VEC> &I, bool ti, const Vf<VEC> &O,
+                                            bool to, int64_t deg) {
+  if (op == AG_OP_SUM) return vadd<VEC>(I, O);
+  if (op == AG_OP_MEAN) {
+    const float d = static_cast<float>(deg < 1 ? 1 : deg);
+    Vf<VEC> s = vadd<VEC>(I, O), r;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) r.v[i] = __fdiv_rn(s.v[i], d);
+    return r;
+  }
+  if (ti && to) return vmax<VEC>(I, O);
+  if (ti) return I;
+  if (to) return O;
+  return splat<VEC>(0.0f);
 }
 
-int launch_long_any(const LongArgs &la, bool is_max, cudaStream_t st) {
-  switch (pick_vec(la.f.feat, la.f.x, la.f.y)) {
-    case 4: return launch_long<4>(la, is_max, st);
-    case 2: return launch_long<2>(la, is_max, st);
-    default: return launch_long<1>(la, is_max, st);
+template <int VEC, bool IS_MAX, bool W>
+__global__ void __launch_bounds__(kThreads, 2) gather_kernel(GArgs a) {
+  constexpr int T = 32 * VEC;
+  __shared__ int64_t bounds[2];
+  __shared__ __align__(16) uint64_t wins[kThreads / 32][kWin * 2];
+  const int tile = static_cast<int>(blockIdx.x % a.ntiles);
+  const int range = static_cast<int>(blockIdx.x / a.ntiles);
+  if (threadIdx.x < 2) bounds[threadIdx.x] = range_start(a, range + threadIdx.x);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  RowWarp<VEC, W> w;
+  w.win = static_cast<uint32_t>(__cvta_generic_to_shared(wins[warp]));
+  w.col = a.col;
+  w.val = a.val;
+  w.feat = static_cast<uint32_t>(a.feat);
+  w.lane = threadIdx.x & 31;
+  w.one = pk(a.one, a.one);
+  const int64_t fcol = static_cast<int64_t>(tile) * T + w.lane * VEC;
+  const bool act = fcol < a.feat;
+  w.xl = a.x + (act ? fcol : 0);
+  w.p = 0;
+  w.end = 0;
+  const int64_t ld = a.feat;
+  const int nwarps = blockDim.x >> 5;
+#pragma unroll 1
+  for (int64_t r = bounds[0] + warp; r < bounds[1]; r += nwarps) {
+    const int32_t s = a.row_ptr[r], e = a.row_ptr[r + 1];
+    const int32_t m = a.mid ? a.mid[r] : (a.mask == 1 ? e : s);
+    const int32_t ni = (a.mask & 1) ? m - s : 0;
+    const int32_t no = (a.mask & 2) ? e - m : 0;
+    const Vf<VEC> I = lv_out<VEC>(w.template role<IS_MAX>(s, ni));
+    const Vf<VEC> O = lv_out<VEC>(w.template role<IS_MAX>(m, no));
+    if (!act) continue;
+    float *yp = a.y + r * ld + fcol;
+    const int64_t d = (a.ep.op == AG_OP_MEAN && a.ep.deg) ? a.ep.deg[r] : 1;
+    Vf<VEC> out;
+    if (a.mask == 3) {
+      out = combine2<VEC>(a.ep.op, I, ni > 0, O, no > 0, d);
+    } else {
+      const Vf<VEC> v = (a.mask == 1) ? I : O;
+      const bool t = (a.mask == 1) ? ni > 0 : no > 0;
+      if (!(a.ep.flags & AG_EPI_COMBINE)) {
+        out = t ? v : splat<VEC>(0.0f);
+      } else if (a.ep.flags & AG_EPI_EMPTY_OTHER) {
+        out = combine2<VEC>(a.ep.op, v, t, splat<VEC>(0.0f), false, d);
+      } else {
+        const bool ot = a.ep.other_touched ? a.ep.other_touched[r] != 0 : false;
+        out = combine2<VEC>(a.ep.op, v, t, ldv_rw<VEC>(yp), ot, d);
+      }
+    }
+    if (a.ep.flags & AG_EPI_GIN)
+      out = vadd<VEC>(vscale<VEC>(a.ep.gin_scale, ldv<VEC>(a.x + r * ld + fcol)), out);
+    if (a.ep.flags & AG_EPI_RELU_MASK) {
+      const Vf<VEC> h = ldv<VEC>(a.ep.relu_src + r * ld + fcol);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) out.v[i] = h.v[i] > 0.0f ? out.v[i] : 0.0f;
+    }
+    stv<VEC>(yp, out);
   }
 }
 
-template <int FV>
-int launch_fused(FusedArgs a, bool is_max, cudaStream_t st) {
-  a.stages = FV == 1 ? 4 : 2;
-  const int hdr = (8 * a.stages + 4 * kSlots * a.stages + 16 + 127) / 128 * 128;
-  const int ring = a.stages * kSlots * a.feat * 4;
-  a.warp_bytes = hdr + (ring + 127) / 128 * 128;
-  const int budget = 220 * 1024;
-  const int max_warps = FV == 1 ? 16 : 12;
-  a.warps = std::max(1, std::min(max_warps, budget / a.warp_bytes));
-  a.one = 1.0f;
-  const int smem = a.warps * a.warp_bytes;
-  const int64_t nchunks = (a.rows + kChunk - 1) / kChunk;
-  auto k = is_max ? fused_kernel<FV, true> : fused_kernel<FV, false>;
-  AG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+// -------------------------------------------------- role-ordered CSR build --
+__global__ void role_csr_kernel(int64_t rows, const int32_t *row_ptr, const int32_t *col,
+                                const float *val, int64_t B, int32_t *rcol, float *rval,
+                                int32_t *mid) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = row_ptr[r], e = row_ptr[r + 1];
+    const int64_t cb = (r / B) * B;
+    int64_t lo = s, hi = e;
+    while (lo < hi) { const int64_t m = (lo + hi) >> 1; if (col[m] < cb) lo = m + 1; else hi = m; }
+    const int64_t ia = lo;
+    hi = e;
+    while (lo < hi) { const int64_t m = (lo + hi) >> 1; if (col[m] < cb + B) lo = m + 1; else hi = m; }
+    const int64_t ib = lo;
+    int64_t t = s;
+    for (int64_t k = ia; k < ib; ++k, ++t) { rcol[t] = col[k]; if (rval) rval[t] = val[k]; }
+    for (int64_t k = s; k < ia; ++k, ++t) { rcol[t] = col[k]; if (rval) rval[t] = val[k]; }
+    for (int64_t k = ib; k < e; ++k, ++t) { rcol[t] = col[k]; if (rval) rval[t] = val[k]; }
+    mid[r] = static_cast<int32_t>(s + (ib - ia));
+  }
+}
+
+int env_int(const char *name, int dflt) {
+  const char *v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+template <int VEC>
+int launch_gather(GArgs a, bool is_max, cudaStream_t st) {
+  constexpr int T = 32 * VEC;
+  auto k = is_max ? (a.val ? gather_kernel<VEC, true, true> : gather_kernel<VEC, true, false>)
+                  : (a.val ? gather_kernel<VEC, false, true> : gather_kernel<VEC, false, false>);
+  // prefer L1 over shared memory: the gathers' reuse lives in L1
+  AG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 8));
   int per_sm = 0;
-  AG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, a.warps * 32, smem));
+  AG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0));
   if (per_sm < 1) per_sm = 1;
-  int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;
-  const int64_t need = (nchunks + a.warps - 1) / a.warps;
-  if (grid > need) grid = need;
-  if (grid < 1) grid = 1;
-  Scratch ctr;
-  AG_CUDA(ctr.alloc(sizeof(unsigned int), st));
-  AG_CUDA(cudaMemsetAsync(ctr.ptr, 0, sizeof(unsigned int), st));
-  a.chunk_ctr = ctr.as<unsigned int>();
-  k<<<(int)grid, a.warps * 32, smem, st>>>(a);
-  AG_LAUNCH_CHECK("fused_kernel");
+  a.ntiles = static_cast<int>((a.feat + T - 1) / T);
+  const int waves = std::max(1, env_int("AG_GATHER_WAVES", 1));
+  int64_t ranges = static_cast<int64_t>(sm_count()) * per_sm * waves / a.ntiles;
+  const int64_t max_ranges = (a.rows + 63) / 64;  // >= 64 rows per range
+  ranges = std::max<int64_t>(1, std::min(ranges, max_ranges));
+  a.ranges = static_cast<int>(ranges);
+  const int64_t grid = ranges * a.ntiles;
+  k<<<(unsigned)grid, kThreads, 0, st>>>(a);
+  AG_LAUNCH_CHECK("gather_kernel");
   return AG_OK;
 }
 
@@ -821,76 +521,49 @@ int launch_fused(FusedArgs a, bool is_max, cudaStream_t st) {
 
 using namespace ag;
 
-extern "C" int ag_stage_layout_count(int64_t num_rows, const int32_t *row_ptr,
-                                     const int32_t *col_idx, int64_t block_size,
-                                     int32_t role_mask, int32_t *stage_ptr, int32_t *counts,
-                                     int64_t *num_stages_host, void *stream) {
-  *num_stages_host = 0;
-  if (block_size < 0) return fail(AG_ERR_VALUE, "block_size must be >= 0");
-  if (role_mask < 1 || role_mask > 3) return fail(AG_ERR_VALUE, "role_mask must be 1, 2 or 3");
-  if (block_size == 0 && role_mask != 2)
-    return fail(AG_ERR_VALUE, "block_size 0 (no split) requires role_mask 2");
-  cudaStream_t st = as_stream(stream);
-  const int64_t n = num_rows + 1;
-  Scratch ns, tmp;
-  AG_CUDA(ns.alloc(n * sizeof(int32_t), st));
-  AG_CUDA(cudaMemsetAsync(ns.ptr, 0, n * sizeof(int32_t), st));
-  if (num_rows > 0) {
-    layout_count_kernel<<<grid_for(num_rows, 256), 256, 0, st>>>(
-        num_rows, row_ptr, col_idx, block_size, role_mask, reinterpret_cast<int2 *>(counts),
-        ns.as<int32_t>());
-    AG_LAUNCH_CHECK("layout_count_kernel");
-  }
-  size_t bytes = 0;
-  AG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, ns.as<int32_t>(), stage_ptr, (int)n, st));
-  AG_CUDA(tmp.alloc(bytes, st));
-  AG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, bytes, ns.as<int32_t>(), stage_ptr, (int)n, st));
-  int32_t total = 0;
-  AG_CUDA(cudaMemcpyAsync(&total, stage_ptr + num_rows, 4, cudaMemcpyDeviceToHost, st));
-  AG_CUDA(cudaStreamSynchronize(st));
-  *num_stages_host = total;
-  return AG_OK;
-}
-
-extern "C" int ag_stage_layout_fill(int64_t num_rows, const int32_t *row_ptr,
-                                    const int32_t *col_idx, const float *val, int64_t block_size,
-                                    const int32_t *stage_ptr, const int32_t *counts,
-                                    int32_t *stage_col, float *stage_val, void *stream) {
+extern "C" int ag_role_csr_build(int64_t num_rows, const int32_t *row_ptr, const int32_t *col_idx,
+                                 const float *val, int64_t block_size, int32_t *role_col,
+                                 float *role_val, int32_t *role_mid, void *stream) {
+  if (num_rows < 0) return fail(AG_ERR_VALUE, "negative sizes");
+  if (block_size < 1) return fail(AG_ERR_VALUE, "block_size must be >= 1");
+  if (val != nullptr && role_val == nullptr)
+    return fail(AG_ERR_VALUE, "role_val is required for a weighted CSR");
   if (num_rows == 0) return AG_OK;
-  layout_fill_kernel<<<grid_for(num_rows, 128), 128, 0, as_stream(stream)>>>(
-      num_rows, row_ptr, col_idx, val, block_size, stage_ptr,
-      reinterpret_cast<const int2 *>(counts), stage_col, stage_val);
-  AG_LAUNCH_CHECK("layout_fill_kernel");
+  role_csr_kernel<<<grid_for(num_rows, 128), 128, 0, as_stream(stream)>>>(
+      num_rows, row_ptr, col_idx, val, block_size, role_col, val ? role_val : nullptr, role_mid);
+  AG_LAUNCH_CHECK("role_csr_kernel");
   return AG_OK;
 }
 
-extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int64_t block_size,
-                             int32_t role_mask, const int32_t *row_ptr, const int32_t *col_idx,
-                             const float *val, const int32_t *stage_ptr, const int32_t *counts,
-                             const int32_t *stage_col, const float *stage_val, const float *x,
-                             float *y, int32_t op, int32_t epi_flags,
+extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
+                             const int32_t *row_ptr, const int32_t *role_mid,
+                             const int32_t *col_idx, const float *val, int64_t num_edges,
+                             const float *x, float *y, int32_t op, int32_t epi_flags,
                              const uint8_t *other_touched, const int64_t *deg, float gin_scale,
-                             void *stream) {
-  if (num_rows < 0 || feat < 0) return fail(AG_ERR_VALUE, "negative sizes");
+                             const float *relu_src, void *stream) {
+  if (num_rows < 0 || feat < 0 || num_edges < 0) return fail(AG_ERR_VALUE, "negative sizes");
   if (op < AG_OP_SUM || op > AG_OP_MAX) return fail(AG_ERR_KERNEL, "unknown op %d", op);
   if (role_mask < 1 || role_mask > 3) return fail(AG_ERR_VALUE, "role_mask must be 1, 2 or 3");
-  if (block_size < 0) return fail(AG_ERR_VALUE, "block_size must be >= 0");
-  if (block_size == 0 && role_mask != 2)
-    return fail(AG_ERR_VALUE, "block_size 0 (no split) requires role_mask 2");
+  if (role_mid == nullptr && role_mask == 3)
+    return fail(AG_ERR_VALUE, "role_mask 3 needs the role-ordered CSR (role_mid)");
   if (op == AG_OP_MEAN && deg == nullptr && (role_mask == 3 || (epi_flags & AG_EPI_COMBINE)))
     return fail(AG_ERR_KERNEL, "mean combine requires the full-graph degree vector");
+  if ((epi_flags & AG_EPI_RELU_MASK) && relu_src == nullptr)
+    return fail(AG_ERR_VALUE, "AG_EPI_RELU_MASK needs relu_src");
   if (num_rows == 0 || feat == 0) return AG_OK;
-  if (num_rows > 2147483647LL || block_size > 2147483647LL)
-    return fail(AG_ERR_VALUE, "too many rows");
+  if (num_rows > 2147483647LL || num_edges > 2147483647LL)
+    return fail(AG_ERR_VALUE, "too many rows or edges for int32 CSR");
+  if (num_rows * feat > 4294967295LL)
+    return fail(AG_ERR_VALUE, "feature matrix too large for 32-bit row offsets");
   cudaStream_t st = as_stream(stream);
-  FusedArgs a{num_rows, static_cast<int>(feat), static_cast<int>(block_size), role_mask, row_ptr,
-              col_idx, val, x, y, Epi{op, epi_flags, other_touched, deg, x, feat, gin_scale},
-              stage_ptr, reinterpret_cast<const int2 *>(counts), stage_col, stage_val, nullptr,
-              0, 0, 2, 1.0f};
+  GArgs a{num_rows, static_cast<int>(feat), role_mask, row_ptr, role_mid, col_idx, val, x, y,
+          Epi{op, epi_flags, other_touched, deg, x, feat, gin_scale, relu_src}, 1, 1, 0, 1.0f};
+  a.cost_total = num_edges + kRowCost * num_rows;
   const bool is_max = op == AG_OP_MAX;
-  const bool bulk_ok = feat % 4 == 0 && feat <= 256 && stage_ptr && counts && stage_col &&
-                       stage_val && (reinterpret_cast<uintptr_t>(x) % 16) == 0 &&
-                       (reinterpret_cast<uintptr_t>(y) % 16) == 0;
-  if (!bulk_ok) return launch_long_any(LongArgs{a, nullptr, 0}, is_max, st);
-  return feat <= 128 ? launch_fused<1>(a, is_max, st) : launch_fused<2>(a, is_max, st);
+  const bool v4 = feat % 4 == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0 &&
+                  (reinterpret_cast<uintptr_t>(y) % 16) == 0;
+  if (!v4) return launch_gather<1>(a, is_max, st);
+  const int vec = env_int("AG_GATHER_VEC", 4);
+  if (vec == 8 && feat % 8 == 0 && feat > 128) return launch_gather<8>(a, is_max, st);
+  return launch_gather<4>(a, is_max, st);
 }

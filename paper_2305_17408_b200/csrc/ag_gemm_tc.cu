@@ -1,0 +1,553 @@
+// The dense update GEMMs of the GCN/GIN layers on the 5th-generation tensor
+// cores (tcgen05, kind::tf32) with fp32-faithful 3xTF32 splitting.
+//
+//   forward  out = agg @ W          A = agg [M=V][K] (K-major), B = W [K][N] (N-major)
+//   backward dH  = G @ W^T          A = G   [V][K]   (K-major), B = W [N][K] (K-major)
+//            dW  = agg^T @ G        A = agg [K=V][M] (M-major), B = G [K][N] (N-major)
+// (models.py:99, :112 `agg @ W`; the backward products are the composed
+// training step of SURVEY.md §8c.)
+//
+// 3xTF32: every fp32 operand x is split in shared memory into hi = x with the
+// low 13 mantissa bits cleared (exactly representable in tf32) and
+// lo = x - hi (exact in fp32); the tile product is accumulated in fp32 TMEM as
+// A_hi*B_hi + A_hi*B_lo + A_lo*B_hi, i.e. within a few ulp of an fp32 GEMM
+// (the dropped A_lo*B_lo term is ~2^-22 relative).
+//
+// Kernel anatomy (one CTA per SM, persistent over 128 x BN output tiles and,
+// for the skinny dW product, K splits):
+//   warp 0        TMA producer: A and B k-blocks (32 fp32 = one 128-byte
+//                 swizzle row) into a 2-3 stage shared-memory ring, SWIZZLE_128B
+//   warps 2-5     splitters: x -> hi (in place) and lo (second buffer), then
+//                 fence.proxy.async so the tensor core sees the writes
+//   warp 1        TMEM allocator + single-thread tcgen05.mma issuer (3 MMAs per
+//                 K=8 step), tcgen05.commit frees ring slots / publishes tiles
+//   warps 6-9     epilogue: tcgen05.ld 32x32b -> alpha/beta/ReLU -> global,
+//                 double-buffered TMEM accumulators so it overlaps the next tile
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "ag_common.cuh"
+
+namespace ag {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 32;  // fp32 elements per k-block: one 128-byte swizzle row
+constexpr int kThreads = 320;
+constexpr int kConvWarp0 = 2, kEpiWarp0 = 6;
+
+struct TcArgs {
+  int64_t M, N, K;
+  float *C;         // output (splits == 1) or partial workspace [splits][M][N]
+  int64_t ldc;
+  float alpha, beta;
+  int relu;
+  int m_tiles, n_tiles, splits;
+  int64_t k_per_split;  // multiple of BK
+};
+
+// ------------------------------------------------------------ PTX helpers --
+__device__ __forceinline__ uint32_t su32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                   su32(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+          su32(b)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap *map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Shared-memory matrix descriptor (sm_100 version 1).  K-major operands use
+// SWIZZLE_128B (layout 2: 8 rows x 128 B atoms, 16-byte chunks XOR row%8);
+// tf32 MN-major operands must use SWIZZLE_128B_BASE32B (layout 1: 4 K-rows x
+// 128 B atoms, 32-byte chunks XOR row%4), which TMA writes with
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
+                                              bool mn) {
+  return (static_cast<uint64_t>((addr >> 4) & 0x3FFFu)) |
+         (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) |
+         ((mn ? 1ull : 2ull) << 61);
+}
+
+// Instruction descriptor: D f32, A/B tf32, majors, N, M = 128.
+__host__ __device__ constexpr uint32_t instr_desc(bool a_mn, bool b_mn, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
+         (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(BM >> 4) << 24);
+}
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 4;   // 16 KB
+  static constexpr int B_BYTES = BN * BK * 4;   // BN * 128 B
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES = STAGE * 3 <= 200 * 1024 ? 3 : 2;
+  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64
+                                 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int SMEM = STAGES * STAGE + 1024 /* align */ + 256 /* barriers */;
+};
+
+// split x (fp32) into hi (in place) and lo, n4 float4s
+__device__ __forceinline__ void split_tile(float4 *hi, float4 *lo, int n4, int t, int nt) {
+  for (int i = t; i < n4; i += nt) {
+    float4 v = hi[i], h, l;
+    h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+    h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+    h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+    h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    l.x = __fsub_rn(v.x, h.x);
+    l.y = __fsub_rn(v.y, h.y);
+    l.z = __fsub_rn(v.z, h.z);
+    l.w = __fsub_rn(v.w, h.w);
+    hi[i] = h;
+    lo[i] = l;
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                   const __grid_constant__ CUtensorMap tmB, TcArgs g) {
+  using C = Cfg<BN>;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE);
+  uint64_t *conv = full + C::STAGES;
+  uint64_t *empty = conv + C::STAGES;
+  uint64_t *tfull = empty + C::STAGES;  // [2]
+  uint64_t *tempty = tfull + 2;         // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tiles_mn = static_cast<int64_t>(g.m_tiles) * g.n_tiles;
+  const int64_t total = tiles_mn * g.splits;
+  const int nkb_full = static_cast<int>(g.k_per_split / BK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // k-blocks of tile t (the last split may be shorter)
+  auto tile_kblocks = [&](int64_t t, int64_t &k0) -> int {
+    const int64_t s = t / tiles_mn;
+    k0 = s * g.k_per_split;
+    const int64_t k1 = std::min<int64_t>(g.K, k0 + g.k_per_split);
+    const int64_t nk = (k1 - k0 + BK - 1) / BK;
+    return static_cast<int>(nk < nkb_full ? nk : nkb_full);
+  };
+
+  if (warp == 0) {
+    // ----------------------------------------------------- TMA producer --
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        const int64_t mn = t % tiles_mn;
+        const int m0 = static_cast<int>((mn / g.n_tiles) * BM);
+        const int n0 = static_cast<int>((mn % g.n_tiles) * BN);
+        int64_t k0;
+        const int nkb = tile_kblocks(t, k0);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          unsigned char *st = smem + stage * C::STAGE;
+          unsigned char *sa = st, *sb = st + 2 * C::A_BYTES;
+          mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+          const int kk = static_cast<int>(k0 + static_cast<int64_t>(kb) * BK);
+          if (A_MN) {  // boxes {32 (m), 32 (k)}: 4 KB each, LBO apart
+#pragma unroll
+            for (int c = 0; c < BM / 32; ++c) tma_load_2d(sa + c * 4096, &tmA, &full[stage],
+                                                          m0 + 32 * c, kk);
+          } else {  // box {32 (k), 128 (m)}
+            tma_load_2d(sa, &tmA, &full[stage], kk, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) tma_load_2d(sb + c * 4096, &tmB, &full[stage],
+                                                          n0 + 32 * c, kk);
+          } else {
+            tma_load_2d(sb, &tmB, &full[stage], kk, n0);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ----------------------------------------------------- MMA issuer ----
+    constexpr uint32_t idesc = instr_desc(A_MN, B_MN, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+      int64_t k0;
+      const int nkb = tile_kblocks(t, k0);
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&conv[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t st = su32(smem + stage * C::STAGE);
+          const uint32_t a_hi = st, a_lo = st + C::A_BYTES;
+          const uint32_t b_hi = st + 2 * C::A_BYTES, b_lo = b_hi + C::B_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            // K=8 step: K-major advances 32 B inside the swizzle row, MN-major
+            // advances 8 K-rows (two 512 B atoms, 1 KB)
+            const uint32_t ao = A_MN ? ks * 1024 : ks * 32;
+            const uint32_t bo = B_MN ? ks * 1024 : ks * 32;
+            // MN-major: LBO = next 32-element MN chunk (one 4 KB TMA box),
+            // SBO = next 4-row K atom (512 B); K-major: SBO = next 8-row group
+            const uint32_t albo = A_MN ? 4096 : 16, asbo = A_MN ? 512 : 1024;
+            const uint32_t blbo = B_MN ? 4096 : 16, bsbo = B_MN ? 512 : 1024;
+            const uint64_t dah = smem_desc(a_hi + ao, albo, asbo, A_MN);
+            const uint64_t dal = smem_desc(a_lo + ao, albo, asbo, A_MN);
+            const uint64_t dbh = smem_desc(b_hi + bo, blbo, bsbo, B_MN);
+            const uint64_t dbl = smem_desc(b_lo + bo, blbo, bsbo, B_MN);
+            const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
+            tc_mma_tf32(d, dal, dbh, idesc, first);
+            tc_mma_tf32(d, dah, dbl, idesc, 1u);
+            tc_mma_tf32(d, dah, dbh, idesc, 1u);
+          }
+          tc_commit(&empty[stage]);
+          if (kb == nkb - 1) tc_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (nkb == 0 && lane == 0) tc_commit(&tfull[acc]);  // (K == 0: nothing to do)
+      __syncwarp();
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else if (warp < kEpiWarp0) {
+    // ------------------------------------------------------- splitters ---
+    const int t_id = threadIdx.x - kConvWarp0 * 32;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+      int64_t k0;
+      const int nkb = tile_kblocks(t, k0);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        unsigned char *st = smem + stage * C::STAGE;
+        split_tile(reinterpret_cast<float4 *>(st), reinterpret_cast<float4 *>(st + C::A_BYTES),
+                   C::A_BYTES / 16, t_id, 128);
+        split_tile(reinterpret_cast<float4 *>(st + 2 * C::A_BYTES),
+                   reinterpret_cast<float4 *>(st + 2 * C::A_BYTES + C::B_BYTES),
+                   C::B_BYTES / 16, t_id, 128);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[stage]);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    // -------------------------------------------------------- epilogue ---
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+      const int64_t s = t / tiles_mn;
+      const int64_t mn = t % tiles_mn;
+      const int64_t m0 = (mn / g.n_tiles) * BM;
+      const int64_t n0 = (mn % g.n_tiles) * BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t row = m0 + q * 32 + lane;
+      float *crow;
+      bool direct = g.splits == 1;
+      if (direct) crow = g.C + row * g.ldc;
+      else crow = g.C + (s * g.M + row) * g.N;
+      const bool vec_ok = ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
+                          (direct ? (g.ldc % 4 == 0) : (g.N % 4 == 0));
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                      static_cast<uint32_t>(acc * BN + c), v);
+        if (row < g.M) {
+          const int64_t nb = n0 + c;
+          if (direct) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float o = g.alpha * v[i];
+              if (g.beta != 0.0f && nb + i < g.N) o = fmaf(g.beta, crow[nb + i], o);
+              if (g.relu) o = fmaxf(o, 0.0f);
+              v[i] = o;
+            }
+          }
+          if (vec_ok && nb + 16 <= g.N) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+              *reinterpret_cast<float4 *>(crow + nb + i) =
+                  make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (nb + i < g.N) crow[nb + i] = v[i];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+__global__ void splitk_sum_kernel(int64_t M, int64_t N, int splits, const float *part, float *C,
+                                  int64_t ldc, float alpha, float beta, int relu) {
+  const int64_t n = M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.0f;
+    for (int p = 0; p < splits; ++p) s += part[p * n + i];  // fixed order: deterministic
+    const int64_t m = i / N, c = i % N;
+    float v = alpha * s;
+    if (beta != 0.0f) v = fmaf(beta, C[m * ldc + c], v);
+    if (relu) v = fmaxf(v, 0.0f);
+    C[m * ldc + c] = v;
+  }
+}
+
+// ------------------------------------------------------------- host side --
+using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                              const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                              const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 2-D fp32 tensor map: inner dim `inner` (contiguous), outer dim `outer` with
+// row stride ld (elements); box {32, box_outer}, 128-byte swizzle (32-byte
+// atoms for MN-major operands), OOB -> 0.
+int make_map(CUtensorMap *m, const float *base, int64_t inner, int64_t outer, int64_t ld,
+             int box_outer, bool mn) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return fail(AG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint32_t box[2] = {32, static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims,
+                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(AG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return AG_OK;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, TcArgs g, cudaStream_t st) {
+  using C = Cfg<BN>;
+  auto k = tc_gemm_kernel<BN, A_MN, B_MN>;
+  AG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  const int64_t total = static_cast<int64_t>(g.m_tiles) * g.n_tiles * g.splits;
+  const int grid = static_cast<int>(std::min<int64_t>(total, sm_count()));
+  k<<<grid, kThreads, C::SMEM, st>>>(ma, mb, g);
+  AG_LAUNCH_CHECK("tc_gemm_kernel");
+  return AG_OK;
+}
+
+template <int BN>
+int launch_bn(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &mb,
+              const TcArgs &g, cudaStream_t st) {
+  if (!a_mn && b_mn) return launch_tc<BN, false, true>(ma, mb, g, st);
+  if (!a_mn && !b_mn) return launch_tc<BN, false, false>(ma, mb, g, st);
+  if (a_mn && b_mn) return launch_tc<BN, true, true>(ma, mb, g, st);
+  return launch_tc<BN, true, false>(ma, mb, g, st);
+}
+
+}  // namespace
+}  // namespace ag
+
+using namespace ag;
+
+extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                              int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
+                              float *C, int64_t ldc, float alpha, float beta, int32_t epilogue,
+                              void *stream) {
+  if (M < 0 || N < 0 || K < 0) return fail(AG_ERR_VALUE, "negative GEMM sizes");
+  if (M == 0 || N == 0) return AG_OK;
+  const bool a_mn = trans_a != 0;  // A stored [K][M]
+  const bool b_mn = trans_b == 0;  // B stored [K][N]
+  auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al16(A) || !al16(B) || (lda % 4) || (ldb % 4))
+    return fail(AG_ERR_VALUE, "tensor-core GEMM needs 16-byte aligned operands and row strides");
+  if (M > 2147483647LL || N > 2147483647LL || K > 2147483647LL)
+    return fail(AG_ERR_VALUE, "GEMM dimension too large");
+  cudaStream_t st = as_stream(stream);
+  if (K == 0) {  // C = beta * C (relu)
+    return fail(AG_ERR_VALUE, "K == 0 is not supported by the tensor-core GEMM");
+  }
+  // N tile: the whole N when it fits one MMA (<= 256), padded to 16
+  int bn = static_cast<int>(std::min<int64_t>(256, ((N + 15) / 16) * 16));
+  bn = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
+  TcArgs g{};
+  g.M = M; g.N = N; g.K = K;
+  g.alpha = alpha; g.beta = beta; g.relu = (epilogue & AG_GEMM_RELU) ? 1 : 0;
+  g.m_tiles = static_cast<int>((M + BM - 1) / BM);
+  g.n_tiles = static_cast<int>((N + bn - 1) / bn);
+  const int64_t tiles = static_cast<int64_t>(g.m_tiles) * g.n_tiles;
+  const int sms = sm_count();
+  int splits = 1;
+  const int64_t kblocks = (K + BK - 1) / BK;
+  if (tiles < sms / 2 && kblocks >= 16) {  // skinny-output product (dW): split K
+    splits = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, sms / tiles), kblocks / 8));
+  }
+  const int64_t kb_per = (kblocks + splits - 1) / splits;
+  g.k_per_split = kb_per * BK;
+  splits = static_cast<int>((kblocks + kb_per - 1) / kb_per);
+  g.splits = splits;
+  CUtensorMap ma, mb;
+  int rc;
+  // A: K-major [M][K] (inner K) or M-major [K][M] (inner M)
+  if (a_mn) rc = make_map(&ma, A, M, K, lda, 32, true);
+  else rc = make_map(&ma, A, K, M, lda, BM, false);
+  if (rc) return rc;
+  if (b_mn) rc = make_map(&mb, B, N, K, ldb, 32, true);
+  else rc = make_map(&mb, B, K, N, ldb, bn, false);
+  if (rc) return rc;
+  Scratch ws;
+  if (splits > 1) {
+    AG_CUDA(ws.alloc(static_cast<size_t>(splits) * M * N * sizeof(float), st));
+    g.C = ws.as<float>();
+    g.ldc = N;
+  } else {
+    g.C = C;
+    g.ldc = ldc;
+  }
+  switch (bn) {
+    case 32: rc = launch_bn<32>(a_mn, b_mn, ma, mb, g, st); break;
+    case 64: rc = launch_bn<64>(a_mn, b_mn, ma, mb, g, st); break;
+    case 128: rc = launch_bn<128>(a_mn, b_mn, ma, mb, g, st); break;
+    default: rc = launch_bn<256>(a_mn, b_mn, ma, mb, g, st); break;
+  }
+  if (rc) return rc;
+  if (splits > 1) {
+    splitk_sum_kernel<<<grid_for(M * N, 256), 256, 0, st>>>(M, N, splits, g.C, C, ldc, alpha,
+                                                            beta, g.relu);
+    AG_LAUNCH_CHECK("splitk_sum_kernel");
+  }
+  return AG_OK;
+}

@@ -95,32 +95,29 @@ class CsrMatrix:
             self._off_block[block_size] = out.value
         return self._off_block[block_size]
 
-    def stage_layout(self, block_size: int, role_mask: int):
-        """Stage-aligned CSR for the fused kernel, cached per (B, role_mask).
+    def role_layout(self, block_size: int):
+        """Role-ordered copy of this CSR for the fused kernel, cached per B.
 
-        Returns (stage_ptr int32[V+1], counts int32[V, 2], stage_col int32[S, 9],
-        stage_val f32[S, 9]); see ag_stage_layout_* in include/adaptgear_b200.h.
+        Every row's edges are re-listed as the intra run (cols in
+        [floor(r/B)B, +B), ascending) followed by the inter edges (the row's
+        prefix ++ suffix, ascending).  Returns (mid int32[V], col int32[E],
+        val f32[E] | None); mid[r] ends row r's intra run.  See
+        ag_role_csr_build in include/adaptgear_b200.h.
         """
         if self._long is None:
             self._long = {}
-        key = (int(block_size), int(role_mask))
+        key = int(block_size)
         lay = self._long.get(key)
         if lay is None:
             dev = self.row_ptr.device
-            V = self.num_vertices
-            stage_ptr = torch.empty(V + 1, dtype=torch.int32, device=dev)
-            counts = torch.empty((V, 2), dtype=torch.int32, device=dev)
-            ns = _lib.out_i64()
-            _lib.call("ag_stage_layout_count", V, _lib.ptr(self.row_ptr), _lib.ptr(self.col_idx),
-                      key[0], key[1], _lib.ptr(stage_ptr), _lib.ptr(counts), _lib.byref(ns),
+            V, E = self.num_vertices, self.num_edges
+            mid = torch.empty(V, dtype=torch.int32, device=dev)
+            rcol = torch.empty(E, dtype=torch.int32, device=dev)
+            rval = None if self._val is None else torch.empty(E, dtype=torch.float32, device=dev)
+            _lib.call("ag_role_csr_build", V, _lib.ptr(self.row_ptr), _lib.ptr(self.col_idx),
+                      _lib.ptr(self._val), key, _lib.ptr(rcol), _lib.ptr(rval), _lib.ptr(mid),
                       _lib.stream())
-            S = ns.value
-            scol = torch.empty((S, 9), dtype=torch.int32, device=dev)
-            sval = torch.empty((S, 9), dtype=torch.float32, device=dev)
-            _lib.call("ag_stage_layout_fill", V, _lib.ptr(self.row_ptr), _lib.ptr(self.col_idx),
-                      _lib.ptr(self._val), key[0], _lib.ptr(stage_ptr), _lib.ptr(counts),
-                      _lib.ptr(scol), _lib.ptr(sval), _lib.stream())
-            lay = (stage_ptr, counts, scol, sval)
+            lay = (mid, rcol, rval)
             self._long[key] = lay
         return lay
 

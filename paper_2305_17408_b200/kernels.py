@@ -3,8 +3,8 @@
 Same operator API as the reference; every kernel is a hand-written sm_100a
 kernel behind the C ABI:
 
-  csr_inter          ag_fused_spmm          TMA-ring row gather, values bitwise
-                                            equal to the reference's
+  csr_inter          ag_fused_spmm          L1-swept warp-per-row gather, values
+                                            bitwise equal to the reference's
                                             np.add.reduceat order
   csr_intra_blocked  ag_csr_intra_spmm      per-community smem-staged slab (the
                                             public call, honouring the tile
@@ -94,17 +94,20 @@ def launch_csr(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp, 
 def launch_fused(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp,
                  block: int = 0, mask: int = 2, flags: int = 0,
                  other_touched: torch.Tensor | None = None, deg: torch.Tensor | None = None,
-                 gin_scale: float = 0.0) -> None:
-    """ag_fused_spmm: TMA-ring gather + reduceat-order reduction (+ role split)."""
-    F = x.shape[1]
-    if F % 4 == 0 and F <= 256:
-        sp, cnt, scol, sval = a.stage_layout(block, mask)
-    else:  # the register-gather path needs only the CSR
-        sp = cnt = scol = sval = None
-    _lib.call("ag_fused_spmm", a.num_vertices, F, int(block), int(mask),
-              _lib.ptr(a.row_ptr), _lib.ptr(a.col_idx), _lib.ptr(a.kernel_val), _lib.ptr(sp),
-              _lib.ptr(cnt), _lib.ptr(scol), _lib.ptr(sval), _lib.ptr(x), _lib.ptr(y),
-              _opcode(op), flags, _lib.ptr(other_touched), _lib.ptr(deg), float(gin_scale),
+                 gin_scale: float = 0.0, relu_src: torch.Tensor | None = None) -> None:
+    """ag_fused_spmm: L1-swept row gather, reduceat-order reduction (+ role split).
+
+    block > 0 splits every row into its intra run and inter edges (role-ordered
+    copy of the CSR, built once); block == 0 treats the row as one role.
+    """
+    if block > 0:
+        mid, col, val = a.role_layout(block)
+    else:
+        mid, col, val = None, a.col_idx, a.kernel_val
+    _lib.call("ag_fused_spmm", a.num_vertices, x.shape[1], int(mask), _lib.ptr(a.row_ptr),
+              _lib.ptr(mid), _lib.ptr(col), _lib.ptr(val), a.num_edges, _lib.ptr(x), _lib.ptr(y),
+              _opcode(op), flags | (_lib.AG_EPI_RELU_MASK if relu_src is not None else 0),
+              _lib.ptr(other_touched), _lib.ptr(deg), float(gin_scale), _lib.ptr(relu_src),
               _lib.stream())
 
 
@@ -245,10 +248,20 @@ def dense_adjacency(g: Graph) -> torch.Tensor:
     return a
 
 
+def _tc_ok(t: torch.Tensor) -> bool:
+    return t.data_ptr() % 16 == 0 and t.stride(0) % 4 == 0 and t.stride(1) == 1
+
+
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
          trans_a: bool = False, trans_b: bool = False, alpha: float = 1.0, beta: float = 0.0,
-         relu: bool = False) -> torch.Tensor:
-    """out = alpha * op(a) @ op(b) + beta * out on the hand-written fp32 GEMM."""
+         relu: bool = False, engine: str = "auto") -> torch.Tensor:
+    """out = alpha * op(a) @ op(b) + beta * out (the layers' update GEMM).
+
+    engine "auto" runs the tcgen05 3xTF32 tensor-core kernel (ag_gemm_tf32x3)
+    whenever the operands are 16-byte aligned with row strides that are
+    multiples of 4 floats, else the fp32 SIMT kernel (ag_gemm_f32); "tc" /
+    "simt" force one of them.
+    """
     M = a.shape[1] if trans_a else a.shape[0]
     K = a.shape[0] if trans_a else a.shape[1]
     N = b.shape[0] if trans_b else b.shape[1]
@@ -257,7 +270,9 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
         raise KernelError(f"gemm inner dimensions differ: {K} vs {Kb}")
     if out is None:
         out = torch.empty((M, N), dtype=torch.float32, device=a.device)
-    _lib.call("ag_gemm_f32", M, N, K, _lib.ptr(a), a.stride(0), int(trans_a), _lib.ptr(b),
+    tc = engine == "tc" or (engine == "auto" and K > 0 and _tc_ok(a) and _tc_ok(b))
+    fn = "ag_gemm_tf32x3" if tc else "ag_gemm_f32"
+    _lib.call(fn, M, N, K, _lib.ptr(a), a.stride(0), int(trans_a), _lib.ptr(b),
               b.stride(0), int(trans_b), _lib.ptr(out), out.stride(0), float(alpha), float(beta),
               _lib.AG_GEMM_RELU if relu else 0, _lib.stream())
     return out
@@ -383,12 +398,14 @@ def fusable(kernel_intra: KernelKind, kernel_inter: KernelKind) -> bool:
 
 
 def run_fused_pair(d: DecomposedGraph, x: torch.Tensor, y: torch.Tensor, op: AggregateOp,
-                   gin_scale: float | None = None) -> None:
-    """y = combine(intra, inter) [+ gin] in one pass over the full reordered CSR."""
+                   gin_scale: float | None = None, relu_src: torch.Tensor | None = None) -> None:
+    """y = combine(intra, inter) [+ gin] [* (relu_src > 0)] in one pass over the
+    full reordered CSR."""
     full = full_graph(d)
     flags = _lib.AG_EPI_GIN if gin_scale is not None else 0
     launch_fused(to_csr(full), x, y, op, block=d.block_size, mask=3, flags=flags,
-                 deg=d.full_in_degree, gin_scale=0.0 if gin_scale is None else gin_scale)
+                 deg=d.full_in_degree, gin_scale=0.0 if gin_scale is None else gin_scale,
+                 relu_src=relu_src)
 
 
 def aggregate_full(g: Graph, x, op: AggregateOp, kernel: KernelKind = KernelKind.CSR_INTER,

@@ -32,10 +32,28 @@ from .kernels import (
     _check_features,
     aggregate_decomposed,
     aggregate_full,
+    fusable,
     gemm,
+    run_fused_pair,
 )
 
+
+def _base(t: torch.Tensor) -> torch.Tensor:
+    """The full padded buffer behind a [:, :n] column view."""
+    if t.is_contiguous():
+        return t
+    return t.as_strided((t.shape[0], t.stride(0)), (t.stride(0), 1))
+
 MODELS = ("gcn", "gin", "agg_only")
+
+
+def _pad4(n: int) -> int:
+    return (n + 3) // 4 * 4
+
+
+def _padded_empty(rows: int, cols: int, dev) -> torch.Tensor:
+    """[rows, cols] view of a [rows, pad4(cols)] buffer (16-byte row stride)."""
+    return torch.empty((rows, _pad4(cols)), dtype=torch.float32, device=dev)[:, :cols]
 
 
 @dataclass(frozen=True)
@@ -202,9 +220,16 @@ class GNN:
             raise ValueError(f"unknown model {model!r}")
         if subject_t is None:
             subject_t = decompose(full_graph(subject).reverse(), subject.block_size)
-        ws = [as_device(LayerParams.seeded(model, dims[i], dims[i + 1], seed=seed + i,
-                                           gin_eps=gin_eps).weight, torch.float32).clone()
-              for i in range(len(dims) - 1)]
+        ws = []
+        for i in range(len(dims) - 1):
+            w = LayerParams.seeded(model, dims[i], dims[i + 1], seed=seed + i,
+                                   gin_eps=gin_eps).weight
+            # output width padded to a multiple of 4 floats (16-byte rows), so
+            # every GEMM operand view is TMA-addressable; the pad stays 0
+            buf = torch.zeros((dims[i], _pad4(dims[i + 1])), dtype=torch.float32,
+                              device=_lib.device())
+            buf[:, :dims[i + 1]] = as_device(w, torch.float32)
+            ws.append(buf[:, :dims[i + 1]])
         return cls(model=model, dims=list(dims), subject=subject, subject_t=subject_t,
                    weights=ws, gin_eps=gin_eps)
 
@@ -232,18 +257,30 @@ class GNN:
                 self.kernels[(direction, f)] = (s.choice_intra, s.choice_inter)
         return dict(self.kernels)
 
-    def _aggregate(self, subj: DecomposedGraph, h: torch.Tensor, direction: str):
+    def _aggregate(self, subj: DecomposedGraph, h: torch.Tensor, direction: str,
+                   relu_src: torch.Tensor | None = None):
+        """Aggregation of one layer; relu_src fuses the ReLU backward of the
+        layer below into the (transposed) aggregation's epilogue."""
         ki, ke = self.pair(direction, h.shape[1])
-        if self.events is None:
-            return aggregate_decomposed(subj, h, AggregateOp.SUM, kernel_intra=ki,
-                                        kernel_inter=ke, gin_scale=self.gin_scale())
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        out = aggregate_decomposed(subj, h, AggregateOp.SUM, kernel_intra=ki, kernel_inter=ke,
-                                   gin_scale=self.gin_scale())
-        e1.record()
-        self.events.append((e0, e1, h.shape[1], subj))
+        e0 = e1 = None
+        if self.events is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        if fusable(ki, ke):
+            h = _check_features(subj.num_vertices, h)
+            out = torch.empty((subj.num_vertices, h.shape[1]), dtype=torch.float32,
+                              device=h.device)
+            run_fused_pair(subj, h, out, AggregateOp.SUM, self.gin_scale(), relu_src=relu_src)
+        else:
+            out = aggregate_decomposed(subj, h, AggregateOp.SUM, kernel_intra=ki,
+                                       kernel_inter=ke, gin_scale=self.gin_scale())
+            if relu_src is not None:
+                _lib.call("ag_relu_backward", out.numel(), _lib.ptr(relu_src), _lib.ptr(out),
+                          _lib.stream())
+        if e0 is not None:
+            e1.record()
+            self.events.append((e0, e1, h.shape[1], subj))
         return out
 
     def forward(self, x: torch.Tensor):
@@ -253,7 +290,8 @@ class GNN:
         for l in range(self.num_layers):
             agg = self._aggregate(self.subject, h, "fwd")
             last = l == self.num_layers - 1
-            out = gemm(agg, self.weights[l], relu=not last)
+            out = _padded_empty(agg.shape[0], self.dims[l + 1], agg.device)
+            gemm(agg, self.weights[l], out, relu=not last)
             saved.append((agg, out))
             h = out
         return h, saved
@@ -264,28 +302,29 @@ class GNN:
         g = d_logits
         for l in range(self.num_layers - 1, -1, -1):
             agg, _ = saved[l]
-            grads[l] = gemm(agg, g, trans_a=True)
+            grads[l] = torch.zeros((agg.shape[1], _pad4(self.dims[l + 1])), dtype=torch.float32,
+                                   device=agg.device)[:, :self.dims[l + 1]]
+            gemm(agg, g, grads[l], trans_a=True)
             if l == 0:
                 break
             d_in = gemm(g, self.weights[l], trans_b=True)
-            d_h = self._aggregate(self.subject_t, d_in, "bwd")
             _, h_prev = saved[l - 1]
-            _lib.call("ag_relu_backward", d_h.numel(), _lib.ptr(h_prev), _lib.ptr(d_h),
-                      _lib.stream())
-            g = d_h
+            g = self._aggregate(self.subject_t, d_in, "bwd", relu_src=h_prev)
         return grads
 
     def loss_and_grad(self, logits, labels, mask, num_masked: int):
         loss = torch.empty(1, dtype=torch.float32, device=logits.device)
-        d_logits = torch.empty_like(logits)
-        _lib.call("ag_softmax_xent", logits.shape[0], logits.shape[1], _lib.ptr(logits),
-                  _lib.ptr(labels), _lib.ptr(mask), int(num_masked), _lib.ptr(loss),
-                  _lib.ptr(d_logits), _lib.stream())
+        d_logits = _padded_empty(logits.shape[0], logits.shape[1], logits.device)
+        _lib.call("ag_softmax_xent", logits.shape[0], logits.shape[1], logits.stride(0),
+                  _lib.ptr(logits), _lib.ptr(labels), _lib.ptr(mask), int(num_masked),
+                  _lib.ptr(loss), _lib.ptr(d_logits), _lib.stream())
         return loss, d_logits
 
     def sgd(self, grads, lr: float) -> None:
+        """w -= lr * dw over the whole padded buffers (the pads stay 0)."""
         for w, dw in zip(self.weights, grads):
-            _lib.call("ag_sgd_step", w.numel(), _lib.ptr(w), _lib.ptr(dw), float(lr),
+            wb, gb = _base(w), _base(dw)
+            _lib.call("ag_sgd_step", wb.numel(), _lib.ptr(wb), _lib.ptr(gb), float(lr),
                       _lib.stream())
 
     def train_step(self, x, labels, mask, num_masked: int, lr: float = 0.01):

@@ -56,6 +56,17 @@ def main():
             continue
         ba = bench.bytes_alg(V, E, F, rg.weights is not None)
         res = {}
+        import os
+        ref = torch.empty_like(x)
+        os.environ["AG_GATHER_VEC"], os.environ["AG_GATHER_WAVES"] = "4", "1"
+        K.run_fused_pair(dec, x, ref, ag.AggregateOp.SUM)
+        for vec in ("4", "8"):
+            for wv in ("1", "2", "4"):
+                os.environ["AG_GATHER_VEC"], os.environ["AG_GATHER_WAVES"] = vec, wv
+                res[f"fused_pair_vec{vec}_w{wv}"] = timeit(
+                    lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM))
+                out.setdefault("bitwise_same", []).append(bool(torch.equal(y, ref)))
+        os.environ["AG_GATHER_VEC"], os.environ["AG_GATHER_WAVES"] = "4", "1"
         res["fused_pair"] = timeit(lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM))
         res["fused_full_O1"] = timeit(lambda: K.launch_fused(full, x, y, ag.AggregateOp.SUM))
         res["inter_csr_fused_raw"] = timeit(lambda: K.launch_fused(inter.csr, x, y,
@@ -67,6 +78,9 @@ def main():
         res["intra_dense_block"] = timeit(lambda: K.launch_dense_block(intra.blocks, x, y,
                                                                        ag.AggregateOp.SUM))
         res["full_csr_old"] = timeit(lambda: K.launch_csr(full, x, y, ag.AggregateOp.SUM))
+        yo = torch.empty_like(x)
+        K.launch_fused(full, x, yo, ag.AggregateOp.SUM)
+        out.setdefault("fused_O1_equals_old_csr", []).append(bool(torch.equal(y, yo)))
         res["copy_xy"] = timeit(lambda: y.copy_(x))
         w = torch.randn((F, 256), device="cuda")
         res["gemm_Fx256"] = timeit(lambda: K.gemm(x, w))
