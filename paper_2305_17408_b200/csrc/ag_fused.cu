@@ -63,6 +63,7 @@ struct GArgs {
   int ranges;               // row ranges
   int64_t cost_total;       // nnz + kRowCost * rows
   float one;                // 1.0f, passed at run time (see add2)
+  int chunk_rows;           // rows per work unit
 };
 
 constexpr int64_t kRowCost = 4;  // a row's fixed cost in edge units (epilogue, topology)
@@ -242,6 +243,13 @@ struct RowWarp {
     }
     __syncwarp();
   }
+  // install a prefetched window [at, at + kWin) ∩ [at, end): lane l's (c, v)
+  __device__ __forceinline__ void install(int32_t at, int32_t c, float v) {
+    __syncwarp();
+    p = at;
+    if (at + lane < end) win_st(win + lane * 16, static_cast<uint32_t>(c) * feat, pk(v, v));
+    __syncwarp();
+  }
   __device__ __forceinline__ void ensure(int32_t lo, int n) {
     if (lo + n > p + kWin) fill(lo);
   }
@@ -351,13 +359,13 @@ template <int VEC, bool W>
 template <bool IS_MAX>
 __device__ __forceinline__ Lv<VEC> RowWarp<VEC, W>::role(int32_t e0, int32_t n) {
   if (n <= 0) return lv_splat<VEC>(0.0f);
-  end = e0 + n;
-  fill(e0);
+  ensure(e0, n < kWin ? static_cast<int>(n) : kWin);  // the row's window normally covers it
   if constexpr (IS_MAX) {
     Lv<VEC> acc = item<true>(e0);
+    const int32_t rend = e0 + n;  // this role's end (end is the row's)
 #pragma unroll 1
-    for (int32_t b = e0 + 1; b < end; b += 8) {
-      const int cnt = end - b < 8 ? end - b : 8;
+    for (int32_t b = e0 + 1; b < rend; b += 8) {
+      const int cnt = rend - b < 8 ? rend - b : 8;
       ensure(b, cnt);
       Lv<VEC> c[8];
 #pragma unroll
@@ -406,15 +414,56 @@ __device__ __forceinline__ Vf<VEC> combine2(int op, const Vf<VEC> &I, bool ti, c
   return splat<VEC>(0.0f);
 }
 
+// One destination row (both roles, epilogue) for this lane's columns.
+template <int VEC, bool IS_MAX, bool W>
+__device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64_t r, int32_t s,
+                                       int32_t e, int32_t m, int64_t fcol, bool act) {
+  const int64_t ld = a.feat;
+  const int32_t ni = (a.mask & 1) ? m - s : 0;
+  const int32_t no = (a.mask & 2) ? e - m : 0;
+  const Vf<VEC> I = lv_out<VEC>(w.template role<IS_MAX>(s, ni));
+  const Vf<VEC> O = lv_out<VEC>(w.template role<IS_MAX>(m, no));
+  if (!act) return;
+  float *yp = a.y + r * ld + fcol;
+  const int64_t d = (a.ep.op == AG_OP_MEAN && a.ep.deg) ? a.ep.deg[r] : 1;
+  Vf<VEC> out;
+  if (a.mask == 3) {
+    out = combine2<VEC>(a.ep.op, I, ni > 0, O, no > 0, d);
+  } else {
+    const Vf<VEC> v = (a.mask == 1) ? I : O;
+    const bool t = (a.mask == 1) ? ni > 0 : no > 0;
+    if (!(a.ep.flags & AG_EPI_COMBINE)) {
+      out = t ? v : splat<VEC>(0.0f);
+    } else if (a.ep.flags & AG_EPI_EMPTY_OTHER) {
+      out = combine2<VEC>(a.ep.op, v, t, splat<VEC>(0.0f), false, d);
+    } else {
+      const bool ot = a.ep.other_touched ? a.ep.other_touched[r] != 0 : false;
+      out = combine2<VEC>(a.ep.op, v, t, ldv_rw<VEC>(yp), ot, d);
+    }
+  }
+  if (a.ep.flags & AG_EPI_GIN)
+    out = vadd<VEC>(vscale<VEC>(a.ep.gin_scale, ldv<VEC>(a.x + r * ld + fcol)), out);
+  if (a.ep.flags & AG_EPI_RELU_MASK) {
+    const Vf<VEC> h = ldv<VEC>(a.ep.relu_src + r * ld + fcol);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) out.v[i] = h.v[i] > 0.0f ? out.v[i] : 0.0f;
+  }
+  stv<VEC>(yp, out);
+}
+
+// Work order.  Units are (chunk of kChunkRows consecutive rows, column tile),
+// tile fastest; global warp gw takes units gw, gw + W, gw + 2W, ... (W = all
+// warps of the persistent grid).  Every warp advances at about the same rate,
+// so the whole GPU sweeps the row space as ONE narrow wavefront: the source
+// rows the reorder keeps near each destination are re-read from L2 (and from
+// L1: a CTA's warps hold adjacent chunks, i.e. one contiguous band of rows and
+// both column tiles of it), and no atomics or CTA barriers are needed.
+// Within its sequence a warp software-pipelines the next row's row_ptr / mid /
+// first kWin (col, val) while the current row gathers.
 template <int VEC, bool IS_MAX, bool W>
 __global__ void __launch_bounds__(kThreads, 2) gather_kernel(GArgs a) {
   constexpr int T = 32 * VEC;
-  __shared__ int64_t bounds[2];
   __shared__ __align__(16) uint64_t wins[kThreads / 32][kWin * 2];
-  const int tile = static_cast<int>(blockIdx.x % a.ntiles);
-  const int range = static_cast<int>(blockIdx.x / a.ntiles);
-  if (threadIdx.x < 2) bounds[threadIdx.x] = range_start(a, range + threadIdx.x);
-  __syncthreads();
   const int warp = threadIdx.x >> 5;
   RowWarp<VEC, W> w;
   w.win = static_cast<uint32_t>(__cvta_generic_to_shared(wins[warp]));
@@ -423,47 +472,58 @@ __global__ void __launch_bounds__(kThreads, 2) gather_kernel(GArgs a) {
   w.feat = static_cast<uint32_t>(a.feat);
   w.lane = threadIdx.x & 31;
   w.one = pk(a.one, a.one);
-  const int64_t fcol = static_cast<int64_t>(tile) * T + w.lane * VEC;
-  const bool act = fcol < a.feat;
-  w.xl = a.x + (act ? fcol : 0);
   w.p = 0;
   w.end = 0;
-  const int64_t ld = a.feat;
-  const int nwarps = blockDim.x >> 5;
+  const int CR = a.chunk_rows;
+  const int64_t nrc = (a.rows + CR - 1) / CR;
+  const int64_t nunits = nrc * a.ntiles;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + warp;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
+  // cursor over this warp's (unit, row-in-chunk) sequence
+  int64_t k = gw;
+  int j = 0;
+  auto row_of = [&](int64_t kk, int jj) { return (kk / a.ntiles) * CR + jj; };
+  auto advance = [&](int64_t &kk, int &jj) {
+    ++jj;
+    if (jj == CR || row_of(kk, jj) >= a.rows) { kk += nw; jj = 0; }
+  };
+  int32_t ns = 0, ne = 0, nm = 0, nc = 0;
+  float nv = 1.0f;
+  auto prefetch = [&](int64_t kk, int jj) {
+    if (kk < nunits) {
+      const int64_t rr = row_of(kk, jj);
+      ns = a.row_ptr[rr];
+      ne = a.row_ptr[rr + 1];
+      nm = a.mid ? a.mid[rr] : (a.mask == 1 ? ne : ns);
+      const int32_t ed = ns + w.lane;
+      nc = ed < ne ? __ldg(a.col + ed) : 0;
+      nv = (W && ed < ne) ? __ldg(a.val + ed) : 1.0f;
+    }
+  };
+  prefetch(k, j);
+  int cur_tile = -1;
+  int64_t fcol = 0;
+  bool act = false;
 #pragma unroll 1
-  for (int64_t r = bounds[0] + warp; r < bounds[1]; r += nwarps) {
-    const int32_t s = a.row_ptr[r], e = a.row_ptr[r + 1];
-    const int32_t m = a.mid ? a.mid[r] : (a.mask == 1 ? e : s);
-    const int32_t ni = (a.mask & 1) ? m - s : 0;
-    const int32_t no = (a.mask & 2) ? e - m : 0;
-    const Vf<VEC> I = lv_out<VEC>(w.template role<IS_MAX>(s, ni));
-    const Vf<VEC> O = lv_out<VEC>(w.template role<IS_MAX>(m, no));
-    if (!act) continue;
-    float *yp = a.y + r * ld + fcol;
-    const int64_t d = (a.ep.op == AG_OP_MEAN && a.ep.deg) ? a.ep.deg[r] : 1;
-    Vf<VEC> out;
-    if (a.mask == 3) {
-      out = combine2<VEC>(a.ep.op, I, ni > 0, O, no > 0, d);
-    } else {
-      const Vf<VEC> v = (a.mask == 1) ? I : O;
-      const bool t = (a.mask == 1) ? ni > 0 : no > 0;
-      if (!(a.ep.flags & AG_EPI_COMBINE)) {
-        out = t ? v : splat<VEC>(0.0f);
-      } else if (a.ep.flags & AG_EPI_EMPTY_OTHER) {
-        out = combine2<VEC>(a.ep.op, v, t, splat<VEC>(0.0f), false, d);
-      } else {
-        const bool ot = a.ep.other_touched ? a.ep.other_touched[r] != 0 : false;
-        out = combine2<VEC>(a.ep.op, v, t, ldv_rw<VEC>(yp), ot, d);
-      }
+  while (k < nunits) {
+    const int tile = static_cast<int>(k % a.ntiles);
+    if (tile != cur_tile) {
+      cur_tile = tile;
+      fcol = static_cast<int64_t>(tile) * T + w.lane * VEC;
+      act = fcol < a.feat;
+      w.xl = a.x + (act ? fcol : 0);
     }
-    if (a.ep.flags & AG_EPI_GIN)
-      out = vadd<VEC>(vscale<VEC>(a.ep.gin_scale, ldv<VEC>(a.x + r * ld + fcol)), out);
-    if (a.ep.flags & AG_EPI_RELU_MASK) {
-      const Vf<VEC> h = ldv<VEC>(a.ep.relu_src + r * ld + fcol);
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) out.v[i] = h.v[i] > 0.0f ? out.v[i] : 0.0f;
-    }
-    stv<VEC>(yp, out);
+    const int64_t r = row_of(k, j);
+    const int32_t s = ns, e = ne, m = nm;
+    w.end = e;
+    w.install(s, nc, nv);
+    int64_t k2 = k;
+    int j2 = j;
+    advance(k2, j2);
+    prefetch(k2, j2);
+    do_row<VEC, IS_MAX, W>(a, w, r, s, e, m, fcol, act);
+    k = k2;
+    j = j2;
   }
 }
 
@@ -505,12 +565,11 @@ int launch_gather(GArgs a, bool is_max, cudaStream_t st) {
   AG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0));
   if (per_sm < 1) per_sm = 1;
   a.ntiles = static_cast<int>((a.feat + T - 1) / T);
-  const int waves = std::max(1, env_int("AG_GATHER_WAVES", 1));
-  int64_t ranges = static_cast<int64_t>(sm_count()) * per_sm * waves / a.ntiles;
-  const int64_t max_ranges = (a.rows + 63) / 64;  // >= 64 rows per range
-  ranges = std::max<int64_t>(1, std::min(ranges, max_ranges));
-  a.ranges = static_cast<int>(ranges);
-  const int64_t grid = ranges * a.ntiles;
+  a.chunk_rows = std::max(1, env_int("AG_GATHER_CHUNK", 16));
+  const int64_t units = (a.rows + a.chunk_rows - 1) / a.chunk_rows * a.ntiles;
+  const int64_t warps = (units + 0);
+  int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;
+  grid = std::max<int64_t>(1, std::min(grid, (warps + kThreads / 32 - 1) / (kThreads / 32)));
   k<<<(unsigned)grid, kThreads, 0, st>>>(a);
   AG_LAUNCH_CHECK("gather_kernel");
   return AG_OK;
@@ -557,7 +616,8 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
     return fail(AG_ERR_VALUE, "feature matrix too large for 32-bit row offsets");
   cudaStream_t st = as_stream(stream);
   GArgs a{num_rows, static_cast<int>(feat), role_mask, row_ptr, role_mid, col_idx, val, x, y,
-          Epi{op, epi_flags, other_touched, deg, x, feat, gin_scale, relu_src}, 1, 1, 0, 1.0f};
+          Epi{op, epi_flags, other_touched, deg, x, feat, gin_scale, relu_src}, 1, 1, 0, 1.0f,
+          16};
   a.cost_total = num_edges + kRowCost * num_rows;
   const bool is_max = op == AG_OP_MAX;
   const bool v4 = feat % 4 == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0 &&

@@ -9,9 +9,13 @@
 //
 // 3xTF32: every fp32 operand x is split in shared memory into hi = x with the
 // low 13 mantissa bits cleared (exactly representable in tf32) and
-// lo = x - hi (exact in fp32); the tile product is accumulated in fp32 TMEM as
-// A_hi*B_hi + A_hi*B_lo + A_lo*B_hi, i.e. within a few ulp of an fp32 GEMM
-// (the dropped A_lo*B_lo term is ~2^-22 relative).
+// lo = x - hi (exact in fp32).  The tile product is accumulated in TWO fp32
+// TMEM accumulators -- A_hi*B_hi (exact 22-bit products) and the correction
+// A_hi*B_lo + A_lo*B_hi (~2^-11 smaller, so its own rounding is negligible) --
+// which the epilogue adds in IEEE fp32.  Keeping the correction out of the
+// main accumulator matters: the tensor core's fp32 accumulation truncates, and
+// folding the small terms into the large sum tripled the error.  The dropped
+// A_lo*B_lo term is ~2^-22 relative.
 //
 // Kernel anatomy (one CTA per SM, persistent over 128 x BN output tiles and,
 // for the skinny dW product, K splits):
@@ -28,6 +32,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "ag_common.cuh"
@@ -154,8 +159,12 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 4;   // BN * 128 B
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = STAGE * 3 <= 200 * 1024 ? 3 : 2;
-  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64
-                                 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  // two fp32 accumulators per tile (hi*hi and the hi*lo + lo*hi correction),
+  // double-buffered when TMEM allows
+  static constexpr int ACC_BUFS = 4 * BN <= 512 ? 2 : 1;
+  static constexpr int COLS = ACC_BUFS * 2 * BN;
+  static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128
+                                 : COLS <= 256 ? 256 : 512;
   static constexpr int SMEM = STAGES * STAGE + 1024 /* align */ + 256 /* barriers */;
 };
 
@@ -280,7 +289,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nkb = tile_kblocks(t, k0);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+      const uint32_t d = tmem_base + static_cast<uint32_t>(acc * 2 * BN);  // hi*hi
+      const uint32_t dc = d + BN;                                          // correction
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&conv[stage], phase);
         tc_fence_after();
@@ -303,9 +313,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t dbh = smem_desc(b_hi + bo, blbo, bsbo, B_MN);
             const uint64_t dbl = smem_desc(b_lo + bo, blbo, bsbo, B_MN);
             const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
-            tc_mma_tf32(d, dal, dbh, idesc, first);
-            tc_mma_tf32(d, dah, dbl, idesc, 1u);
-            tc_mma_tf32(d, dah, dbh, idesc, 1u);
+            tc_mma_tf32(dc, dal, dbh, idesc, first);
+            tc_mma_tf32(dc, dah, dbl, idesc, 1u);
+            tc_mma_tf32(d, dah, dbh, idesc, first);
           }
           tc_commit(&empty[stage]);
           if (kb == nkb - 1) tc_commit(&tfull[acc]);
@@ -315,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (nkb == 0 && lane == 0) tc_commit(&tfull[acc]);  // (K == 0: nothing to do)
       __syncwarp();
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == C::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp < kEpiWarp0) {
     // ------------------------------------------------------- splitters ---
@@ -360,9 +370,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                           (direct ? (g.ldc % 4 == 0) : (g.N % 4 == 0));
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
-        float v[16];
-        tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                      static_cast<uint32_t>(acc * BN + c), v);
+        float v[16], vc[16];
+        const uint32_t ta = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                            static_cast<uint32_t>(acc * 2 * BN + c);
+        tmem_ld16(ta, v);
+        tmem_ld16(ta + BN, vc);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], vc[i]);
         if (row < g.M) {
           const int64_t nb = n0 + c;
           if (direct) {
@@ -389,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == C::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
     }
   }
 
@@ -503,6 +517,7 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   // N tile: the whole N when it fits one MMA (<= 256), padded to 16
   int bn = static_cast<int>(std::min<int64_t>(256, ((N + 15) / 16) * 16));
   bn = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
+  if (const char *e = std::getenv("AG_TC_BN")) bn = std::min(bn, std::max(32, std::atoi(e)));
   TcArgs g{};
   g.M = M; g.N = N; g.K = K;
   g.alpha = alpha; g.beta = beta; g.relu = (epilogue & AG_GEMM_RELU) ? 1 : 0;

@@ -58,15 +58,15 @@ def main():
         res = {}
         import os
         ref = torch.empty_like(x)
-        os.environ["AG_GATHER_VEC"], os.environ["AG_GATHER_WAVES"] = "4", "1"
+        os.environ["AG_GATHER_VEC"], os.environ["AG_GATHER_CHUNK"] = "4", "16"
         K.run_fused_pair(dec, x, ref, ag.AggregateOp.SUM)
         for vec in ("4", "8"):
-            for wv in ("1", "2", "4"):
-                os.environ["AG_GATHER_VEC"], os.environ["AG_GATHER_WAVES"] = vec, wv
-                res[f"fused_pair_vec{vec}_w{wv}"] = timeit(
+            for ch in ("4", "16", "64", "256"):
+                os.environ["AG_GATHER_VEC"], os.environ["AG_GATHER_CHUNK"] = vec, ch
+                res[f"fused_pair_vec{vec}_c{ch}"] = timeit(
                     lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM))
                 out.setdefault("bitwise_same", []).append(bool(torch.equal(y, ref)))
-        os.environ["AG_GATHER_VEC"], os.environ["AG_GATHER_WAVES"] = "4", "1"
+        os.environ["AG_GATHER_VEC"], os.environ["AG_GATHER_CHUNK"] = "4", "16"
         res["fused_pair"] = timeit(lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM))
         res["fused_full_O1"] = timeit(lambda: K.launch_fused(full, x, y, ag.AggregateOp.SUM))
         res["inter_csr_fused_raw"] = timeit(lambda: K.launch_fused(inter.csr, x, y,
@@ -83,8 +83,14 @@ def main():
         out.setdefault("fused_O1_equals_old_csr", []).append(bool(torch.equal(y, yo)))
         res["copy_xy"] = timeit(lambda: y.copy_(x))
         w = torch.randn((F, 256), device="cuda")
-        res["gemm_Fx256"] = timeit(lambda: K.gemm(x, w))
-        res["gemm_TN_dW"] = timeit(lambda: K.gemm(x, x, trans_a=True))
+        g256 = torch.randn((V, 256), device="cuda")
+        for bn in ("256", "128"):
+            os.environ["AG_TC_BN"] = bn
+            res[f"gemm_Fx256_bn{bn}"] = timeit(lambda: K.gemm(x, w))
+            res[f"gemm_dW_bn{bn}"] = timeit(lambda: K.gemm(x, g256, trans_a=True))
+            res[f"gemm_dH_bn{bn}"] = timeit(lambda: K.gemm(g256, w, trans_b=True))
+        os.environ.pop("AG_TC_BN")
+        res["gemm_Fx256_simt"] = timeit(lambda: K.gemm(x, w, engine="simt"))
         gbs = {k: round(ba / (v / 1e3) / 1e9, 1) for k, v in res.items() if "gemm" not in k}
         out[f"F{F}"] = {"ms": {k: round(v, 4) for k, v in res.items()}, "alg_GBps": gbs,
                         "bytes_alg": ba}
