@@ -195,18 +195,51 @@ int ag_role_csr_build(int64_t num_rows, const int32_t *row_ptr,
  * each in the reference's np.add.reduceat order (bitwise), then
  *   role_mask 3: y = combine(I, O) (kernels.py:253-276)   [+ gin term]
  *   role_mask 1/2: a single role with the AG_EPI_* epilogue of ag_csr_spmm.
- * role_mid NULL: the whole row is the single role of role_mask 1 or 2, and
- * col_idx / val are the plain CSR -- this is aggregate_csr_inter
- * (kernels.py:117-134).  num_edges = row_ptr[num_rows] (used to balance the
- * row ranges).  One warp per row, 32-column tiles swept over nnz-balanced
- * row ranges so re-used source rows hit L1; any F (float4 path when F % 4
- * == 0 and x, y are 16-byte aligned). */
+ * role_mid NULL: the whole row is the single role of role_mask 1 or 2 --
+ * aggregate_csr_inter (kernels.py:117-134).  The edges are given as `codes`
+ * (ag_slab_codes over the role-ordered -- or plain -- column indices, built
+ * with the same `window`), val in the same order.  num_edges =
+ * row_ptr[num_rows] (used to balance the row ranges).
+ * "Slab" kernel: one CTA per SM sweeps a column tile of an nnz-balanced range
+ * of 16-row blocks; a TMA producer warp streams X into a shared-memory ring
+ * holding the blocks within `window` blocks of the current one (sources
+ * there are read from shared memory, farther ones from global); 15 consumer
+ * warps take the range's rows round-robin.  `window` only affects speed,
+ * never values (ag_slab_window picks it per graph).  Any F (TMA when F % 4
+ * == 0 and x is 16-byte aligned, cp.async otherwise).  x has x_rows >=
+ * num_rows rows (a rank's halo rows follow its own rows). */
 int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                   const int32_t *row_ptr, const int32_t *role_mid,
-                  const int32_t *col_idx, const float *val, int64_t num_edges,
+                  const int32_t *codes, const int32_t *far_cnt,
+                  const int32_t *far_src, const float *val, int64_t num_edges,
                   const float *x, float *y, int32_t op, int32_t epi_flags,
                   const uint8_t *other_touched, const int64_t *deg,
-                  float gin_scale, const float *relu_src, void *stream);
+                  float gin_scale, const float *relu_src, int64_t x_rows,
+                  int32_t window, void *stream);
+
+/* Window radius (in 16-row blocks) for ag_fused_spmm over this CSR: the
+ * smallest radius whose ring covers `coverage` (e.g. 0.995) of the edges the
+ * largest supported radius (19) would cover, from a device histogram of
+ * |src/16 - dst/16|.  Synchronous (reads the histogram back); call once per
+ * topology and cache the result.  No reference counterpart: a B200 layout
+ * parameter of the cached formats (formats.py:76-140). */
+int ag_slab_window(int64_t num_rows, const int32_t *row_ptr,
+                   const int32_t *col_idx, double coverage, int32_t *window,
+                   void *stream);
+
+/* Edge codes for ag_fused_spmm (same order as col_idx: plain or
+ * role-ordered CSR).  codes[e] = X-ring row of col_idx[e] when its 16-row
+ * block is within `window` blocks of row r's block; otherwise the source is
+ * staged per 16-row block in the far ring (the block's j-th distinct far
+ * source, j < ag_slab_far_capacity(): far_src[block * cap + j], far_cnt[block]
+ * = number staged) or, past the capacity, codes[e] = ~col_idx[e] (read from
+ * global memory).  far_cnt: int32[ceil(num_rows / 16)], far_src: int32[that
+ * * ag_slab_far_capacity()]. */
+int ag_slab_codes(int64_t num_rows, const int32_t *row_ptr,
+                  const int32_t *col_idx, int32_t window, int32_t *codes,
+                  int32_t *far_cnt, int32_t *far_src, void *stream);
+/* Staged far sources per 16-row block (the far-ring capacity). */
+int ag_slab_far_capacity(void);
 
 /* K5 combine (kernels.py:253-276) as a standalone pass. out may alias a. */
 int ag_combine(int64_t num_rows, int64_t feat, const float *a,

@@ -13,40 +13,59 @@
 // tree ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8 tail in order;
 // n > 128: split at n/2 rounded down to a multiple of 8 and recurse).
 //
-// Work decomposition (sm_100a, HBM/L2-bound gather):
-//  * The feature dimension is cut into column tiles of T = 32 floats (one
-//    128-byte L1 line per source row).  A CTA owns one column tile of one
-//    contiguous, nnz-balanced range of rows and sweeps it front to back, so
-//    the source rows of a reordered graph (the 16-row community block and its
-//    neighbourhood) are re-read from the SM's L1 instead of L2.  The CTAs of
-//    the ntiles column tiles of a range are adjacent in launch order and share
-//    the range's topology through L2.
-//  * One warp per row.  The warp is split into NG groups of 32/NG lanes; every
-//    group covers the SAME T columns (float4 per lane) and owns 8/NG of the
-//    8 pairwise accumulators, so a warp has NG independent row gathers in
-//    flight per round and the accumulator tree's upper levels are two
-//    xor-shuffles -- the exact numpy tree, no re-association.
-//  * Column indices and weights are streamed 32 edges at a time into lane
-//    registers (one coalesced load each) and broadcast with shuffles.
+// Work decomposition: the "slab" kernel (sm_100a).
+//  * A reordered graph keeps most sources near their destination: the
+//    community's own 16-row block (intra) and, for the inter edges, a band of
+//    neighbouring blocks.  One CTA per SM owns a column tile of T = 32*VEC
+//    floats of one contiguous, nnz-balanced range of 16-row blocks and sweeps
+//    it front to back.
+//  * A producer warp streams the X tile of block b (16 rows x T floats) into
+//    an S-slot ring in shared memory with one TMA tensor load per block
+//    (cp.async.bulk.tensor.2d, mbarrier complete_tx), S blocks ahead of the
+//    slowest consumer.  X crosses HBM -> L2 -> SM once per tile.
+//  * 16 consumer warps: warp w owns row w of every block.  At block k the ring
+//    holds blocks [k-H, k+H] (H = window radius, picked per graph from the
+//    edge-distance histogram, ag_slab_window); a source inside it is read
+//    from shared memory (one 128/256-byte row per warp, conflict free),
+//    anything farther with a direct global load.  The per-row reduction is
+//    the exact numpy order above, one lane per VEC columns.
+//  * Ring slots are recycled through per-slot full/empty mbarriers: a warp
+//    finishing block k releases block k-H; the producer refills a slot once
+//    all 16 warps released it.  Warps drift freely up to S-2H-1 blocks apart,
+//    which absorbs the row-length imbalance without CTA-wide barriers.
+//  * Column indices and weights of the current row are staged in a per-warp
+//    32-entry window (one coalesced load per 32 edges) already translated to
+//    ring byte offsets, so the inner loop is LDS(window) + LDS(x) + math.
 //  * Products / sums are packed FMUL2 / FADD2 (fp32x2, round-to-nearest, no
 //    FMA contraction), so results stay bitwise equal to the reference.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "ag_common.cuh"
+#include "ag_ptx.cuh"
 #include "ag_vec.cuh"
 
 namespace ag {
 namespace {
 using namespace vec;
+using namespace ptx;
 
 constexpr int kLeafN = 128;  // numpy PW_BLOCKSIZE
 constexpr int kDepth = 40;
-constexpr int kThreads = 256;
-constexpr unsigned kFull = 0xffffffffu;
+constexpr int kRB = 16;      // rows per ring block
+constexpr int kCons = 14;    // consumer warps; + 2 producer warps = 16 (4 per SMSP, 128 regs)
+constexpr int kThreads = (kCons + 2) * 32;
+constexpr int kWin = 32;     // topology items per window refill
+constexpr int kSlots = 42;   // X ring capacity in blocks (window H <= (kSlots - 9) / 2 = 16)
+constexpr int kFarSlots = 8; // far ring: staged out-of-window sources of the next blocks
+constexpr int kFarMax = 24;  // staged far sources per block (more: read from global)
+constexpr int kFarRow0 = kSlots * 16;  // first far-ring row (codes >= kFarRow0)
+constexpr int64_t kRowCost = 4;  // a row's fixed cost in edge units (epilogue, topology)
 
 struct GArgs {
   int64_t rows;
@@ -54,19 +73,23 @@ struct GArgs {
   int mask;                 // 1 intra only, 2 inter only, 3 both (combine)
   const int32_t *row_ptr;   // [rows + 1]
   const int32_t *mid;       // [rows] end of the intra run; nullptr: single role
-  const int32_t *col;       // role-ordered column indices
+  const int32_t *code;      // role-ordered edge codes (ag_slab_codes)
+  const int32_t *far_cnt;   // [nblocks] staged far sources per block (<= kFarMax)
+  const int32_t *far_src;   // [nblocks * kFarMax] their source rows
   const float *val;         // role-ordered weights; nullptr = implicit 1.0
   const float *x;
   float *y;
   Epi ep;
   int ntiles;               // column tiles
-  int ranges;               // row ranges
+  int ranges;               // row ranges (of whole blocks)
   int64_t cost_total;       // nnz + kRowCost * rows
   float one;                // 1.0f, passed at run time (see add2)
-  int chunk_rows;           // rows per work unit
+  int H;                    // window radius (blocks)
+  int64_t nblocks;          // ceil(rows / 16)
+  int64_t x_rows;           // rows of x (>= rows: a rank's halo rows follow its own)
+  int64_t xblocks;          // ceil(x_rows / 16)
+  int tma;                  // 1: TMA tensor loads; 0: cp.async element copies
 };
-
-constexpr int64_t kRowCost = 4;  // a row's fixed cost in edge units (epilogue, topology)
 
 // ---------------------------------------------------------- packed fp32x2 --
 __device__ __forceinline__ uint64_t pk(float a, float b) {
@@ -91,8 +114,6 @@ __device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b, uint64_t one) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(one), "l"(b));
   return d;
 }
-
-// Predicated packed add: acc = on ? fl(acc + c) : acc (no select, no branch).
 __device__ __forceinline__ uint64_t add2_if(uint64_t acc, uint64_t c, uint64_t one, bool on) {
   asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q fma.rn.f32x2 %0, %0, %1, %2;\n\t}"
       : "+l"(acc)
@@ -147,13 +168,12 @@ __device__ __forceinline__ Lv<VEC> lv_add_if(const Lv<VEC> &a, const Lv<VEC> &b,
   return r;
 }
 template <int VEC>
-__device__ __forceinline__ Lv<VEC> lv_scale(const Lv<VEC> &a, uint64_t vv) {
+__device__ __forceinline__ Lv<VEC> lv_scale(const Lv<VEC> &a, float v) {
   Lv<VEC> r;
   if constexpr (VEC == 1) {
-    float v, v2;
-    upk(vv, v, v2);
     r.s = __fmul_rn(a.s, v);
   } else {
+    const uint64_t vv = pk(v, v);
 #pragma unroll
     for (int i = 0; i < Lv<VEC>::NP; ++i) r.p[i] = mul2(a.p[i], vv);
   }
@@ -175,20 +195,29 @@ __device__ __forceinline__ Lv<VEC> lv_max(const Lv<VEC> &a, const Lv<VEC> &b) {
   }
   return r;
 }
-// Unconditional non-coherent 16-byte loads straight into packed pairs.  Every
-// caller passes a valid address (inactive lanes / discarded tail items read a
-// clamped, in-bounds row), so no predicate or branch surrounds the load.
+// shared-memory row slice (ring) and global row slice (far sources)
 template <int VEC>
-__device__ __forceinline__ Lv<VEC> lv_load(const float *p) {
+__device__ __forceinline__ Lv<VEC> lv_lds(uint32_t addr) {
+  Lv<VEC> r;
+  if constexpr (VEC == 1) {
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r.s) : "r"(addr) : "memory");
+  } else if constexpr (VEC == 2) {
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(r.p[0]) : "r"(addr) : "memory");
+  } else {
+    asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(r.p[0]), "=l"(r.p[1]) : "r"(addr)
+                 : "memory");
+  }
+  return r;
+}
+template <int VEC>
+__device__ __forceinline__ Lv<VEC> lv_ldg(const float *p) {
   Lv<VEC> r;
   if constexpr (VEC == 1) {
     r.s = __ldg(p);
+  } else if constexpr (VEC == 2) {
+    asm("ld.global.nc.b64 %0, [%1];" : "=l"(r.p[0]) : "l"(p));
   } else {
-#pragma unroll
-    for (int i = 0; i < Lv<VEC>::NP; i += 2)
-      asm("ld.global.nc.v2.b64 {%0, %1}, [%2];"
-          : "=l"(r.p[i]), "=l"(r.p[i + 1])
-          : "l"(p + 2 * i));
+    asm("ld.global.nc.v2.b64 {%0, %1}, [%2];" : "=l"(r.p[0]), "=l"(r.p[1]) : "l"(p));
   }
   return r;
 }
@@ -204,18 +233,13 @@ __device__ __forceinline__ Vf<VEC> lv_out(const Lv<VEC> &a) {
   return r;
 }
 
-// One entry of a warp's topology window (16 bytes): the source row's offset
-// into x in floats, and its weight duplicated as an fp32 pair (the FMUL2
-// operand), so one broadcast LDS.128 yields everything an item needs.
-constexpr int kWin = 32;  // items per window refill
-
-__device__ __forceinline__ void win_st(uint32_t addr, uint64_t a, uint64_t b) {
-  asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(addr), "l"(a), "l"(b) : "memory");
+// Window entry (8 bytes): the source's ring byte offset (>= 0) or ~src for a
+// far source (< 0), and its weight.
+__device__ __forceinline__ void win_st(uint32_t addr, int32_t code, float v) {
+  asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(code), "f"(v) : "memory");
 }
-__device__ __forceinline__ void win_ld(uint32_t addr, uint32_t &off, uint64_t &vv) {
-  uint64_t a;
-  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(vv) : "r"(addr) : "memory");
-  off = static_cast<uint32_t>(a);
+__device__ __forceinline__ void win_ld(uint32_t addr, int32_t &code, float &v) {
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(code), "=f"(v) : "r"(addr) : "memory");
 }
 
 // ------------------------------------------------------------ the warp ----
@@ -224,56 +248,147 @@ __device__ __forceinline__ void win_ld(uint32_t addr, uint32_t &off, uint64_t &v
 template <int VEC, bool W>
 struct RowWarp {
   uint32_t win;        // shared address of this warp's window (kWin entries)
-  const int32_t *col;  // role-ordered topology
+  uint32_t ring;       // shared address of the ring + this lane's column byte
+  const int32_t *code; // role-ordered edge codes
   const float *val;    // nullptr = 1.0
   const float *xl;     // x + this lane's first column (clamped in-bounds)
   uint32_t feat;
   int lane;
-  uint64_t one;    // {1.0f, 1.0f} loaded at run time (see add2)
-  int32_t p, end;  // window holds items [p, p + kWin)
-
+  uint64_t one;        // {1.0f, 1.0f} loaded at run time (see add2)
+  int32_t p, end;      // window holds items [p, p + kWin)
+  uint32_t far;        // bit i: window item p + i is a far (global) source
   __device__ __forceinline__ void fill(int32_t at) {
     __syncwarp();
     p = at;
     const int32_t e = at + lane;
+    int32_t cd = 0;
     if (e < end) {
-      const uint32_t off = static_cast<uint32_t>(__ldg(col + e)) * feat;
+      cd = __ldg(code + e);
       const float v = W ? __ldg(val + e) : 1.0f;
-      win_st(win + lane * 16, off, pk(v, v));
+      win_st(win + lane * 8, cd, v);
     }
+    far = __ballot_sync(0xffffffffu, cd < 0);
     __syncwarp();
   }
   // install a prefetched window [at, at + kWin) ∩ [at, end): lane l's (c, v)
   __device__ __forceinline__ void install(int32_t at, int32_t c, float v) {
     __syncwarp();
     p = at;
-    if (at + lane < end) win_st(win + lane * 16, static_cast<uint32_t>(c) * feat, pk(v, v));
+    if (at + lane < end) win_st(win + lane * 8, c, v);
+    far = __ballot_sync(0xffffffffu, at + lane < end && c < 0);
     __syncwarp();
   }
   __device__ __forceinline__ void ensure(int32_t lo, int n) {
     if (lo + n > p + kWin) fill(lo);
   }
-  template <bool RAW>
+  // NEAR: the caller checked `far` -- the item is in the ring
+  template <bool RAW, bool NEAR = false>
   __device__ __forceinline__ Lv<VEC> item(int32_t e) const {
-    uint32_t off;
-    uint64_t vv;
-    win_ld(win + static_cast<uint32_t>(e - p) * 16u, off, vv);
-    const float *ptr;  // xl + off as one IMAD.WIDE.U32
-    asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(ptr) : "r"(off), "l"(xl));
-    const Lv<VEC> xv = lv_load<VEC>(ptr);
+    int32_t cd;
+    float v;
+    win_ld(win + static_cast<uint32_t>(e - p) * 8u, cd, v);
+    Lv<VEC> xv;
+    if (NEAR || cd >= 0) {
+      xv = lv_lds<VEC>(ring + static_cast<uint32_t>(cd) * (32u * VEC * 4u));
+    } else {
+      const float *ptr;  // xl + src * feat as one IMAD.WIDE.U32
+      asm("mad.wide.u32 %0, %1, %2, %3;"
+          : "=l"(ptr)
+          : "r"(static_cast<uint32_t>(~cd)), "r"(feat * 4u), "l"(xl));
+      xv = lv_ldg<VEC>(ptr);
+    }
     if (RAW || !W) return xv;
-    return lv_scale<VEC>(xv, vv);
+    return lv_scale<VEC>(xv, v);
   }
 
-  // res + c_e0 + ... + c_{e0+t-1} in order, t < 8 (warp-uniform)
+  // ---- fast path: the whole row is in the window and every source is
+  // staged in shared memory (X ring or far ring): straight-line, no checks.
+  template <bool RAW>
+  __device__ __forceinline__ Lv<VEC> it(int j) const {
+    int32_t cd;
+    float v;
+    win_ld(win + static_cast<uint32_t>(j) * 8u, cd, v);
+    const Lv<VEC> xv = lv_lds<VEC>(ring + static_cast<uint32_t>(cd) * (32u * VEC * 4u));
+    if (RAW || !W) return xv;
+    return lv_scale<VEC>(xv, v);
+  }
+  template <int N>
+  __device__ __forceinline__ Lv<VEC> seqf_n(Lv<VEC> res, int j) const {
+    Lv<VEC> c[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) c[i] = it<false>(j + i);
+#pragma unroll
+    for (int i = 0; i < N; ++i) res = lv_add<VEC>(res, c[i], one);
+    return res;
+  }
+  __device__ __forceinline__ Lv<VEC> seqf(Lv<VEC> res, int j, int t) const {
+    if (t & 4) { res = seqf_n<4>(res, j); j += 4; }
+    if (t & 2) { res = seqf_n<2>(res, j); j += 2; }
+    if (t & 1) res = seqf_n<1>(res, j);
+    return res;
+  }
+  // one role over window offsets [o, o + n), o + n <= kWin
+  template <bool IS_MAX>
+  __device__ __forceinline__ Lv<VEC> role_fast(int o, int n) const {
+    if (n <= 0) return lv_splat<VEC>(0.0f);
+    if constexpr (IS_MAX) {
+      Lv<VEC> acc = it<true>(o);
+#pragma unroll 1
+      for (int j = 1; j < n; ++j) acc = lv_max<VEC>(acc, it<true>(o + j));
+      return acc;
+    } else {
+      const Lv<VEC> c0 = it<false>(o);
+      const int m = n - 1;
+      if (m == 0) return c0;
+      if (m < 8) return lv_add<VEC>(c0, seqf(lv_splat<VEC>(-0.0f), o + 1, m), one);
+      Lv<VEC> r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = it<false>(o + 1 + j);
+      const int q = m >> 3;
+#pragma unroll 1
+      for (int g = 1; g < q; ++g) {
+        Lv<VEC> c[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) c[j] = it<false>(o + 1 + 8 * g + j);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = lv_add<VEC>(r[j], c[j], one);
+      }
+      const Lv<VEC> t = lv_add<VEC>(
+          lv_add<VEC>(lv_add<VEC>(r[0], r[1], one), lv_add<VEC>(r[2], r[3], one), one),
+          lv_add<VEC>(lv_add<VEC>(r[4], r[5], one), lv_add<VEC>(r[6], r[7], one), one), one);
+      return lv_add<VEC>(c0, seqf(t, o + 1 + 8 * q, m & 7), one);
+    }
+  }
+
+  // N consecutive items [e, e + N) of the window: one uniform branch picks
+  // the all-in-ring path (shared loads only) or the mixed one
+  template <int N, bool RAW>
+  __device__ __forceinline__ void items(int32_t e, Lv<VEC> (&c)[N]) const {
+    const uint32_t fb = (far >> (e - p)) & ((1u << N) - 1u);
+    if (fb == 0) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) c[j] = item<RAW, true>(e + j);
+    } else {
+#pragma unroll
+      for (int j = 0; j < N; ++j) c[j] = item<RAW, false>(e + j);
+    }
+  }
+  template <int N>
+  __device__ __forceinline__ Lv<VEC> seq_n(Lv<VEC> res, int32_t e) const {
+    Lv<VEC> c[N];
+    items<N, false>(e, c);
+#pragma unroll
+    for (int j = 0; j < N; ++j) res = lv_add<VEC>(res, c[j], one);
+    return res;
+  }
+  // res + c_e0 + ... + c_{e0+t-1} in order, t < 8 (warp-uniform): chunks of
+  // 4, 2, 1 so no load is wasted
   __device__ __forceinline__ Lv<VEC> seq(Lv<VEC> res, int32_t e0, int t) {
     if (t <= 0) return res;
     ensure(e0, t);
-    Lv<VEC> c[7];
-#pragma unroll
-    for (int i = 0; i < 7; ++i) c[i] = item<false>(e0 + (i < t ? i : 0));
-#pragma unroll
-    for (int i = 0; i < 7; ++i) res = lv_add_if<VEC>(res, c[i], one, i < t);
+    if (t & 4) { res = seq_n<4>(res, e0); e0 += 4; }
+    if (t & 2) { res = seq_n<2>(res, e0); e0 += 2; }
+    if (t & 1) res = seq_n<1>(res, e0);
     return res;
   }
 
@@ -282,15 +397,13 @@ struct RowWarp {
     const int q = n >> 3;
     Lv<VEC> r[8];
     ensure(e0, 8);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = item<false>(e0 + j);
+    items<8, false>(e0, r);
 #pragma unroll 1
     for (int g = 1; g < q; ++g) {
       const int32_t b = e0 + 8 * g;
       ensure(b, 8);
       Lv<VEC> c[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) c[j] = item<false>(b + j);
+      items<8, false>(b, c);
 #pragma unroll
       for (int j = 0; j < 8; ++j) r[j] = lv_add<VEC>(r[j], c[j], one);
     }
@@ -362,7 +475,7 @@ __device__ __forceinline__ Lv<VEC> RowWarp<VEC, W>::role(int32_t e0, int32_t n) 
   ensure(e0, n < kWin ? static_cast<int>(n) : kWin);  // the row's window normally covers it
   if constexpr (IS_MAX) {
     Lv<VEC> acc = item<true>(e0);
-    const int32_t rend = e0 + n;  // this role's end (end is the row's)
+    const int32_t rend = e0 + n;
 #pragma unroll 1
     for (int32_t b = e0 + 1; b < rend; b += 8) {
       const int cnt = rend - b < 8 ? rend - b : 8;
@@ -384,9 +497,10 @@ __device__ __forceinline__ Lv<VEC> RowWarp<VEC, W>::role(int32_t e0, int32_t n) 
   }
 }
 
-__device__ __forceinline__ int64_t range_start(const GArgs &a, int k) {
+// First block of row range k (ranges are balanced by nnz + kRowCost * rows).
+__device__ __forceinline__ int64_t range_block(const GArgs &a, int k) {
   if (k <= 0) return 0;
-  if (k >= a.ranges) return a.rows;
+  if (k >= a.ranges) return a.nblocks;
   const int64_t target = a.cost_total / a.ranges * k + (a.cost_total % a.ranges) * k / a.ranges;
   int64_t lo = 0, hi = a.rows;  // first r with cost(r) >= target
   while (lo < hi) {
@@ -394,7 +508,7 @@ __device__ __forceinline__ int64_t range_start(const GArgs &a, int k) {
     if (static_cast<int64_t>(a.row_ptr[m]) + kRowCost * m < target) lo = m + 1;
     else hi = m;
   }
-  return lo;
+  return std::min<int64_t>((lo + kRB - 1) / kRB, a.nblocks);
 }
 
 template <int VEC>
@@ -414,22 +528,38 @@ __device__ __forceinline__ Vf<VEC> combine2(int op, const Vf<VEC> &I, bool ti, c
   return splat<VEC>(0.0f);
 }
 
+// Kernel modes: the training path (both roles, sum combine) gets its own
+// instantiation without the generic epilogue's runtime dispatch.
+constexpr int kModeSum3 = 0;   // role_mask 3, op sum (flags: GIN / RELU_MASK only)
+constexpr int kModeAny = 1;    // any role mask, sum or mean, any flags
+constexpr int kModeMax = 2;    // any role mask, max
+
 // One destination row (both roles, epilogue) for this lane's columns.
-template <int VEC, bool IS_MAX, bool W>
+template <int VEC, int MODE, bool W>
 __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64_t r, int32_t s,
                                        int32_t e, int32_t m, int64_t fcol, bool act) {
+  constexpr bool IS_MAX = MODE == kModeMax;
   const int64_t ld = a.feat;
-  const int32_t ni = (a.mask & 1) ? m - s : 0;
-  const int32_t no = (a.mask & 2) ? e - m : 0;
-  const Vf<VEC> I = lv_out<VEC>(w.template role<IS_MAX>(s, ni));
-  const Vf<VEC> O = lv_out<VEC>(w.template role<IS_MAX>(m, no));
+  const int32_t ni = (MODE == kModeSum3 || (a.mask & 1)) ? m - s : 0;
+  const int32_t no = (MODE == kModeSum3 || (a.mask & 2)) ? e - m : 0;
+  Vf<VEC> I, O;
+  if (e - s <= kWin && w.far == 0) {
+    I = lv_out<VEC>(w.template role_fast<IS_MAX>(0, ni));
+    O = lv_out<VEC>(w.template role_fast<IS_MAX>(m - s, no));
+  } else {
+    I = lv_out<VEC>(w.template role<IS_MAX>(s, ni));
+    O = lv_out<VEC>(w.template role<IS_MAX>(m, no));
+  }
   if (!act) return;
   float *yp = a.y + r * ld + fcol;
-  const int64_t d = (a.ep.op == AG_OP_MEAN && a.ep.deg) ? a.ep.deg[r] : 1;
   Vf<VEC> out;
-  if (a.mask == 3) {
+  if constexpr (MODE == kModeSum3) {
+    out = vadd<VEC>(I, O);
+  } else if (a.mask == 3) {
+    const int64_t d = (a.ep.op == AG_OP_MEAN && a.ep.deg) ? a.ep.deg[r] : 1;
     out = combine2<VEC>(a.ep.op, I, ni > 0, O, no > 0, d);
   } else {
+    const int64_t d = (a.ep.op == AG_OP_MEAN && a.ep.deg) ? a.ep.deg[r] : 1;
     const Vf<VEC> v = (a.mask == 1) ? I : O;
     const bool t = (a.mask == 1) ? ni > 0 : no > 0;
     if (!(a.ep.flags & AG_EPI_COMBINE)) {
@@ -441,8 +571,12 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
       out = combine2<VEC>(a.ep.op, v, t, ldv_rw<VEC>(yp), ot, d);
     }
   }
-  if (a.ep.flags & AG_EPI_GIN)
-    out = vadd<VEC>(vscale<VEC>(a.ep.gin_scale, ldv<VEC>(a.x + r * ld + fcol)), out);
+  if (a.ep.flags & AG_EPI_GIN) {
+    // x[r] sits in the ring (its own block is always resident)
+    const uint32_t rr = static_cast<uint32_t>(((r / kRB) % kSlots) * kRB + (r % kRB));
+    const Vf<VEC> xr = lv_out<VEC>(lv_lds<VEC>(w.ring + rr * (32u * VEC * 4u)));
+    out = vadd<VEC>(vscale<VEC>(a.ep.gin_scale, xr), out);
+  }
   if (a.ep.flags & AG_EPI_RELU_MASK) {
     const Vf<VEC> h = ldv<VEC>(a.ep.relu_src + r * ld + fcol);
 #pragma unroll
@@ -451,80 +585,416 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
   stv<VEC>(yp, out);
 }
 
-// Work order.  Units are (chunk of kChunkRows consecutive rows, column tile),
-// tile fastest; global warp gw takes units gw, gw + W, gw + 2W, ... (W = all
-// warps of the persistent grid).  Every warp advances at about the same rate,
-// so the whole GPU sweeps the row space as ONE narrow wavefront: the source
-// rows the reorder keeps near each destination are re-read from L2 (and from
-// L1: a CTA's warps hold adjacent chunks, i.e. one contiguous band of rows and
-// both column tiles of it), and no atomics or CTA barriers are needed.
-// Within its sequence a warp software-pipelines the next row's row_ptr / mid /
-// first kWin (col, val) while the current row gathers.
-template <int VEC, bool IS_MAX, bool W>
-__global__ void __launch_bounds__(kThreads, 2) gather_kernel(GArgs a) {
-  constexpr int T = 32 * VEC;
-  __shared__ __align__(16) uint64_t wins[kThreads / 32][kWin * 2];
-  const int warp = threadIdx.x >> 5;
-  RowWarp<VEC, W> w;
-  w.win = static_cast<uint32_t>(__cvta_generic_to_shared(wins[warp]));
-  w.col = a.col;
-  w.val = a.val;
-  w.feat = static_cast<uint32_t>(a.feat);
-  w.lane = threadIdx.x & 31;
-  w.one = pk(a.one, a.one);
-  w.p = 0;
-  w.end = 0;
-  const int CR = a.chunk_rows;
-  const int64_t nrc = (a.rows + CR - 1) / CR;
-  const int64_t nunits = nrc * a.ntiles;
-  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + warp;
-  const int64_t nw = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
-  // cursor over this warp's (unit, row-in-chunk) sequence
-  int64_t k = gw;
-  int j = 0;
-  auto row_of = [&](int64_t kk, int jj) { return (kk / a.ntiles) * CR + jj; };
-  auto advance = [&](int64_t &kk, int &jj) {
-    ++jj;
-    if (jj == CR || row_of(kk, jj) >= a.rows) { kk += nw; jj = 0; }
-  };
-  int32_t ns = 0, ne = 0, nm = 0, nc = 0;
-  float nv = 1.0f;
-  auto prefetch = [&](int64_t kk, int jj) {
-    if (kk < nunits) {
-      const int64_t rr = row_of(kk, jj);
-      ns = a.row_ptr[rr];
-      ne = a.row_ptr[rr + 1];
-      nm = a.mid ? a.mid[rr] : (a.mask == 1 ? ne : ns);
-      const int32_t ed = ns + w.lane;
-      nc = ed < ne ? __ldg(a.col + ed) : 0;
-      nv = (W && ed < ne) ? __ldg(a.val + ed) : 1.0f;
-    }
-  };
-  prefetch(k, j);
-  int cur_tile = -1;
-  int64_t fcol = 0;
-  bool act = false;
-#pragma unroll 1
-  while (k < nunits) {
-    const int tile = static_cast<int>(k % a.ntiles);
-    if (tile != cur_tile) {
-      cur_tile = tile;
-      fcol = static_cast<int64_t>(tile) * T + w.lane * VEC;
-      act = fcol < a.feat;
-      w.xl = a.x + (act ? fcol : 0);
-    }
-    const int64_t r = row_of(k, j);
-    const int32_t s = ns, e = ne, m = nm;
-    w.end = e;
-    w.install(s, nc, nv);
-    int64_t k2 = k;
-    int j2 = j;
-    advance(k2, j2);
-    prefetch(k2, j2);
-    do_row<VEC, IS_MAX, W>(a, w, r, s, e, m, fcol, act);
-    k = k2;
-    j = j2;
+template <int VEC>
+struct SlabGeom {
+  static constexpr int T = 32 * VEC;
+  static constexpr uint32_t kRowBytes = T * 4;
+  static constexpr uint32_t kSlotBytes = kRB * kRowBytes;
+  static constexpr uint32_t kFarSlotBytes = kFarMax * kRowBytes;
+  static constexpr uint32_t kRingBytes = kSlots * kSlotBytes + kFarSlots * kFarSlotBytes;
+  static constexpr uint32_t kBarBytes = (2 * kSlots + 2 * kFarSlots) * 8;
+  static constexpr uint32_t kWinBytes = kCons * kWin * 8;
+  static constexpr size_t kSmem = kRingBytes + kBarBytes + kWinBytes;
+};
+
+// Bulk L2 prefetch of [p, p + bytes), widened to 16-byte granules.
+__device__ __forceinline__ void l2_prefetch(const void *p, int64_t bytes) {
+  if (bytes <= 0) return;
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t hi = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo),
+               "r"(static_cast<uint32_t>(hi - lo))
+               : "memory");
+}
+// One lane per block: pull block b's rows of the topology into L2 so the
+// consumers' per-row loads (row_ptr, mid, first 32 codes / weights) hit L2.
+// The block's edge range [e0, e1) was loaded one batch earlier (topo_bounds).
+struct TopoBounds {
+  int32_t e0, e1;
+};
+__device__ __forceinline__ TopoBounds topo_bounds(const GArgs &a, uint32_t b, uint32_t kb1) {
+  TopoBounds t{0, 0};
+  if (b < kb1) {
+    const int64_t r0 = static_cast<int64_t>(b) * kRB;
+    t.e0 = a.row_ptr[r0];
+    t.e1 = a.row_ptr[std::min<int64_t>(r0 + kRB, a.rows)];
   }
+  return t;
+}
+__device__ __forceinline__ void prefetch_topology(const GArgs &a, uint32_t b, uint32_t kb0,
+                                                  uint32_t kb1, TopoBounds tb) {
+  if (b < kb0 || b >= kb1) return;
+  const int64_t r0 = static_cast<int64_t>(b) * kRB;
+  const int64_t r1 = std::min<int64_t>(r0 + kRB, a.rows);
+  const int64_t e0 = tb.e0, e1 = tb.e1;
+  l2_prefetch(a.row_ptr + r0, (r1 - r0 + 1) * 4);
+  if (a.mid) l2_prefetch(a.mid + r0, (r1 - r0) * 4);
+  l2_prefetch(a.code + e0, (e1 - e0) * 4);
+  if (a.val) l2_prefetch(a.val + e0, (e1 - e0) * 4);
+}
+
+// Cursor over a ring of NS slots: slot = b % NS (absolute, so the edge codes
+// do not depend on the range) and the parity of the fill, ((b - b0) / NS) & 1
+// with b0 the first block the range puts in the ring.  Advanced one block at
+// a time -- no divisions on the hot path.
+template <int NS>
+struct RingPos {
+  uint32_t slot, off, phase;
+  __device__ __forceinline__ void init(uint32_t b, uint32_t b0) {
+    slot = b % NS;
+    off = (b - b0) % NS;
+    phase = ((b - b0) / NS) & 1u;
+  }
+  __device__ __forceinline__ void next() {
+    if (++slot == NS) slot = 0;
+    if (++off == NS) { off = 0; phase ^= 1u; }
+  }
+};
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+// X producer warp: streams X blocks [Llo, Lhi) of column tile `tile` into
+// the X ring, one TMA tensor tile per block (cp.async element copies when x
+// is not TMA-addressable), refilling a slot once every consumer released it.
+// It also pulls the consumers' topology into L2 ahead of them.
+template <int VEC>
+__device__ __forceinline__ void produce_x(const GArgs &a, const CUtensorMap *map, uint32_t ring,
+                                          uint32_t full, uint32_t empty, uint32_t Llo,
+                                          uint32_t Lhi, uint32_t kb0, uint32_t kb1, int tile,
+                                          int lane) {
+  using G = SlabGeom<VEC>;
+  const int64_t c0 = static_cast<int64_t>(tile) * G::T;
+  RingPos<kSlots> pos;
+  pos.init(Llo, Llo);
+  // topology bounds are loaded one 32-block batch ahead of their use
+  TopoBounds tb = topo_bounds(a, Llo + lane, kb1);
+  TopoBounds tb_next = topo_bounds(a, Llo + 32 + lane, kb1);
+  for (uint32_t t = Llo; t < Lhi; ++t, pos.next()) {
+    const uint32_t i = t - Llo;
+    if (i % 32 == 0) {
+      prefetch_topology(a, t + lane, kb0, kb1, tb);
+      tb = tb_next;
+      tb_next = topo_bounds(a, t + 64 + lane, kb1);
+    }
+    const bool refill = i >= kSlots;  // fill n >= 1 waits for the release of fill n - 1
+    if (a.tma) {
+      if (lane == 0) {
+        if (refill) mbar_wait_sleep(empty + pos.slot * 8, pos.phase ^ 1u);
+        mbar_expect_tx(full + pos.slot * 8, G::kSlotBytes);
+        tma_load_2d(ring + pos.slot * G::kSlotBytes, map, full + pos.slot * 8,
+                    static_cast<int>(c0), static_cast<int>(t * kRB));
+      }
+    } else {
+      if (refill) mbar_wait_sleep(empty + pos.slot * 8, pos.phase ^ 1u);
+#pragma unroll 4
+      for (int rr = 0; rr < kRB; ++rr) {
+        const int64_t row = static_cast<int64_t>(t) * kRB + rr;  // past x_rows: zero
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          const int64_t c = c0 + lane * VEC + j;
+          const bool ok = row < a.x_rows && c < a.feat;
+          const float *src = ok ? a.x + row * a.feat + c : a.x;
+          cp_async4(ring + pos.slot * G::kSlotBytes + (rr * G::T + lane * VEC + j) * 4, src,
+                    ok ? 4 : 0);
+        }
+      }
+      cp_async_mbar_arrive(full + pos.slot * 8);
+    }
+    __syncwarp();
+  }
+}
+
+// Far producer warp: for every consumer block f in [kb0, kb1), copies the
+// tile columns of its staged far sources (far_src, one bulk copy per source
+// row, lanes in parallel) into far-ring slot f % kFarSlots as soon as the
+// consumers released that slot's previous block -- kFarSlots blocks ahead.
+template <int VEC>
+__device__ __forceinline__ void produce_far(const GArgs &a, uint32_t ring, uint32_t ffull,
+                                            uint32_t fempty, uint32_t kb0, uint32_t kb1,
+                                            int tile, int lane) {
+  using G = SlabGeom<VEC>;
+  const uint32_t far_ring = ring + kSlots * G::kSlotBytes;
+  const int64_t c0 = static_cast<int64_t>(tile) * G::T;
+  const uint32_t tile_bytes =
+      static_cast<uint32_t>(std::min<int64_t>(G::T, a.feat - c0)) * 4u;  // partial last tile
+  RingPos<kFarSlots> fpos;
+  fpos.init(kb0, kb0);
+  // far source lists are loaded three blocks ahead, counts one batch ahead
+  auto far_list = [&](uint32_t f) -> int32_t {
+    return (f < kb1 && lane < kFarMax) ? a.far_src[static_cast<int64_t>(f) * kFarMax + lane] : 0;
+  };
+  auto far_counts = [&](uint32_t f) -> int32_t { return f + lane < kb1 ? a.far_cnt[f + lane] : 0; };
+  int32_t fs0 = far_list(kb0), fs1 = far_list(kb0 + 1), fs2 = far_list(kb0 + 2);
+  int32_t fc = far_counts(kb0), fc_next = far_counts(kb0 + 32);
+  for (uint32_t f = kb0; f < kb1; ++f, fpos.next()) {
+    const uint32_t fi = f - kb0;
+    const int cnt = __shfl_sync(0xffffffffu, fc, fi & 31);
+    const int32_t src = fs0;
+    fs0 = fs1;
+    fs1 = fs2;
+    fs2 = far_list(f + 3);
+    if ((fi & 31) == 31) {
+      fc = fc_next;
+      fc_next = far_counts(f + 33);
+    }
+    const uint32_t slot_base = far_ring + fpos.slot * G::kFarSlotBytes;
+    const bool refill = fi >= kFarSlots;
+    if (a.tma) {
+      if (lane == 0) {
+        if (refill) mbar_wait_sleep(fempty + fpos.slot * 8, fpos.phase ^ 1u);
+        mbar_expect_tx(ffull + fpos.slot * 8, static_cast<uint32_t>(cnt) * tile_bytes);
+      }
+      __syncwarp();
+      if (lane < cnt)
+        bulk_g2s(slot_base + lane * G::kRowBytes, a.x + static_cast<int64_t>(src) * a.feat + c0,
+                 tile_bytes, ffull + fpos.slot * 8);
+    } else {
+      if (refill) mbar_wait_sleep(fempty + fpos.slot * 8, fpos.phase ^ 1u);
+      for (int j = 0; j < cnt; ++j) {
+        const int32_t sj = __shfl_sync(0xffffffffu, src, j);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          const int64_t c = c0 + lane * VEC + v;
+          const bool ok = c < a.feat;
+          cp_async4(slot_base + j * G::kRowBytes + (lane * VEC + v) * 4,
+                    ok ? a.x + static_cast<int64_t>(sj) * a.feat + c : a.x, ok ? 4 : 0);
+        }
+      }
+      cp_async_mbar_arrive(ffull + fpos.slot * 8);
+    }
+    __syncwarp();
+  }
+}
+
+template <int VEC, int MODE, bool W>
+__global__ void __launch_bounds__(kThreads, 1)
+    slab_kernel(const __grid_constant__ CUtensorMap tmap, GArgs a) {
+  using G = SlabGeom<VEC>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ int64_t s_kb[2];
+  const uint32_t ring = su32(smem);
+  const uint32_t full = ring + G::kRingBytes;
+  const uint32_t empty = full + kSlots * 8;
+  const uint32_t ffull = empty + kSlots * 8;
+  const uint32_t fempty = ffull + kFarSlots * 8;
+  const uint32_t wins = fempty + kFarSlots * 8;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t H = static_cast<uint32_t>(a.H);
+  const int64_t units = static_cast<int64_t>(a.ranges) * a.ntiles;
+  if (a.tma && threadIdx.x == kCons * 32) tma_prefetch_desc(&tmap);
+
+#pragma unroll 1
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int tile = static_cast<int>(u % a.ntiles);
+    const int range = static_cast<int>(u / a.ntiles);
+    if (threadIdx.x == 0) {
+      s_kb[0] = range_block(a, range);
+      s_kb[1] = range_block(a, range + 1);
+      const uint32_t n = a.tma ? 1u : 32u;
+      for (int s = 0; s < kSlots; ++s) {
+        mbar_init(full + s * 8, n);
+        mbar_init(empty + s * 8, kCons);
+      }
+      for (int s = 0; s < kFarSlots; ++s) {
+        mbar_init(ffull + s * 8, n);
+        mbar_init(fempty + s * 8, kCons);
+      }
+      fence_mbar_init();
+    }
+    __syncthreads();
+    const uint32_t kb0 = static_cast<uint32_t>(s_kb[0]), kb1 = static_cast<uint32_t>(s_kb[1]);
+    const uint32_t Llo = kb0 > H ? kb0 - H : 0u;
+    const uint32_t Lhi = static_cast<uint32_t>(std::min<int64_t>(a.xblocks, int64_t(kb1) + H));
+    if (kb0 < kb1) {
+      if (warp == kCons) {
+        produce_x<VEC>(a, &tmap, ring, full, empty, Llo, Lhi, kb0, kb1, tile, lane);
+      } else if (warp == kCons + 1) {
+        produce_far<VEC>(a, ring, ffull, fempty, kb0, kb1, tile, lane);
+      } else {
+        RowWarp<VEC, W> w;
+        const int64_t fcol = static_cast<int64_t>(tile) * G::T + lane * VEC;
+        const bool act = fcol < a.feat;
+        w.win = wins + warp * kWin * 8;
+        w.ring = ring + lane * VEC * 4;
+        w.code = a.code;
+        w.val = a.val;
+        w.xl = a.x + (act ? fcol : 0);
+        w.feat = static_cast<uint32_t>(a.feat);
+        w.lane = lane;
+        w.one = pk(a.one, a.one);
+        w.p = 0;
+        w.end = 0;
+        w.far = 0;
+        // two-stage topology pipeline: row bounds two rows ahead, the first
+        // 32 codes / weights one row ahead
+        int32_t bs = 0, be = 0, bm = 0;          // stage 1 (row + 2 kCons)
+        int32_t ns = 0, ne = 0, nm = 0, nc = 0;  // stage 2 (row + kCons)
+        float nv = 1.0f;
+        auto bounds = [&](uint32_t rr) {
+          if (rr < a.rows) {
+            bs = a.row_ptr[rr];
+            be = a.row_ptr[rr + 1];
+            bm = (MODE == kModeSum3 || a.mid) ? a.mid[rr] : (a.mask == 1 ? be : bs);
+          }
+        };
+        auto codes = [&]() {
+          ns = bs;
+          ne = be;
+          nm = bm;
+          const int32_t ed = ns + lane;
+          nc = ed < ne ? __ldg(a.code + ed) : 0;
+          nv = (W && ed < ne) ? __ldg(a.val + ed) : 1.0f;
+        };
+        const uint32_t r0 = kb0 * kRB;
+        const uint32_t r1 = static_cast<uint32_t>(std::min<int64_t>(int64_t(kb1) * kRB, a.rows));
+        // X ring: blocks [Llo, waited_end) have been waited on
+        uint32_t waited_end = Llo;
+        RingPos<kSlots> wpos;
+        wpos.init(Llo, Llo);
+        RingPos<kSlots> rpos;  // next X block to release
+        rpos.init(Llo, Llo);
+        RingPos<kFarSlots> fpos;  // far slot of the current block
+        fpos.init(kb0, kb0);
+        auto enter = [&](uint32_t k) {
+          const uint32_t need_end = std::min(k + H + 1, Lhi);
+          for (; waited_end < need_end; ++waited_end, wpos.next())
+            mbar_wait(full + wpos.slot * 8, wpos.phase);
+          mbar_wait(ffull + fpos.slot * 8, fpos.phase);
+        };
+        auto leave = [&](uint32_t k) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(fempty + fpos.slot * 8);
+          fpos.next();
+          if (k >= Llo + H) {  // block k - H leaves the window of every later block
+            if (lane == 0) mbar_arrive(empty + rpos.slot * 8);
+            rpos.next();
+          }
+        };
+        uint32_t kcur = kb0;
+        enter(kb0);
+        bounds(r0 + warp);
+        codes();
+        bounds(r0 + warp + kCons);
+#pragma unroll 1
+        for (uint32_t r = r0 + warp; r < r1; r += kCons) {
+          const uint32_t k = r / kRB;
+          while (kcur != k) {
+            leave(kcur);
+            ++kcur;
+            enter(kcur);
+          }
+          const int32_t s = ns, e = ne, m = nm;
+          w.end = e;
+          w.install(s, nc, nv);
+          codes();
+          bounds(r + 2 * kCons);
+          do_row<VEC, MODE, W>(a, w, r, s, e, m, fcol, act);
+        }
+        while (true) {
+          leave(kcur);
+          if (++kcur >= kb1) break;
+          enter(kcur);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < kSlots; ++s) {
+        mbar_inval(full + s * 8);
+        mbar_inval(empty + s * 8);
+      }
+      for (int s = 0; s < kFarSlots; ++s) {
+        mbar_inval(ffull + s * 8);
+        mbar_inval(fempty + s * 8);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------- window radius (per graph) --
+constexpr int kHistBins = 64;
+
+__global__ void block_dist_hist_kernel(int64_t rows, const int32_t *row_ptr, const int32_t *col,
+                                       unsigned long long *hist) {
+  __shared__ unsigned int h[kHistBins + 1];
+  for (int i = threadIdx.x; i <= kHistBins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rb = r / kRB;
+    for (int32_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+      int64_t d = static_cast<int64_t>(col[e] / kRB) - rb;
+      if (d < 0) d = -d;
+      atomicAdd(&h[d < kHistBins ? d : kHistBins], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= kHistBins; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], static_cast<unsigned long long>(h[i]));
+}
+
+int env_int(const char *name, int dflt) {
+  const char *v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+// largest window radius: >= 8 blocks of drift slack between the fastest and
+// slowest consumer warp
+constexpr int kMaxWindow = (kSlots - 9) / 2;
+
+template <int VEC>
+int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
+  using G = SlabGeom<VEC>;
+  auto k = mode == kModeMax
+               ? (a.val ? slab_kernel<VEC, kModeMax, true> : slab_kernel<VEC, kModeMax, false>)
+           : mode == kModeSum3
+               ? (a.val ? slab_kernel<VEC, kModeSum3, true> : slab_kernel<VEC, kModeSum3, false>)
+               : (a.val ? slab_kernel<VEC, kModeAny, true> : slab_kernel<VEC, kModeAny, false>);
+  a.H = window;
+  a.nblocks = (a.rows + kRB - 1) / kRB;
+  a.xblocks = (a.x_rows + kRB - 1) / kRB;
+  a.ntiles = static_cast<int>((a.feat + G::T - 1) / G::T);
+  const size_t smem = G::kSmem;
+  AG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  const int sms = sm_count();
+  // ~2 units (range x tile) per CTA, ranges of >= 4 blocks
+  int64_t ranges = (2LL * sms + a.ntiles - 1) / a.ntiles;
+  ranges = std::max<int64_t>(1, std::min<int64_t>(ranges, a.nblocks / 4));
+  a.ranges = static_cast<int>(ranges);
+  const int64_t units = ranges * a.ntiles;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, sms)));
+
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  a.tma = 0;
+  const bool tma_ok = a.feat % 4 == 0 && (reinterpret_cast<uintptr_t>(a.x) % 16) == 0 &&
+                      env_int("AG_SLAB_NO_TMA", 0) == 0;
+  if (tma_ok) {
+    TmaEncodeFn enc = tma_encode_fn();
+    if (enc) {
+      cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.feat), static_cast<cuuint64_t>(a.x_rows)};
+      cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.feat) * 4};
+      cuuint32_t box[2] = {static_cast<cuuint32_t>(G::T), static_cast<cuuint32_t>(kRB)};
+      cuuint32_t es[2] = {1, 1};
+      CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(a.x), dims,
+                       strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r == CUDA_SUCCESS) a.tma = 1;
+    }
+  }
+  k<<<grid, kThreads, smem, st>>>(map, a);
+  AG_LAUNCH_CHECK("slab_kernel");
+  return AG_OK;
 }
 
 // -------------------------------------------------- role-ordered CSR build --
@@ -549,36 +1019,63 @@ __global__ void role_csr_kernel(int64_t rows, const int32_t *row_ptr, const int3
   }
 }
 
-int env_int(const char *name, int dflt) {
-  const char *v = std::getenv(name);
-  return v ? std::atoi(v) : dflt;
-}
-
-template <int VEC>
-int launch_gather(GArgs a, bool is_max, cudaStream_t st) {
-  constexpr int T = 32 * VEC;
-  auto k = is_max ? (a.val ? gather_kernel<VEC, true, true> : gather_kernel<VEC, true, false>)
-                  : (a.val ? gather_kernel<VEC, false, true> : gather_kernel<VEC, false, false>);
-  // prefer L1 over shared memory: the gathers' reuse lives in L1
-  AG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 8));
-  int per_sm = 0;
-  AG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0));
-  if (per_sm < 1) per_sm = 1;
-  a.ntiles = static_cast<int>((a.feat + T - 1) / T);
-  a.chunk_rows = std::max(1, env_int("AG_GATHER_CHUNK", 16));
-  const int64_t units = (a.rows + a.chunk_rows - 1) / a.chunk_rows * a.ntiles;
-  const int64_t warps = (units + 0);
-  int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;
-  grid = std::max<int64_t>(1, std::min(grid, (warps + kThreads / 32 - 1) / (kThreads / 32)));
-  k<<<(unsigned)grid, kThreads, 0, st>>>(a);
-  AG_LAUNCH_CHECK("gather_kernel");
-  return AG_OK;
+// Edge codes of the slab kernel, one thread per 16-row block (edges in the
+// given order).  A source within `window` blocks of the destination's block
+// is an X-ring row, slot-major ((src / 16) % kSlots) * 16 + src % 16.  A
+// farther one is staged in the far ring: the block's j-th distinct far
+// source (j < kFarMax) is row kFarRow0 + (block % kFarSlots) * kFarMax + j
+// and far_src[block * kFarMax + j] = src.  Beyond kFarMax distinct far
+// sources the code is ~src (read from global memory).
+__global__ void slab_code_kernel(int64_t rows, const int32_t *row_ptr, const int32_t *col,
+                                 int32_t window, int32_t *code, int32_t *far_cnt,
+                                 int32_t *far_src) {
+  const int64_t nb = (rows + kRB - 1) / kRB;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    int32_t staged[kFarMax];
+    int j = 0;
+    const int64_t r1 = std::min<int64_t>(b * kRB + kRB, rows);
+    for (int64_t r = b * kRB; r < r1; ++r) {
+      for (int32_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+        const int32_t c = col[e];
+        const int64_t sb = c / kRB;
+        const int64_t d = sb - b;
+        if (d >= -window && d <= window) {
+          code[e] = static_cast<int32_t>((sb % kSlots) * kRB + c % kRB);
+          continue;
+        }
+        int k = 0;
+        while (k < j && staged[k] != c) ++k;
+        if (k == j && j < kFarMax) staged[j++] = c;
+        code[e] = k < j ? static_cast<int32_t>(kFarRow0 + (b % kFarSlots) * kFarMax + k) : ~c;
+      }
+    }
+    far_cnt[b] = j;
+    for (int k = 0; k < j; ++k) far_src[b * kFarMax + k] = staged[k];
+  }
 }
 
 }  // namespace
 }  // namespace ag
 
 using namespace ag;
+
+extern "C" int ag_slab_far_capacity(void) { return kFarMax; }
+
+extern "C" int ag_slab_codes(int64_t num_rows, const int32_t *row_ptr, const int32_t *col_idx,
+                             int32_t window, int32_t *codes, int32_t *far_cnt, int32_t *far_src,
+                             void *stream) {
+  if (num_rows < 0) return fail(AG_ERR_VALUE, "negative sizes");
+  if (window < 0 || window > kMaxWindow)
+    return fail(AG_ERR_VALUE, "window must be in [0, %d]", kMaxWindow);
+  if (num_rows > 2147483647LL) return fail(AG_ERR_VALUE, "too many rows for int32 CSR");
+  if (num_rows == 0) return AG_OK;
+  const int64_t nb = (num_rows + kRB - 1) / kRB;
+  slab_code_kernel<<<grid_for(nb, 128), 128, 0, as_stream(stream)>>>(
+      num_rows, row_ptr, col_idx, window, codes, far_cnt, far_src);
+  AG_LAUNCH_CHECK("slab_code_kernel");
+  return AG_OK;
+}
 
 extern "C" int ag_role_csr_build(int64_t num_rows, const int32_t *row_ptr, const int32_t *col_idx,
                                  const float *val, int64_t block_size, int32_t *role_col,
@@ -594,12 +1091,46 @@ extern "C" int ag_role_csr_build(int64_t num_rows, const int32_t *row_ptr, const
   return AG_OK;
 }
 
+extern "C" int ag_slab_window(int64_t num_rows, const int32_t *row_ptr, const int32_t *col_idx,
+                              double coverage, int32_t *window, void *stream) {
+  if (num_rows < 0) return fail(AG_ERR_VALUE, "negative sizes");
+  if (window == nullptr) return fail(AG_ERR_VALUE, "window output is NULL");
+  *window = 0;
+  if (num_rows == 0) return AG_OK;
+  cudaStream_t st = as_stream(stream);
+  Scratch hist;
+  AG_CUDA(hist.alloc((kHistBins + 1) * sizeof(unsigned long long), st));
+  AG_CUDA(cudaMemsetAsync(hist.ptr, 0, (kHistBins + 1) * sizeof(unsigned long long), st));
+  block_dist_hist_kernel<<<grid_for(num_rows, 256, 148LL * 8), 256, 0, st>>>(
+      num_rows, row_ptr, col_idx, hist.as<unsigned long long>());
+  AG_LAUNCH_CHECK("block_dist_hist_kernel");
+  unsigned long long h[kHistBins + 1];
+  AG_CUDA(cudaMemcpyAsync(h, hist.ptr, sizeof(h), cudaMemcpyDeviceToHost, st));
+  AG_CUDA(cudaStreamSynchronize(st));
+  // smallest radius whose ring covers `coverage` of what the largest
+  // supported radius would cover
+  const int hmax = kMaxWindow;
+  unsigned long long total = 0;
+  for (int d = 0; d <= hmax && d < kHistBins; ++d) total += h[d];
+  unsigned long long acc = 0;
+  int H = 0;
+  for (int d = 0; d <= hmax && d < kHistBins; ++d) {
+    acc += h[d];
+    H = d;
+    if (static_cast<double>(acc) >= coverage * static_cast<double>(total)) break;
+  }
+  *window = H;
+  return AG_OK;
+}
+
 extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                              const int32_t *row_ptr, const int32_t *role_mid,
-                             const int32_t *col_idx, const float *val, int64_t num_edges,
+                             const int32_t *codes, const int32_t *far_cnt,
+                             const int32_t *far_src, const float *val, int64_t num_edges,
                              const float *x, float *y, int32_t op, int32_t epi_flags,
                              const uint8_t *other_touched, const int64_t *deg, float gin_scale,
-                             const float *relu_src, void *stream) {
+                             const float *relu_src, int64_t x_rows, int32_t window,
+                             void *stream) {
   if (num_rows < 0 || feat < 0 || num_edges < 0) return fail(AG_ERR_VALUE, "negative sizes");
   if (op < AG_OP_SUM || op > AG_OP_MAX) return fail(AG_ERR_KERNEL, "unknown op %d", op);
   if (role_mask < 1 || role_mask > 3) return fail(AG_ERR_VALUE, "role_mask must be 1, 2 or 3");
@@ -609,21 +1140,41 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
     return fail(AG_ERR_KERNEL, "mean combine requires the full-graph degree vector");
   if ((epi_flags & AG_EPI_RELU_MASK) && relu_src == nullptr)
     return fail(AG_ERR_VALUE, "AG_EPI_RELU_MASK needs relu_src");
+  if (window < 0 || window > kMaxWindow)
+    return fail(AG_ERR_VALUE, "window must be in [0, %d]", kMaxWindow);
+  if (x_rows < num_rows) return fail(AG_ERR_VALUE, "x_rows must be >= num_rows");
   if (num_rows == 0 || feat == 0) return AG_OK;
-  if (num_rows > 2147483647LL || num_edges > 2147483647LL)
+  if (x_rows > 2147483647LL || num_edges > 2147483647LL)
     return fail(AG_ERR_VALUE, "too many rows or edges for int32 CSR");
-  if (num_rows * feat > 4294967295LL)
-    return fail(AG_ERR_VALUE, "feature matrix too large for 32-bit row offsets");
   cudaStream_t st = as_stream(stream);
-  GArgs a{num_rows, static_cast<int>(feat), role_mask, row_ptr, role_mid, col_idx, val, x, y,
-          Epi{op, epi_flags, other_touched, deg, x, feat, gin_scale, relu_src}, 1, 1, 0, 1.0f,
-          16};
+  GArgs a{};
+  a.rows = num_rows;
+  a.x_rows = x_rows;
+  a.feat = static_cast<int>(feat);
+  a.mask = role_mask;
+  a.row_ptr = row_ptr;
+  a.mid = role_mid;
+  a.code = codes;
+  a.far_cnt = far_cnt;
+  a.far_src = far_src;
+  if (far_cnt == nullptr || far_src == nullptr)
+    return fail(AG_ERR_VALUE, "far_cnt / far_src (from ag_slab_codes) are required");
+  a.val = val;
+  a.x = x;
+  a.y = y;
+  a.ep = Epi{op, epi_flags, other_touched, deg, x, feat, gin_scale, relu_src};
   a.cost_total = num_edges + kRowCost * num_rows;
+  a.one = 1.0f;
   const bool is_max = op == AG_OP_MAX;
-  const bool v4 = feat % 4 == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0 &&
-                  (reinterpret_cast<uintptr_t>(y) % 16) == 0;
-  if (!v4) return launch_gather<1>(a, is_max, st);
-  const int vec = env_int("AG_GATHER_VEC", 4);
-  if (vec == 8 && feat % 8 == 0 && feat > 128) return launch_gather<8>(a, is_max, st);
-  return launch_gather<4>(a, is_max, st);
+  const bool v2 = feat % 2 == 0 && feat > 32 && (reinterpret_cast<uintptr_t>(x) % 8) == 0 &&
+                  (reinterpret_cast<uintptr_t>(y) % 8) == 0 &&
+                  (relu_src == nullptr || (reinterpret_cast<uintptr_t>(relu_src) % 8) == 0) &&
+                  env_int("AG_SLAB_VEC", 2) == 2;
+  const int mode = is_max ? kModeMax
+                   : (role_mask == 3 && op == AG_OP_SUM &&
+                      (epi_flags & ~(AG_EPI_GIN | AG_EPI_RELU_MASK)) == 0)
+                       ? kModeSum3
+                       : kModeAny;
+  if (v2) return launch_slab<2>(a, mode, window, st);
+  return launch_slab<1>(a, mode, window, st);
 }

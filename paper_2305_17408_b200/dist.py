@@ -170,6 +170,29 @@ class LocalOperator:
     def num_rows(self) -> int:
         return self.plan.n_local
 
+    def window(self) -> int:
+        """Slab-kernel ring radius over the local operator (halo rows sit
+        past the local ones, so they read as far sources)."""
+        w = getattr(self, "_window", None)
+        if w is None:
+            from . import _lib
+            from .formats import SLAB_COVERAGE
+            o = _lib.out_i32()
+            _lib.call("ag_slab_window", self.num_rows, _lib.ptr(self.row_ptr), _lib.ptr(self.col),
+                      SLAB_COVERAGE, _lib.byref(o), _lib.stream())
+            w = int(o.value)
+            object.__setattr__(self, "_window", w)
+        return w
+
+    def codes(self):
+        """self.col as slab-ring codes for window(): (codes, far_cnt, far_src)."""
+        c = getattr(self, "_codes", None)
+        if c is None:
+            from .formats import slab_codes
+            c = slab_codes(self.num_rows, self.row_ptr, self.col, self.window())
+            object.__setattr__(self, "_codes", c)
+        return c
+
     @property
     def num_edges(self) -> int:
         return int(self.col.numel())
@@ -263,9 +286,10 @@ class DistGNN:
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
         _lib.call("ag_fused_spmm", op.num_rows, F, 3 if op.mid is not None else 2,
-                  _lib.ptr(op.row_ptr), _lib.ptr(op.mid), _lib.ptr(op.col), _lib.ptr(op.val),
+                  _lib.ptr(op.row_ptr), _lib.ptr(op.mid), *map(_lib.ptr, op.codes()), _lib.ptr(op.val),
                   op.num_edges, _lib.ptr(x_ext), _lib.ptr(out), _lib.AG_OP["sum"], flags, None,
-                  _lib.ptr(op.deg), 0.0 if gs is None else gs, _lib.ptr(relu_src), _lib.stream())
+                  _lib.ptr(op.deg), 0.0 if gs is None else gs, _lib.ptr(relu_src), x_ext.shape[0], op.window(),
+                  _lib.stream())
         if e0 is not None:
             e1.record()
             self.events.append((e0, e1, F, op))

@@ -16,6 +16,9 @@ import torch
 from . import _lib
 from .graph import Graph, as_device
 
+# fraction of the (largest-ring-coverable) edges the slab kernel's ring must hold
+SLAB_COVERAGE = 0.995
+
 
 class CooMatrix:
     """Coordinate-format adjacency sorted by (row, col)."""
@@ -44,11 +47,24 @@ class CooMatrix:
         return int(self.row.numel())
 
 
+def slab_codes(num_rows: int, row_ptr: torch.Tensor, col: torch.Tensor, window: int):
+    """ag_slab_codes: (codes int32[E], far_cnt int32[nb], far_src int32[nb * cap])."""
+    dev = row_ptr.device
+    nb = (int(num_rows) + 15) // 16
+    cap = int(_lib.load().ag_slab_far_capacity())
+    codes = torch.empty_like(col)
+    far_cnt = torch.empty(max(nb, 1), dtype=torch.int32, device=dev)
+    far_src = torch.empty(max(nb * cap, 1), dtype=torch.int32, device=dev)
+    _lib.call("ag_slab_codes", int(num_rows), _lib.ptr(row_ptr), _lib.ptr(col), int(window),
+              _lib.ptr(codes), _lib.ptr(far_cnt), _lib.ptr(far_src), _lib.stream())
+    return codes, far_cnt, far_src
+
+
 class CsrMatrix:
     """Compressed sparse rows over destination vertices."""
 
     __slots__ = ("num_vertices", "row_ptr", "col_idx", "_val", "_ones", "_rows", "_touched",
-                 "_off_block", "_long")
+                 "_off_block", "_long", "_window", "_codes")
 
     def __init__(self, num_vertices: int, row_ptr: torch.Tensor, col_idx: torch.Tensor,
                  val: torch.Tensor | None, rows: torch.Tensor | None = None):
@@ -58,6 +74,8 @@ class CsrMatrix:
         self._touched = None
         self._off_block: dict[int, int] = {}
         self._long = None
+        self._window = None
+        self._codes = {}
 
     @property
     def val(self) -> torch.Tensor:
@@ -75,6 +93,16 @@ class CsrMatrix:
     @property
     def num_edges(self) -> int:
         return int(self.col_idx.numel())
+
+    def window(self) -> int:
+        """Ring radius (16-row blocks) of the slab aggregation kernel over this
+        topology, picked once from the edge-distance histogram (ag_slab_window)."""
+        if self._window is None:
+            w = _lib.out_i32()
+            _lib.call("ag_slab_window", self.num_vertices, _lib.ptr(self.row_ptr),
+                      _lib.ptr(self.col_idx), SLAB_COVERAGE, _lib.byref(w), _lib.stream())
+            self._window = int(w.value)
+        return self._window
 
     def touched(self) -> torch.Tensor:
         """bool[V]: row has >= 1 edge (kernels.py:121)."""
@@ -119,6 +147,23 @@ class CsrMatrix:
                       _lib.stream())
             lay = (mid, rcol, rval)
             self._long[key] = lay
+        return lay
+
+    def slab_layout(self, block_size: int = 0):
+        """(mid | None, codes, far_cnt, far_src, val | None) for ag_fused_spmm,
+        cached per B: the role-ordered layout (block_size > 0) or the plain CSR
+        (0), columns translated into slab-ring codes for window()."""
+        key = int(block_size)
+        lay = self._codes.get(key)
+        if lay is None:
+            if key > 0:
+                mid, col, val = self.role_layout(key)
+            else:
+                mid, col, val = None, self.col_idx, self._val
+            codes, far_cnt, far_src = slab_codes(self.num_vertices, self.row_ptr, col,
+                                                 self.window())
+            lay = (mid, codes, far_cnt, far_src, val)
+            self._codes[key] = lay
         return lay
 
     def rows(self) -> torch.Tensor:

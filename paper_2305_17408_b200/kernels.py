@@ -3,7 +3,7 @@
 Same operator API as the reference; every kernel is a hand-written sm_100a
 kernel behind the C ABI:
 
-  csr_inter          ag_fused_spmm          L1-swept warp-per-row gather, values
+  csr_inter          ag_fused_spmm          slab kernel (TMA-fed smem X ring), values
                                             bitwise equal to the reference's
                                             np.add.reduceat order
   csr_intra_blocked  ag_csr_intra_spmm      per-community smem-staged slab (the
@@ -95,20 +95,18 @@ def launch_fused(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp
                  block: int = 0, mask: int = 2, flags: int = 0,
                  other_touched: torch.Tensor | None = None, deg: torch.Tensor | None = None,
                  gin_scale: float = 0.0, relu_src: torch.Tensor | None = None) -> None:
-    """ag_fused_spmm: L1-swept row gather, reduceat-order reduction (+ role split).
+    """ag_fused_spmm: slab (smem X ring) row gather, reduceat-order reduction (+ role split).
 
     block > 0 splits every row into its intra run and inter edges (role-ordered
     copy of the CSR, built once); block == 0 treats the row as one role.
     """
-    if block > 0:
-        mid, col, val = a.role_layout(block)
-    else:
-        mid, col, val = None, a.col_idx, a.kernel_val
+    mid, codes, far_cnt, far_src, val = a.slab_layout(block)
     _lib.call("ag_fused_spmm", a.num_vertices, x.shape[1], int(mask), _lib.ptr(a.row_ptr),
-              _lib.ptr(mid), _lib.ptr(col), _lib.ptr(val), a.num_edges, _lib.ptr(x), _lib.ptr(y),
+              _lib.ptr(mid), _lib.ptr(codes), _lib.ptr(far_cnt), _lib.ptr(far_src),
+              _lib.ptr(val), a.num_edges, _lib.ptr(x), _lib.ptr(y),
               _opcode(op), flags | (_lib.AG_EPI_RELU_MASK if relu_src is not None else 0),
               _lib.ptr(other_touched), _lib.ptr(deg), float(gin_scale), _lib.ptr(relu_src),
-              _lib.stream())
+              x.shape[0], a.window(), _lib.stream())
 
 
 def _check_block_local(a: CsrMatrix, block_size: int) -> None:

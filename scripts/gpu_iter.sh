@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 for what in "$@"; do
 case $what in
 tests)
-  timeout 1200 python -m pytest tests -q -m gpu -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log ;;
+  timeout 900 python -m pytest tests -q -m gpu -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log ;;
 smoke)
   timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log ;;
 bench)
@@ -14,7 +14,7 @@ benchnocpu)
 ncu)
   timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch_bench.log 2>&1 ;;
 ncufused)
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gather_kernel -c 1 -o gpurun_out/prof_fused -f python scripts/kbench.py --feat 256 --only fused_pair > gpurun_out/ncu_fused.log 2>&1 ;;
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:slab_kernel -c 1 -o gpurun_out/prof_fused -f python scripts/kbench.py --feat 256 --only fused_pair > gpurun_out/ncu_fused.log 2>&1 ;;
 kbench)
   timeout 900 python scripts/kbench.py > gpurun_out/kbench.log 2>&1 ;;
 esac

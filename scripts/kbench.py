@@ -58,15 +58,14 @@ def main():
         res = {}
         import os
         ref = torch.empty_like(x)
-        os.environ["AG_GATHER_VEC"], os.environ["AG_GATHER_CHUNK"] = "4", "16"
         K.run_fused_pair(dec, x, ref, ag.AggregateOp.SUM)
-        for vec in ("4", "8"):
-            for ch in ("4", "16", "64", "256"):
-                os.environ["AG_GATHER_VEC"], os.environ["AG_GATHER_CHUNK"] = vec, ch
-                res[f"fused_pair_vec{vec}_c{ch}"] = timeit(
-                    lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM))
-                out.setdefault("bitwise_same", []).append(bool(torch.equal(y, ref)))
-        os.environ["AG_GATHER_VEC"], os.environ["AG_GATHER_CHUNK"] = "4", "16"
+        for vec, notma in (("1", "0"), ("2", "0"), ("2", "1")):
+            os.environ["AG_SLAB_VEC"], os.environ["AG_SLAB_NO_TMA"] = vec, notma
+            res[f"fused_pair_vec{vec}_notma{notma}"] = timeit(
+                lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM))
+            out.setdefault("bitwise_same", []).append(bool(torch.equal(y, ref)))
+        os.environ["AG_SLAB_VEC"], os.environ["AG_SLAB_NO_TMA"] = "2", "0"
+        out[f"window_F{F}"] = K.to_csr(full_graph(dec)).window()
         res["fused_pair"] = timeit(lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM))
         res["fused_full_O1"] = timeit(lambda: K.launch_fused(full, x, y, ag.AggregateOp.SUM))
         res["inter_csr_fused_raw"] = timeit(lambda: K.launch_fused(inter.csr, x, y,
