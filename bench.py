@@ -267,6 +267,8 @@ def run_ours(args, cfg):
             "edges_after_gcn_normalize": E_full,
             "intra_edge_fraction": round(dec.intra.num_edges / max(1, E_full), 4),
             "kernels": {f"{k[0]}:{k[1]}": [v[0].value, v[1].value] for k, v in choices.items()},
+            "selector_choice": {f"{k[0]}:{k[1]}": [v[0].value, v[1].value]
+                                for k, v in getattr(timed, "selector_choice", {}).items()},
             "l2": "inputs and activations (>= 0.98 GB per aggregation) exceed the 126 MB L2",
             "preprocess_s": round(prep_s, 2),
             "autotune_s": round(tune_s, 2),
