@@ -196,30 +196,31 @@ int ag_role_csr_build(int64_t num_rows, const int32_t *row_ptr,
  *   role_mask 3: y = combine(I, O) (kernels.py:253-276)   [+ gin term]
  *   role_mask 1/2: a single role with the AG_EPI_* epilogue of ag_csr_spmm.
  * role_mid NULL: the whole row is the single role of role_mask 1 or 2 --
- * aggregate_csr_inter (kernels.py:117-134).  The edges are given as `codes`
- * (ag_slab_codes over the role-ordered -- or plain -- column indices, built
- * with the same `window`), val in the same order.  num_edges =
- * row_ptr[num_rows] (used to balance the row ranges).
- * "Slab" kernel: one CTA per SM sweeps a column tile of an nnz-balanced range
- * of 16-row blocks; a TMA producer warp streams X into a shared-memory ring
- * holding the blocks within `window` blocks of the current one (sources
- * there are read from shared memory, farther ones from global); 15 consumer
- * warps take the range's rows round-robin.  `window` only affects speed,
- * never values (ag_slab_window picks it per graph).  Any F (TMA when F % 4
- * == 0 and x is 16-byte aligned, cp.async otherwise).  x has x_rows >=
- * num_rows rows (a rank's halo rows follow its own rows). */
+ * aggregate_csr_inter (kernels.py:117-134).  The edges are given by the slab
+ * layout of ag_slab_codes over the role-ordered (or plain) CSR, built with
+ * the same `window` and role_mid; `weighted` 0 means every weight is 1.0.
+ * num_edges = row_ptr[num_rows] (balances the row ranges).  x has x_rows >=
+ * num_rows rows (a rank's halo rows follow its own rows).
+ * "Slab" kernel, one CTA per SM sweeping a column tile of an nnz-balanced
+ * range of 16-row blocks: an X producer warp streams X into a shared-memory
+ * ring holding the blocks within `window` blocks of the current one (TMA
+ * tensor tiles), a far producer warp stages each block's out-of-window
+ * sources (bulk copies), and 14 consumer warps take the range's rows
+ * round-robin, reducing out of shared memory.  `window` only affects speed,
+ * never values (ag_slab_window picks it per graph).  Any F (TMA when
+ * F % 4 == 0 and x is 16-byte aligned, cp.async otherwise). */
 int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                   const int32_t *row_ptr, const int32_t *role_mid,
-                  const int32_t *codes, const int32_t *far_cnt,
-                  const int32_t *far_src, const float *val, int64_t num_edges,
-                  const float *x, float *y, int32_t op, int32_t epi_flags,
-                  const uint8_t *other_touched, const int64_t *deg,
-                  float gin_scale, const float *relu_src, int64_t x_rows,
-                  int32_t window, void *stream);
+                  const int32_t *cv, const int32_t *rowinfo,
+                  const int32_t *far_cnt, const int32_t *far_src,
+                  int32_t weighted, int64_t num_edges, const float *x, float *y,
+                  int32_t op, int32_t epi_flags, const uint8_t *other_touched,
+                  const int64_t *deg, float gin_scale, const float *relu_src,
+                  int64_t x_rows, int32_t window, void *stream);
 
 /* Window radius (in 16-row blocks) for ag_fused_spmm over this CSR: the
  * smallest radius whose ring covers `coverage` (e.g. 0.995) of the edges the
- * largest supported radius (19) would cover, from a device histogram of
+ * largest supported radius (16) would cover, from a device histogram of
  * |src/16 - dst/16|.  Synchronous (reads the histogram back); call once per
  * topology and cache the result.  No reference counterpart: a B200 layout
  * parameter of the cached formats (formats.py:76-140). */
@@ -227,17 +228,21 @@ int ag_slab_window(int64_t num_rows, const int32_t *row_ptr,
                    const int32_t *col_idx, double coverage, int32_t *window,
                    void *stream);
 
-/* Edge codes for ag_fused_spmm (same order as col_idx: plain or
- * role-ordered CSR).  codes[e] = X-ring row of col_idx[e] when its 16-row
- * block is within `window` blocks of row r's block; otherwise the source is
- * staged per 16-row block in the far ring (the block's j-th distinct far
- * source, j < ag_slab_far_capacity(): far_src[block * cap + j], far_cnt[block]
- * = number staged) or, past the capacity, codes[e] = ~col_idx[e] (read from
- * global memory).  far_cnt: int32[ceil(num_rows / 16)], far_src: int32[that
- * * ag_slab_far_capacity()]. */
+/* Slab layout for ag_fused_spmm over a CSR (edges in col_idx / val order:
+ * plain or role-ordered; val NULL = unweighted; role_mid NULL = no role
+ * split).  cv: int32[2 * E] (8-byte aligned), pair e = (code, weight bits):
+ * code = X-ring row of col_idx[e] when its 16-row block is within `window`
+ * blocks of row r's block; otherwise the source is one of the block's
+ * staged far sources (far_src[block * cap + j], j < cap =
+ * ag_slab_far_capacity(), far_cnt[block] of them) or, past the capacity,
+ * code = ~col_idx[e] (read from global memory).  rowinfo: int32[4 * V]
+ * (16-byte aligned) = per row {start, intra end, end, flags}.  far_cnt:
+ * int32[ceil(V / 16)], far_src: int32[that * cap]. */
 int ag_slab_codes(int64_t num_rows, const int32_t *row_ptr,
-                  const int32_t *col_idx, int32_t window, int32_t *codes,
-                  int32_t *far_cnt, int32_t *far_src, void *stream);
+                  const int32_t *col_idx, const float *val,
+                  const int32_t *role_mid, int32_t window, int32_t *cv,
+                  int32_t *rowinfo, int32_t *far_cnt, int32_t *far_src,
+                  void *stream);
 /* Staged far sources per 16-row block (the far-ring capacity). */
 int ag_slab_far_capacity(void);
 

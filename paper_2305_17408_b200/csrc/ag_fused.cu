@@ -60,10 +60,13 @@ constexpr int kDepth = 40;
 constexpr int kRB = 16;      // rows per ring block
 constexpr int kCons = 14;    // consumer warps; + 2 producer warps = 16 (4 per SMSP, 128 regs)
 constexpr int kThreads = (kCons + 2) * 32;
-constexpr int kWin = 32;     // topology items per window refill
+constexpr int kWin = 64;     // topology items per window refill (two per lane)
 constexpr int kSlots = 42;   // X ring capacity in blocks (window H <= (kSlots - 9) / 2 = 16)
-constexpr int kFarSlots = 8; // far ring: staged out-of-window sources of the next blocks
-constexpr int kFarMax = 24;  // staged far sources per block (more: read from global)
+constexpr int kFarSlots = 6; // far ring: staged out-of-window sources of the next blocks
+constexpr int kFarMax = 20;  // staged far sources per block (more: read from global)
+constexpr int kReady = 16;   // per-block "ready" barriers (X window + far rows staged)
+constexpr int kDone = 32;    // per-block "done" barriers (every consumer left the block)
+constexpr int kRowSlow = 1;  // rowinfo flag: row has global sources or > kWin pairs
 constexpr int kFarRow0 = kSlots * 16;  // first far-ring row (codes >= kFarRow0)
 constexpr int64_t kRowCost = 4;  // a row's fixed cost in edge units (epilogue, topology)
 
@@ -73,10 +76,12 @@ struct GArgs {
   int mask;                 // 1 intra only, 2 inter only, 3 both (combine)
   const int32_t *row_ptr;   // [rows + 1]
   const int32_t *mid;       // [rows] end of the intra run; nullptr: single role
-  const int32_t *code;      // role-ordered edge codes (ag_slab_codes)
+  const int2 *cv;           // role-ordered (code, weight bits) per edge (ag_slab_codes)
+  const int4 *rowinfo;      // per row {start, intra end, end, flags} (ag_slab_codes)
   const int32_t *far_cnt;   // [nblocks] staged far sources per block (<= kFarMax)
   const int32_t *far_src;   // [nblocks * kFarMax] their source rows
-  const float *val;         // role-ordered weights; nullptr = implicit 1.0
+  int weighted;             // 0: every weight is 1.0 (multiplies skipped: exact)
+  int has_mid;              // rowinfo.y is the intra-run end (role-ordered layout)
   const float *x;
   float *y;
   Epi ep;
@@ -89,6 +94,7 @@ struct GArgs {
   int64_t x_rows;           // rows of x (>= rows: a rank's halo rows follow its own)
   int64_t xblocks;          // ceil(x_rows / 16)
   int tma;                  // 1: TMA tensor loads; 0: cp.async element copies
+  int dbg;                  // development knob (AG_SLAB_DEBUG): 1 = skip the reductions
 };
 
 // ---------------------------------------------------------- packed fp32x2 --
@@ -249,33 +255,43 @@ template <int VEC, bool W>
 struct RowWarp {
   uint32_t win;        // shared address of this warp's window (kWin entries)
   uint32_t ring;       // shared address of the ring + this lane's column byte
-  const int32_t *code; // role-ordered edge codes
-  const float *val;    // nullptr = 1.0
+  const int2 *cv;      // role-ordered (code, weight) pairs in global memory
   const float *xl;     // x + this lane's first column (clamped in-bounds)
   uint32_t feat;
   int lane;
   uint64_t one;        // {1.0f, 1.0f} loaded at run time (see add2)
   int32_t p, end;      // window holds items [p, p + kWin)
-  uint32_t far;        // bit i: window item p + i is a far (global) source
+  uint64_t far;        // bit i: window item p + i is a far (global) source
   __device__ __forceinline__ void fill(int32_t at) {
     __syncwarp();
     p = at;
-    const int32_t e = at + lane;
-    int32_t cd = 0;
-    if (e < end) {
-      cd = __ldg(code + e);
-      const float v = W ? __ldg(val + e) : 1.0f;
-      win_st(win + lane * 8, cd, v);
+    int32_t cd[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int32_t e = at + h * 32 + lane;
+      if (e < end) {
+        const int2 p2 = __ldg(cv + e);
+        cd[h] = p2.x;
+        win_st(win + (h * 32 + lane) * 8, cd[h], __int_as_float(p2.y));
+      }
     }
-    far = __ballot_sync(0xffffffffu, cd < 0);
+    far = __ballot_sync(0xffffffffu, cd[0] < 0) |
+          (static_cast<uint64_t>(__ballot_sync(0xffffffffu, cd[1] < 0)) << 32);
     __syncwarp();
   }
-  // install a prefetched window [at, at + kWin) ∩ [at, end): lane l's (c, v)
-  __device__ __forceinline__ void install(int32_t at, int32_t c, float v) {
+  // install a prefetched window [at, at + kWin) ∩ [at, end): lane l's pairs
+  // at + l and at + 32 + l.  Rows on the fast path have no global sources,
+  // so `far` is only computed for the general path.
+  template <bool FAST>
+  __device__ __forceinline__ void install(int32_t at, int2 q0, int2 q1) {
     __syncwarp();
     p = at;
-    if (at + lane < end) win_st(win + lane * 8, c, v);
-    far = __ballot_sync(0xffffffffu, at + lane < end && c < 0);
+    const bool in0 = at + lane < end, in1 = at + 32 + lane < end;
+    if (in0) win_st(win + lane * 8, q0.x, __int_as_float(q0.y));
+    if (in1) win_st(win + (32 + lane) * 8, q1.x, __int_as_float(q1.y));
+    if (!FAST)
+      far = __ballot_sync(0xffffffffu, in0 && q0.x < 0) |
+            (static_cast<uint64_t>(__ballot_sync(0xffffffffu, in1 && q1.x < 0)) << 32);
     __syncwarp();
   }
   __device__ __forceinline__ void ensure(int32_t lo, int n) {
@@ -364,7 +380,7 @@ struct RowWarp {
   // the all-in-ring path (shared loads only) or the mixed one
   template <int N, bool RAW>
   __device__ __forceinline__ void items(int32_t e, Lv<VEC> (&c)[N]) const {
-    const uint32_t fb = (far >> (e - p)) & ((1u << N) - 1u);
+    const uint32_t fb = static_cast<uint32_t>(far >> (e - p)) & ((1u << N) - 1u);
     if (fb == 0) {
 #pragma unroll
       for (int j = 0; j < N; ++j) c[j] = item<RAW, true>(e + j);
@@ -537,13 +553,21 @@ constexpr int kModeMax = 2;    // any role mask, max
 // One destination row (both roles, epilogue) for this lane's columns.
 template <int VEC, int MODE, bool W>
 __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64_t r, int32_t s,
-                                       int32_t e, int32_t m, int64_t fcol, bool act) {
+                                       int32_t e, int32_t m, float *yrow, bool act, bool fast) {
   constexpr bool IS_MAX = MODE == kModeMax;
   const int64_t ld = a.feat;
   const int32_t ni = (MODE == kModeSum3 || (a.mask & 1)) ? m - s : 0;
   const int32_t no = (MODE == kModeSum3 || (a.mask & 2)) ? e - m : 0;
+  // the ReLU-mask operand is loaded before the reduction so its latency hides
+  // behind it
+  const bool relu = (a.ep.flags & AG_EPI_RELU_MASK) && act;
+  Vf<VEC> h = splat<VEC>(0.0f);
+  if (relu) h = ldv<VEC>(a.ep.relu_src + (yrow - a.y));
   Vf<VEC> I, O;
-  if (e - s <= kWin && w.far == 0) {
+  if (a.dbg == 1) {
+    I = splat<VEC>(0.0f);
+    O = I;
+  } else if (fast) {
     I = lv_out<VEC>(w.template role_fast<IS_MAX>(0, ni));
     O = lv_out<VEC>(w.template role_fast<IS_MAX>(m - s, no));
   } else {
@@ -551,7 +575,7 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
     O = lv_out<VEC>(w.template role<IS_MAX>(m, no));
   }
   if (!act) return;
-  float *yp = a.y + r * ld + fcol;
+  float *yp = yrow;
   Vf<VEC> out;
   if constexpr (MODE == kModeSum3) {
     out = vadd<VEC>(I, O);
@@ -577,8 +601,7 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
     const Vf<VEC> xr = lv_out<VEC>(lv_lds<VEC>(w.ring + rr * (32u * VEC * 4u)));
     out = vadd<VEC>(vscale<VEC>(a.ep.gin_scale, xr), out);
   }
-  if (a.ep.flags & AG_EPI_RELU_MASK) {
-    const Vf<VEC> h = ldv<VEC>(a.ep.relu_src + r * ld + fcol);
+  if (relu) {
 #pragma unroll
     for (int i = 0; i < VEC; ++i) out.v[i] = h.v[i] > 0.0f ? out.v[i] : 0.0f;
   }
@@ -592,7 +615,7 @@ struct SlabGeom {
   static constexpr uint32_t kSlotBytes = kRB * kRowBytes;
   static constexpr uint32_t kFarSlotBytes = kFarMax * kRowBytes;
   static constexpr uint32_t kRingBytes = kSlots * kSlotBytes + kFarSlots * kFarSlotBytes;
-  static constexpr uint32_t kBarBytes = (2 * kSlots + 2 * kFarSlots) * 8;
+  static constexpr uint32_t kBarBytes = (kReady + kDone) * 8;
   static constexpr uint32_t kWinBytes = kCons * kWin * 8;
   static constexpr size_t kSmem = kRingBytes + kBarBytes + kWinBytes;
 };
@@ -607,8 +630,8 @@ __device__ __forceinline__ void l2_prefetch(const void *p, int64_t bytes) {
                : "memory");
 }
 // One lane per block: pull block b's rows of the topology into L2 so the
-// consumers' per-row loads (row_ptr, mid, first 32 codes / weights) hit L2.
-// The block's edge range [e0, e1) was loaded one batch earlier (topo_bounds).
+// consumers' per-row loads (rowinfo, first kWin pairs) hit L2.  The block's
+// pair range [e0, e1) was loaded one batch earlier (topo_bounds).
 struct TopoBounds {
   int32_t e0, e1;
 };
@@ -626,30 +649,9 @@ __device__ __forceinline__ void prefetch_topology(const GArgs &a, uint32_t b, ui
   if (b < kb0 || b >= kb1) return;
   const int64_t r0 = static_cast<int64_t>(b) * kRB;
   const int64_t r1 = std::min<int64_t>(r0 + kRB, a.rows);
-  const int64_t e0 = tb.e0, e1 = tb.e1;
-  l2_prefetch(a.row_ptr + r0, (r1 - r0 + 1) * 4);
-  if (a.mid) l2_prefetch(a.mid + r0, (r1 - r0) * 4);
-  l2_prefetch(a.code + e0, (e1 - e0) * 4);
-  if (a.val) l2_prefetch(a.val + e0, (e1 - e0) * 4);
+  l2_prefetch(a.rowinfo + r0, (r1 - r0) * 16);
+  l2_prefetch(a.cv + tb.e0, static_cast<int64_t>(tb.e1 - tb.e0) * 8);
 }
-
-// Cursor over a ring of NS slots: slot = b % NS (absolute, so the edge codes
-// do not depend on the range) and the parity of the fill, ((b - b0) / NS) & 1
-// with b0 the first block the range puts in the ring.  Advanced one block at
-// a time -- no divisions on the hot path.
-template <int NS>
-struct RingPos {
-  uint32_t slot, off, phase;
-  __device__ __forceinline__ void init(uint32_t b, uint32_t b0) {
-    slot = b % NS;
-    off = (b - b0) % NS;
-    phase = ((b - b0) / NS) & 1u;
-  }
-  __device__ __forceinline__ void next() {
-    if (++slot == NS) slot = 0;
-    if (++off == NS) { off = 0; phase ^= 1u; }
-  }
-};
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
                                          uint32_t bar) {
@@ -659,40 +661,71 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
+// tx expectation without an arrival (more X blocks feed the same block)
+__device__ __forceinline__ void mbar_expect_tx_only(uint32_t b, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(bytes)
+               : "memory");
+}
+
+// Per-block synchronisation, relative to the range's first block kb0:
+//   ready[(k - kb0) % kReady]  completes when consumer block k can run: every
+//       X block of its window is in the X ring and its far rows are staged
+//       (2 arrivals -- X producer, far producer -- plus the copies' bytes);
+//   done[(k - kb0) % kDone]    completes when all consumers left block k.
+// Phases are ((k - kb0) / n) & 1.  done completes in block order (each warp
+// leaves blocks in order), so waiting on done[j] covers every block <= j.
+struct BlockSync {
+  uint32_t ready, done, kb0;
+  __device__ __forceinline__ uint32_t rdy(uint32_t k) const {
+    return ready + ((k - kb0) % kReady) * 8;
+  }
+  __device__ __forceinline__ uint32_t rdy_phase(uint32_t k) const {
+    return ((k - kb0) / kReady) & 1u;
+  }
+  __device__ __forceinline__ void wait_done(uint32_t k) const {
+    mbar_wait_sleep(done + ((k - kb0) % kDone) * 8, ((k - kb0) / kDone) & 1u);
+  }
+};
 
 // X producer warp: streams X blocks [Llo, Lhi) of column tile `tile` into
-// the X ring, one TMA tensor tile per block (cp.async element copies when x
-// is not TMA-addressable), refilling a slot once every consumer released it.
-// It also pulls the consumers' topology into L2 ahead of them.
+// the X ring slot b % kSlots, one TMA tensor tile per block (cp.async element
+// copies when x is not TMA-addressable).  Block t is first needed by
+// consumer block kt = max(kb0, t - H) and completes on ready[kt].  Before
+// overwriting a slot it waits until no consumer block still needs the old
+// block (done[t - kSlots + H]).  It also pulls the topology into L2 ahead.
 template <int VEC>
 __device__ __forceinline__ void produce_x(const GArgs &a, const CUtensorMap *map, uint32_t ring,
-                                          uint32_t full, uint32_t empty, uint32_t Llo,
-                                          uint32_t Lhi, uint32_t kb0, uint32_t kb1, int tile,
+                                          const BlockSync &bs, uint32_t Llo, uint32_t Lhi,
+                                          uint32_t kb0, uint32_t kb1, uint32_t H, int tile,
                                           int lane) {
   using G = SlabGeom<VEC>;
   const int64_t c0 = static_cast<int64_t>(tile) * G::T;
-  RingPos<kSlots> pos;
-  pos.init(Llo, Llo);
-  // topology bounds are loaded one 32-block batch ahead of their use
+  uint32_t slot = Llo % kSlots;
   TopoBounds tb = topo_bounds(a, Llo + lane, kb1);
   TopoBounds tb_next = topo_bounds(a, Llo + 32 + lane, kb1);
-  for (uint32_t t = Llo; t < Lhi; ++t, pos.next()) {
+  for (uint32_t t = Llo; t < Lhi; ++t) {
     const uint32_t i = t - Llo;
     if (i % 32 == 0) {
       prefetch_topology(a, t + lane, kb0, kb1, tb);
       tb = tb_next;
       tb_next = topo_bounds(a, t + 64 + lane, kb1);
     }
-    const bool refill = i >= kSlots;  // fill n >= 1 waits for the release of fill n - 1
+    const uint32_t kt = t > kb0 + H ? t - H : kb0;
+    // the slot's previous block, and the ready barrier's previous block
+    int64_t need = -1;
+    if (t >= Llo + kSlots) need = int64_t(t) - kSlots + H;
+    if (kt >= kb0 + kReady) need = std::max<int64_t>(need, int64_t(kt) - kReady);
+    const bool last = t == kt + H || t + 1 == Lhi;  // last X block feeding ready[kt]
+    const uint32_t dst = ring + slot * G::kSlotBytes;
     if (a.tma) {
       if (lane == 0) {
-        if (refill) mbar_wait_sleep(empty + pos.slot * 8, pos.phase ^ 1u);
-        mbar_expect_tx(full + pos.slot * 8, G::kSlotBytes);
-        tma_load_2d(ring + pos.slot * G::kSlotBytes, map, full + pos.slot * 8,
-                    static_cast<int>(c0), static_cast<int>(t * kRB));
+        if (need >= 0) bs.wait_done(static_cast<uint32_t>(need));
+        if (last) mbar_expect_tx(bs.rdy(kt), G::kSlotBytes);
+        else mbar_expect_tx_only(bs.rdy(kt), G::kSlotBytes);
+        tma_load_2d(dst, map, bs.rdy(kt), static_cast<int>(c0), static_cast<int>(t * kRB));
       }
     } else {
-      if (refill) mbar_wait_sleep(empty + pos.slot * 8, pos.phase ^ 1u);
+      if (need >= 0) bs.wait_done(static_cast<uint32_t>(need));
 #pragma unroll 4
       for (int rr = 0; rr < kRB; ++rr) {
         const int64_t row = static_cast<int64_t>(t) * kRB + rr;  // past x_rows: zero
@@ -700,76 +733,96 @@ __device__ __forceinline__ void produce_x(const GArgs &a, const CUtensorMap *map
         for (int j = 0; j < VEC; ++j) {
           const int64_t c = c0 + lane * VEC + j;
           const bool ok = row < a.x_rows && c < a.feat;
-          const float *src = ok ? a.x + row * a.feat + c : a.x;
-          cp_async4(ring + pos.slot * G::kSlotBytes + (rr * G::T + lane * VEC + j) * 4, src,
+          cp_async4(dst + (rr * G::T + lane * VEC + j) * 4, ok ? a.x + row * a.feat + c : a.x,
                     ok ? 4 : 0);
         }
       }
-      cp_async_mbar_arrive(full + pos.slot * 8);
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncwarp();
+      if (lane == 0 && last) mbar_arrive(bs.rdy(kt));
     }
     __syncwarp();
+    if (++slot == kSlots) slot = 0;
   }
+  // consumer blocks whose window ends past the last X block: arrive plainly
+  const uint32_t k0 = std::max(kb0 + 1, Lhi > H ? Lhi - H : 0u);
+  for (uint32_t k = k0; k < kb1; ++k) {
+    if (lane == 0) {
+      if (k >= kb0 + kReady) bs.wait_done(k - kReady);
+      mbar_arrive(bs.rdy(k));
+    }
+  }
+  __syncwarp();
 }
 
 // Far producer warp: for every consumer block f in [kb0, kb1), copies the
-// tile columns of its staged far sources (far_src, one bulk copy per source
-// row, lanes in parallel) into far-ring slot f % kFarSlots as soon as the
-// consumers released that slot's previous block -- kFarSlots blocks ahead.
+// tile columns of its staged far sources (far_src; one bulk copy per source,
+// lanes in parallel; cp.async elements when x is not bulk-copyable) into
+// far-ring slot f % kFarSlots once every consumer left block f - kFarSlots,
+// completing on ready[f].  Look-ahead loads are consumed in place (the loop
+// is unrolled by D): rotating them through moves would wait on each load.
 template <int VEC>
-__device__ __forceinline__ void produce_far(const GArgs &a, uint32_t ring, uint32_t ffull,
-                                            uint32_t fempty, uint32_t kb0, uint32_t kb1,
-                                            int tile, int lane) {
+__device__ __forceinline__ void produce_far(const GArgs &a, uint32_t ring, const BlockSync &bs,
+                                            uint32_t kb0, uint32_t kb1, int tile, int lane) {
   using G = SlabGeom<VEC>;
+  constexpr int D = 4;
   const uint32_t far_ring = ring + kSlots * G::kSlotBytes;
   const int64_t c0 = static_cast<int64_t>(tile) * G::T;
   const uint32_t tile_bytes =
       static_cast<uint32_t>(std::min<int64_t>(G::T, a.feat - c0)) * 4u;  // partial last tile
-  RingPos<kFarSlots> fpos;
-  fpos.init(kb0, kb0);
-  // far source lists are loaded three blocks ahead, counts one batch ahead
   auto far_list = [&](uint32_t f) -> int32_t {
     return (f < kb1 && lane < kFarMax) ? a.far_src[static_cast<int64_t>(f) * kFarMax + lane] : 0;
   };
   auto far_counts = [&](uint32_t f) -> int32_t { return f + lane < kb1 ? a.far_cnt[f + lane] : 0; };
-  int32_t fs0 = far_list(kb0), fs1 = far_list(kb0 + 1), fs2 = far_list(kb0 + 2);
+  int32_t fsa[D];
+#pragma unroll
+  for (int u = 0; u < D; ++u) fsa[u] = far_list(kb0 + u);
   int32_t fc = far_counts(kb0), fc_next = far_counts(kb0 + 32);
-  for (uint32_t f = kb0; f < kb1; ++f, fpos.next()) {
-    const uint32_t fi = f - kb0;
-    const int cnt = __shfl_sync(0xffffffffu, fc, fi & 31);
-    const int32_t src = fs0;
-    fs0 = fs1;
-    fs1 = fs2;
-    fs2 = far_list(f + 3);
-    if ((fi & 31) == 31) {
-      fc = fc_next;
-      fc_next = far_counts(f + 33);
-    }
-    const uint32_t slot_base = far_ring + fpos.slot * G::kFarSlotBytes;
-    const bool refill = fi >= kFarSlots;
-    if (a.tma) {
-      if (lane == 0) {
-        if (refill) mbar_wait_sleep(fempty + fpos.slot * 8, fpos.phase ^ 1u);
-        mbar_expect_tx(ffull + fpos.slot * 8, static_cast<uint32_t>(cnt) * tile_bytes);
+  uint32_t fslot = kb0 % kFarSlots;
+  for (uint32_t fb = kb0; fb < kb1; fb += D) {
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+      const uint32_t f = fb + u;
+      if (f >= kb1) break;
+      const uint32_t fi = f - kb0;
+      const int cnt = __shfl_sync(0xffffffffu, fc, fi & 31);
+      const int32_t src = fsa[u];
+      fsa[u] = far_list(f + D);
+      if ((fi & 31) == 31) {
+        fc = fc_next;
+        fc_next = far_counts(f + 33);
+      }
+      const uint32_t slot_base = far_ring + fslot * G::kFarSlotBytes;
+      if (++fslot == kFarSlots) fslot = 0;
+      if (a.tma) {
+        if (lane == 0) {
+          if (fi >= kFarSlots) bs.wait_done(f - kFarSlots);
+          mbar_expect_tx(bs.rdy(f), static_cast<uint32_t>(cnt) * tile_bytes);
+        }
+        __syncwarp();
+        if (lane < cnt)
+          bulk_g2s(slot_base + lane * G::kRowBytes, a.x + static_cast<int64_t>(src) * a.feat + c0,
+                   tile_bytes, bs.rdy(f));
+      } else {
+        if (fi >= kFarSlots) bs.wait_done(f - kFarSlots);
+        for (int j = 0; j < cnt; ++j) {
+          const int32_t sj = __shfl_sync(0xffffffffu, src, j);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            const int64_t c = c0 + lane * VEC + v;
+            const bool ok = c < a.feat;
+            cp_async4(slot_base + j * G::kRowBytes + (lane * VEC + v) * 4,
+                      ok ? a.x + static_cast<int64_t>(sj) * a.feat + c : a.x, ok ? 4 : 0);
+          }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bs.rdy(f));
       }
       __syncwarp();
-      if (lane < cnt)
-        bulk_g2s(slot_base + lane * G::kRowBytes, a.x + static_cast<int64_t>(src) * a.feat + c0,
-                 tile_bytes, ffull + fpos.slot * 8);
-    } else {
-      if (refill) mbar_wait_sleep(fempty + fpos.slot * 8, fpos.phase ^ 1u);
-      for (int j = 0; j < cnt; ++j) {
-        const int32_t sj = __shfl_sync(0xffffffffu, src, j);
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          const int64_t c = c0 + lane * VEC + v;
-          const bool ok = c < a.feat;
-          cp_async4(slot_base + j * G::kRowBytes + (lane * VEC + v) * 4,
-                    ok ? a.x + static_cast<int64_t>(sj) * a.feat + c : a.x, ok ? 4 : 0);
-        }
-      }
-      cp_async_mbar_arrive(ffull + fpos.slot * 8);
     }
-    __syncwarp();
   }
 }
 
@@ -780,11 +833,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ int64_t s_kb[2];
   const uint32_t ring = su32(smem);
-  const uint32_t full = ring + G::kRingBytes;
-  const uint32_t empty = full + kSlots * 8;
-  const uint32_t ffull = empty + kSlots * 8;
-  const uint32_t fempty = ffull + kFarSlots * 8;
-  const uint32_t wins = fempty + kFarSlots * 8;
+  const uint32_t ready = ring + G::kRingBytes;
+  const uint32_t done = ready + kReady * 8;
+  const uint32_t wins = done + kDone * 8;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t H = static_cast<uint32_t>(a.H);
@@ -798,34 +849,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
       s_kb[0] = range_block(a, range);
       s_kb[1] = range_block(a, range + 1);
-      const uint32_t n = a.tma ? 1u : 32u;
-      for (int s = 0; s < kSlots; ++s) {
-        mbar_init(full + s * 8, n);
-        mbar_init(empty + s * 8, kCons);
-      }
-      for (int s = 0; s < kFarSlots; ++s) {
-        mbar_init(ffull + s * 8, n);
-        mbar_init(fempty + s * 8, kCons);
-      }
+      for (int s = 0; s < kReady; ++s) mbar_init(ready + s * 8, 2);
+      for (int s = 0; s < kDone; ++s) mbar_init(done + s * 8, kCons);
       fence_mbar_init();
     }
     __syncthreads();
     const uint32_t kb0 = static_cast<uint32_t>(s_kb[0]), kb1 = static_cast<uint32_t>(s_kb[1]);
     const uint32_t Llo = kb0 > H ? kb0 - H : 0u;
     const uint32_t Lhi = static_cast<uint32_t>(std::min<int64_t>(a.xblocks, int64_t(kb1) + H));
+    const BlockSync bs{ready, done, kb0};
     if (kb0 < kb1) {
       if (warp == kCons) {
-        produce_x<VEC>(a, &tmap, ring, full, empty, Llo, Lhi, kb0, kb1, tile, lane);
+        produce_x<VEC>(a, &tmap, ring, bs, Llo, Lhi, kb0, kb1, H, tile, lane);
       } else if (warp == kCons + 1) {
-        produce_far<VEC>(a, ring, ffull, fempty, kb0, kb1, tile, lane);
+        produce_far<VEC>(a, ring, bs, kb0, kb1, tile, lane);
       } else {
         RowWarp<VEC, W> w;
         const int64_t fcol = static_cast<int64_t>(tile) * G::T + lane * VEC;
         const bool act = fcol < a.feat;
         w.win = wins + warp * kWin * 8;
         w.ring = ring + lane * VEC * 4;
-        w.code = a.code;
-        w.val = a.val;
+        w.cv = a.cv;
         w.xl = a.x + (act ? fcol : 0);
         w.feat = static_cast<uint32_t>(a.feat);
         w.lane = lane;
@@ -833,88 +877,64 @@ __global__ void __launch_bounds__(kThreads, 1)
         w.p = 0;
         w.end = 0;
         w.far = 0;
-        // two-stage topology pipeline: row bounds two rows ahead, the first
-        // 32 codes / weights one row ahead
-        int32_t bs = 0, be = 0, bm = 0;          // stage 1 (row + 2 kCons)
-        int32_t ns = 0, ne = 0, nm = 0, nc = 0;  // stage 2 (row + kCons)
-        float nv = 1.0f;
-        auto bounds = [&](uint32_t rr) {
-          if (rr < a.rows) {
-            bs = a.row_ptr[rr];
-            be = a.row_ptr[rr + 1];
-            bm = (MODE == kModeSum3 || a.mid) ? a.mid[rr] : (a.mask == 1 ? be : bs);
-          }
-        };
-        auto codes = [&]() {
-          ns = bs;
-          ne = be;
-          nm = bm;
-          const int32_t ed = ns + lane;
-          nc = ed < ne ? __ldg(a.code + ed) : 0;
-          nv = (W && ed < ne) ? __ldg(a.val + ed) : 1.0f;
-        };
+        float *const ylane = a.y + (act ? fcol : 0);
+        const uint32_t ld = static_cast<uint32_t>(a.feat);
         const uint32_t r0 = kb0 * kRB;
         const uint32_t r1 = static_cast<uint32_t>(std::min<int64_t>(int64_t(kb1) * kRB, a.rows));
-        // X ring: blocks [Llo, waited_end) have been waited on
-        uint32_t waited_end = Llo;
-        RingPos<kSlots> wpos;
-        wpos.init(Llo, Llo);
-        RingPos<kSlots> rpos;  // next X block to release
-        rpos.init(Llo, Llo);
-        RingPos<kFarSlots> fpos;  // far slot of the current block
-        fpos.init(kb0, kb0);
-        auto enter = [&](uint32_t k) {
-          const uint32_t need_end = std::min(k + H + 1, Lhi);
-          for (; waited_end < need_end; ++waited_end, wpos.next())
-            mbar_wait(full + wpos.slot * 8, wpos.phase);
-          mbar_wait(ffull + fpos.slot * 8, fpos.phase);
+        // Topology pipeline in registers: rowinfo two rows ahead, the first
+        // kWin (code, weight) pairs one row ahead.  Both are issued before
+        // the current row's reduction and only moved after it, so each load
+        // has a full row of work to land.
+        const int4 zero4 = make_int4(0, 0, 0, 0);
+        auto info_at = [&](uint32_t rr) -> int4 { return rr < r1 ? __ldg(a.rowinfo + rr) : zero4; };
+        auto pairs_at = [&](const int4 &inf, int h) -> int2 {
+          const int32_t ed = inf.x + h * 32 + lane;
+          return ed < inf.z ? __ldg(a.cv + ed) : make_int2(0, 0);
         };
-        auto leave = [&](uint32_t k) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(fempty + fpos.slot * 8);
-          fpos.next();
-          if (k >= Llo + H) {  // block k - H leaves the window of every later block
-            if (lane == 0) mbar_arrive(empty + rpos.slot * 8);
-            rpos.next();
-          }
-        };
+        uint32_t rr = r0 + warp;
+        int4 info = info_at(rr);
+        int2 q0 = pairs_at(info, 0), q1 = pairs_at(info, 1);
+        int4 info1 = info_at(rr + kCons);
         uint32_t kcur = kb0;
-        enter(kb0);
-        bounds(r0 + warp);
-        codes();
-        bounds(r0 + warp + kCons);
+        mbar_wait(bs.rdy(kb0), 0);
 #pragma unroll 1
-        for (uint32_t r = r0 + warp; r < r1; r += kCons) {
-          const uint32_t k = r / kRB;
-          while (kcur != k) {
-            leave(kcur);
+        for (; rr < r1; rr += kCons) {
+          const uint32_t k = rr / kRB;
+          while (kcur != k) {  // leave block kcur, enter the next
+            __syncwarp();
+            if (lane == 0) mbar_arrive(done + ((kcur - kb0) % kDone) * 8);
             ++kcur;
-            enter(kcur);
+            mbar_wait(bs.rdy(kcur), bs.rdy_phase(kcur));
           }
-          const int32_t s = ns, e = ne, m = nm;
+          const int32_t s = info.x, e = info.z;
+          const int32_t m = (MODE == kModeSum3 || a.has_mid) ? info.y : (a.mask == 1 ? e : s);
+          const bool fast = !(info.w & kRowSlow);
           w.end = e;
-          w.install(s, nc, nv);
-          codes();
-          bounds(r + 2 * kCons);
-          do_row<VEC, MODE, W>(a, w, r, s, e, m, fcol, act);
+          if (fast) w.template install<true>(s, q0, q1);
+          else w.template install<false>(s, q0, q1);
+          // next row's pairs and the row after next's bounds
+          const int2 n0 = pairs_at(info1, 0), n1 = pairs_at(info1, 1);
+          const int4 info2 = info_at(rr + 2 * kCons);
+          float *yrow;  // ylane + rr * ld as one IMAD.WIDE.U32
+          asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(yrow) : "r"(rr), "r"(ld * 4u), "l"(ylane));
+          do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast);
+          info = info1;
+          info1 = info2;
+          q0 = n0;
+          q1 = n1;
         }
         while (true) {
-          leave(kcur);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(done + ((kcur - kb0) % kDone) * 8);
           if (++kcur >= kb1) break;
-          enter(kcur);
+          mbar_wait(bs.rdy(kcur), bs.rdy_phase(kcur));
         }
       }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      for (int s = 0; s < kSlots; ++s) {
-        mbar_inval(full + s * 8);
-        mbar_inval(empty + s * 8);
-      }
-      for (int s = 0; s < kFarSlots; ++s) {
-        mbar_inval(ffull + s * 8);
-        mbar_inval(fempty + s * 8);
-      }
+      for (int s = 0; s < kReady; ++s) mbar_inval(ready + s * 8);
+      for (int s = 0; s < kDone; ++s) mbar_inval(done + s * 8);
     }
     __syncthreads();
   }
@@ -954,12 +974,14 @@ constexpr int kMaxWindow = (kSlots - 9) / 2;
 template <int VEC>
 int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
   using G = SlabGeom<VEC>;
+  const bool wt = a.weighted != 0;
   auto k = mode == kModeMax
-               ? (a.val ? slab_kernel<VEC, kModeMax, true> : slab_kernel<VEC, kModeMax, false>)
+               ? (wt ? slab_kernel<VEC, kModeMax, true> : slab_kernel<VEC, kModeMax, false>)
            : mode == kModeSum3
-               ? (a.val ? slab_kernel<VEC, kModeSum3, true> : slab_kernel<VEC, kModeSum3, false>)
-               : (a.val ? slab_kernel<VEC, kModeAny, true> : slab_kernel<VEC, kModeAny, false>);
+               ? (wt ? slab_kernel<VEC, kModeSum3, true> : slab_kernel<VEC, kModeSum3, false>)
+               : (wt ? slab_kernel<VEC, kModeAny, true> : slab_kernel<VEC, kModeAny, false>);
   a.H = window;
+  a.dbg = env_int("AG_SLAB_DEBUG", 0);
   a.nblocks = (a.rows + kRB - 1) / kRB;
   a.xblocks = (a.x_rows + kRB - 1) / kRB;
   a.ntiles = static_cast<int>((a.feat + G::T - 1) / G::T);
@@ -1019,16 +1041,19 @@ __global__ void role_csr_kernel(int64_t rows, const int32_t *row_ptr, const int3
   }
 }
 
-// Edge codes of the slab kernel, one thread per 16-row block (edges in the
-// given order).  A source within `window` blocks of the destination's block
-// is an X-ring row, slot-major ((src / 16) % kSlots) * 16 + src % 16.  A
-// farther one is staged in the far ring: the block's j-th distinct far
-// source (j < kFarMax) is row kFarRow0 + (block % kFarSlots) * kFarMax + j
-// and far_src[block * kFarMax + j] = src.  Beyond kFarMax distinct far
-// sources the code is ~src (read from global memory).
+// Slab layout, one thread per 16-row block (edges in the given order).  Each
+// edge becomes a (code, weight bits) pair: a source within `window` blocks
+// of the destination's block is an X-ring row, slot-major
+// ((src / 16) % kSlots) * 16 + src % 16; a farther one is staged in the far
+// ring -- the block's j-th distinct far source (j < kFarMax) is row
+// kFarRow0 + (block % kFarSlots) * kFarMax + j, far_src[block * kFarMax + j]
+// = src -- and past kFarMax distinct far sources the code is ~src (global
+// memory).  rowinfo[r] = {start, intra-run end (mid[r], or start when there
+// is no role split), end, flags}; kRowSlow marks rows the fast path cannot
+// take (global sources or more than kWin pairs).
 __global__ void slab_code_kernel(int64_t rows, const int32_t *row_ptr, const int32_t *col,
-                                 int32_t window, int32_t *code, int32_t *far_cnt,
-                                 int32_t *far_src) {
+                                 const float *val, const int32_t *mid, int32_t window, int2 *cv,
+                                 int4 *rowinfo, int32_t *far_cnt, int32_t *far_src) {
   const int64_t nb = (rows + kRB - 1) / kRB;
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb;
        b += (int64_t)gridDim.x * blockDim.x) {
@@ -1036,19 +1061,29 @@ __global__ void slab_code_kernel(int64_t rows, const int32_t *row_ptr, const int
     int j = 0;
     const int64_t r1 = std::min<int64_t>(b * kRB + kRB, rows);
     for (int64_t r = b * kRB; r < r1; ++r) {
-      for (int32_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
-        const int32_t c = col[e];
+      const int32_t s = row_ptr[r], e = row_ptr[r + 1];
+      int flags = e - s > kWin ? kRowSlow : 0;
+      for (int32_t ed = s; ed < e; ++ed) {
+        const int32_t c = col[ed];
         const int64_t sb = c / kRB;
         const int64_t d = sb - b;
+        int32_t code;
         if (d >= -window && d <= window) {
-          code[e] = static_cast<int32_t>((sb % kSlots) * kRB + c % kRB);
-          continue;
+          code = static_cast<int32_t>((sb % kSlots) * kRB + c % kRB);
+        } else {
+          int k = 0;
+          while (k < j && staged[k] != c) ++k;
+          if (k == j && j < kFarMax) staged[j++] = c;
+          if (k < j) {
+            code = static_cast<int32_t>(kFarRow0 + (b % kFarSlots) * kFarMax + k);
+          } else {
+            code = ~c;
+            flags |= kRowSlow;
+          }
         }
-        int k = 0;
-        while (k < j && staged[k] != c) ++k;
-        if (k == j && j < kFarMax) staged[j++] = c;
-        code[e] = k < j ? static_cast<int32_t>(kFarRow0 + (b % kFarSlots) * kFarMax + k) : ~c;
+        cv[ed] = make_int2(code, __float_as_int(val ? val[ed] : 1.0f));
       }
+      rowinfo[r] = make_int4(s, mid ? mid[r] : s, e, flags);
     }
     far_cnt[b] = j;
     for (int k = 0; k < j; ++k) far_src[b * kFarMax + k] = staged[k];
@@ -1063,7 +1098,8 @@ using namespace ag;
 extern "C" int ag_slab_far_capacity(void) { return kFarMax; }
 
 extern "C" int ag_slab_codes(int64_t num_rows, const int32_t *row_ptr, const int32_t *col_idx,
-                             int32_t window, int32_t *codes, int32_t *far_cnt, int32_t *far_src,
+                             const float *val, const int32_t *role_mid, int32_t window,
+                             int32_t *cv, int32_t *rowinfo, int32_t *far_cnt, int32_t *far_src,
                              void *stream) {
   if (num_rows < 0) return fail(AG_ERR_VALUE, "negative sizes");
   if (window < 0 || window > kMaxWindow)
@@ -1072,7 +1108,8 @@ extern "C" int ag_slab_codes(int64_t num_rows, const int32_t *row_ptr, const int
   if (num_rows == 0) return AG_OK;
   const int64_t nb = (num_rows + kRB - 1) / kRB;
   slab_code_kernel<<<grid_for(nb, 128), 128, 0, as_stream(stream)>>>(
-      num_rows, row_ptr, col_idx, window, codes, far_cnt, far_src);
+      num_rows, row_ptr, col_idx, val, role_mid, window, reinterpret_cast<int2 *>(cv),
+      reinterpret_cast<int4 *>(rowinfo), far_cnt, far_src);
   AG_LAUNCH_CHECK("slab_code_kernel");
   return AG_OK;
 }
@@ -1125,8 +1162,9 @@ extern "C" int ag_slab_window(int64_t num_rows, const int32_t *row_ptr, const in
 
 extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                              const int32_t *row_ptr, const int32_t *role_mid,
-                             const int32_t *codes, const int32_t *far_cnt,
-                             const int32_t *far_src, const float *val, int64_t num_edges,
+                             const int32_t *cv, const int32_t *rowinfo,
+                             const int32_t *far_cnt, const int32_t *far_src, int32_t weighted,
+                             int64_t num_edges,
                              const float *x, float *y, int32_t op, int32_t epi_flags,
                              const uint8_t *other_touched, const int64_t *deg, float gin_scale,
                              const float *relu_src, int64_t x_rows, int32_t window,
@@ -1154,12 +1192,16 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
   a.mask = role_mask;
   a.row_ptr = row_ptr;
   a.mid = role_mid;
-  a.code = codes;
+  a.cv = reinterpret_cast<const int2 *>(cv);
+  a.rowinfo = reinterpret_cast<const int4 *>(rowinfo);
   a.far_cnt = far_cnt;
   a.far_src = far_src;
-  if (far_cnt == nullptr || far_src == nullptr)
-    return fail(AG_ERR_VALUE, "far_cnt / far_src (from ag_slab_codes) are required");
-  a.val = val;
+  if (!cv || !rowinfo || !far_cnt || !far_src)
+    return fail(AG_ERR_VALUE, "cv / rowinfo / far_cnt / far_src (ag_slab_codes) are required");
+  if ((reinterpret_cast<uintptr_t>(cv) & 7) || (reinterpret_cast<uintptr_t>(rowinfo) & 15))
+    return fail(AG_ERR_VALUE, "cv must be 8-byte and rowinfo 16-byte aligned");
+  a.weighted = weighted != 0;
+  a.has_mid = role_mid != nullptr;
   a.x = x;
   a.y = y;
   a.ep = Epi{op, epi_flags, other_touched, deg, x, feat, gin_scale, relu_src};

@@ -38,7 +38,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t b, uint32_t parity) {
         : "r"(b), "r"(parity)
         : "memory");
     if (done) return;
-    if (++spins > (1u << 26)) __trap();
+    if (++spins > (1u << 22)) __trap();
   }
 }
 // Same, for a warp that has nothing else to do (the ring producer): each
@@ -55,7 +55,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t b, uint32_t parity) {
         : "r"(b), "r"(parity), "r"(1000u)
         : "memory");
     if (done) return;
-    if (++spins > (1u << 26)) __trap();
+    if (++spins > (1u << 22)) __trap();
   }
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t b) {
@@ -85,6 +85,20 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void *src, uint32_
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
                "r"(src_bytes)
                : "memory");
+}
+// 8-byte cp.async (both addresses 8-byte aligned); src_bytes = 0 zero-fills.
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+// wait until at most N of this thread's most recent cp.async groups are pending
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 // Arrive on `bar` once every prior cp.async of this thread has landed (the
 // arrival counts toward the barrier's expected count: .noinc).

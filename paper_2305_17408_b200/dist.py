@@ -185,11 +185,12 @@ class LocalOperator:
         return w
 
     def codes(self):
-        """self.col as slab-ring codes for window(): (codes, far_cnt, far_src)."""
+        """The slab layout of this operator for window(): (cv, rowinfo, far_cnt, far_src)."""
         c = getattr(self, "_codes", None)
         if c is None:
             from .formats import slab_codes
-            c = slab_codes(self.num_rows, self.row_ptr, self.col, self.window())
+            c = slab_codes(self.num_rows, self.row_ptr, self.col, self.val, self.mid,
+                           self.window())
             object.__setattr__(self, "_codes", c)
         return c
 
@@ -286,7 +287,8 @@ class DistGNN:
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
         _lib.call("ag_fused_spmm", op.num_rows, F, 3 if op.mid is not None else 2,
-                  _lib.ptr(op.row_ptr), _lib.ptr(op.mid), *map(_lib.ptr, op.codes()), _lib.ptr(op.val),
+                  _lib.ptr(op.row_ptr), _lib.ptr(op.mid), *map(_lib.ptr, op.codes()),
+                  int(op.val is not None),
                   op.num_edges, _lib.ptr(x_ext), _lib.ptr(out), _lib.AG_OP["sum"], flags, None,
                   _lib.ptr(op.deg), 0.0 if gs is None else gs, _lib.ptr(relu_src), x_ext.shape[0], op.window(),
                   _lib.stream())

@@ -47,17 +47,21 @@ class CooMatrix:
         return int(self.row.numel())
 
 
-def slab_codes(num_rows: int, row_ptr: torch.Tensor, col: torch.Tensor, window: int):
-    """ag_slab_codes: (codes int32[E], far_cnt int32[nb], far_src int32[nb * cap])."""
+def slab_codes(num_rows: int, row_ptr: torch.Tensor, col: torch.Tensor, val, mid, window: int):
+    """ag_slab_codes: (cv int32[2E], rowinfo int32[4V], far_cnt int32[nb],
+    far_src int32[nb * cap])."""
     dev = row_ptr.device
-    nb = (int(num_rows) + 15) // 16
+    V = int(num_rows)
+    nb = (V + 15) // 16
     cap = int(_lib.load().ag_slab_far_capacity())
-    codes = torch.empty_like(col)
+    cv = torch.empty(max(2 * col.numel(), 2), dtype=torch.int32, device=dev)
+    rowinfo = torch.empty(max(4 * V, 4), dtype=torch.int32, device=dev)
     far_cnt = torch.empty(max(nb, 1), dtype=torch.int32, device=dev)
     far_src = torch.empty(max(nb * cap, 1), dtype=torch.int32, device=dev)
-    _lib.call("ag_slab_codes", int(num_rows), _lib.ptr(row_ptr), _lib.ptr(col), int(window),
-              _lib.ptr(codes), _lib.ptr(far_cnt), _lib.ptr(far_src), _lib.stream())
-    return codes, far_cnt, far_src
+    _lib.call("ag_slab_codes", V, _lib.ptr(row_ptr), _lib.ptr(col), _lib.ptr(val), _lib.ptr(mid),
+              int(window), _lib.ptr(cv), _lib.ptr(rowinfo), _lib.ptr(far_cnt), _lib.ptr(far_src),
+              _lib.stream())
+    return cv, rowinfo, far_cnt, far_src
 
 
 class CsrMatrix:
@@ -150,9 +154,9 @@ class CsrMatrix:
         return lay
 
     def slab_layout(self, block_size: int = 0):
-        """(mid | None, codes, far_cnt, far_src, val | None) for ag_fused_spmm,
+        """(mid | None, cv, rowinfo, far_cnt, far_src, weighted) for ag_fused_spmm,
         cached per B: the role-ordered layout (block_size > 0) or the plain CSR
-        (0), columns translated into slab-ring codes for window()."""
+        (0), edges as slab-ring (code, weight) pairs for window()."""
         key = int(block_size)
         lay = self._codes.get(key)
         if lay is None:
@@ -160,9 +164,9 @@ class CsrMatrix:
                 mid, col, val = self.role_layout(key)
             else:
                 mid, col, val = None, self.col_idx, self._val
-            codes, far_cnt, far_src = slab_codes(self.num_vertices, self.row_ptr, col,
-                                                 self.window())
-            lay = (mid, codes, far_cnt, far_src, val)
+            cv, rowinfo, far_cnt, far_src = slab_codes(self.num_vertices, self.row_ptr, col, val,
+                                                       mid, self.window())
+            lay = (mid, cv, rowinfo, far_cnt, far_src, int(val is not None))
             self._codes[key] = lay
         return lay
 

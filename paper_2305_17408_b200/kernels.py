@@ -100,10 +100,10 @@ def launch_fused(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp
     block > 0 splits every row into its intra run and inter edges (role-ordered
     copy of the CSR, built once); block == 0 treats the row as one role.
     """
-    mid, codes, far_cnt, far_src, val = a.slab_layout(block)
+    mid, cv, rowinfo, far_cnt, far_src, weighted = a.slab_layout(block)
     _lib.call("ag_fused_spmm", a.num_vertices, x.shape[1], int(mask), _lib.ptr(a.row_ptr),
-              _lib.ptr(mid), _lib.ptr(codes), _lib.ptr(far_cnt), _lib.ptr(far_src),
-              _lib.ptr(val), a.num_edges, _lib.ptr(x), _lib.ptr(y),
+              _lib.ptr(mid), _lib.ptr(cv), _lib.ptr(rowinfo), _lib.ptr(far_cnt),
+              _lib.ptr(far_src), weighted, a.num_edges, _lib.ptr(x), _lib.ptr(y),
               _opcode(op), flags | (_lib.AG_EPI_RELU_MASK if relu_src is not None else 0),
               _lib.ptr(other_touched), _lib.ptr(deg), float(gin_scale), _lib.ptr(relu_src),
               x.shape[0], a.window(), _lib.stream())

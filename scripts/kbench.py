@@ -65,6 +65,9 @@ def main():
                 lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM))
             out.setdefault("bitwise_same", []).append(bool(torch.equal(y, ref)))
         os.environ["AG_SLAB_VEC"], os.environ["AG_SLAB_NO_TMA"] = "2", "0"
+        os.environ["AG_SLAB_DEBUG"] = "1"
+        res["fused_pair_noreduce"] = timeit(lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM))
+        os.environ["AG_SLAB_DEBUG"] = "0"
         out[f"window_F{F}"] = K.to_csr(full_graph(dec)).window()
         res["fused_pair"] = timeit(lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM))
         res["fused_full_O1"] = timeit(lambda: K.launch_fused(full, x, y, ag.AggregateOp.SUM))
