@@ -227,6 +227,16 @@ def run_ours(args, cfg):
     lab_host = labels.cpu().pin_memory()
     mask_host = mask.cpu().pin_memory()
     torch.cuda.synchronize()
+    # host->device bandwidth of the feature matrix alone (diagnostic for e2e)
+    xd = torch.empty(x_host.shape, dtype=x_host.dtype, device="cuda")
+    xd.copy_(x_host, non_blocking=True)
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record()
+    xd.copy_(x_host, non_blocking=True)
+    h1.record()
+    torch.cuda.synchronize()
+    h2d_gbs = x_host.numel() * 4 / (h0.elapsed_time(h1) / 1e3) / 1e9
+    del xd
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_steps = max(1, min(args.steps, 5))
     if world > 1:
@@ -277,7 +287,8 @@ def run_ours(args, cfg):
             **({"halo": halo} if halo else {}),
         },
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms/epoch", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": 4, "loss": loss_val},
+                "d2h_bytes_per_step": 4, "loss": loss_val,
+                "h2d_x_GBps": round(h2d_gbs, 1)},
         "roofline": {
             "bound": "hbm",
             "achieved": round(achieved, 1),
@@ -285,7 +296,7 @@ def run_ours(args, cfg):
             "unit": "GB/s",
             "frac": round(achieved / peak, 4),
             "traffic": None,
-            "kernel": "aggregation (inter csr_spmm + intra csr_intra_spmm w/ fused combine)",
+            "kernel": "slab_kernel (ag_fused_spmm: both roles + fused combine, bitwise reduceat order)",
             "aggregations_per_step": n_agg // args.steps,
             "agg_ms_per_step": round(agg_ms / args.steps, 4),
             "algorithmic_bytes_per_step": agg_bytes // args.steps,

@@ -52,6 +52,7 @@ struct TcArgs {
   float alpha, beta;
   int relu;
   int m_tiles, n_tiles, splits;
+  int raw_hi;  // 1: leave x in place as the hi operand (the MMA reads its tf32 bits)
   int64_t k_per_split;  // multiple of BK
 };
 
@@ -168,7 +169,11 @@ struct Cfg {
   static constexpr int SMEM = STAGES * STAGE + 1024 /* align */ + 256 /* barriers */;
 };
 
-// split x (fp32) into hi (in place) and lo, n4 float4s
+// split x (fp32) into hi (in place) and lo, n4 float4s.  RAW: only lo is
+// written and x stays as the hi operand -- valid because kind::tf32 reads
+// just the top 19 bits of each fp32 operand (verified bitwise against the
+// masked split by tests/test_gemm_gpu.py).
+template <bool RAW>
 __device__ __forceinline__ void split_tile(float4 *hi, float4 *lo, int n4, int t, int nt) {
   for (int i = t; i < n4; i += nt) {
     float4 v = hi[i], h, l;
@@ -180,7 +185,7 @@ __device__ __forceinline__ void split_tile(float4 *hi, float4 *lo, int n4, int t
     l.y = __fsub_rn(v.y, h.y);
     l.z = __fsub_rn(v.z, h.z);
     l.w = __fsub_rn(v.w, h.w);
-    hi[i] = h;
+    if (!RAW) hi[i] = h;
     lo[i] = l;
   }
 }
@@ -338,11 +343,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[stage], phase);
         unsigned char *st = smem + stage * C::STAGE;
-        split_tile(reinterpret_cast<float4 *>(st), reinterpret_cast<float4 *>(st + C::A_BYTES),
-                   C::A_BYTES / 16, t_id, 128);
-        split_tile(reinterpret_cast<float4 *>(st + 2 * C::A_BYTES),
-                   reinterpret_cast<float4 *>(st + 2 * C::A_BYTES + C::B_BYTES),
-                   C::B_BYTES / 16, t_id, 128);
+        if (g.raw_hi) {
+          split_tile<true>(reinterpret_cast<float4 *>(st),
+                           reinterpret_cast<float4 *>(st + C::A_BYTES), C::A_BYTES / 16, t_id, 128);
+          split_tile<true>(reinterpret_cast<float4 *>(st + 2 * C::A_BYTES),
+                           reinterpret_cast<float4 *>(st + 2 * C::A_BYTES + C::B_BYTES),
+                           C::B_BYTES / 16, t_id, 128);
+        } else {
+          split_tile<false>(reinterpret_cast<float4 *>(st),
+                            reinterpret_cast<float4 *>(st + C::A_BYTES), C::A_BYTES / 16, t_id, 128);
+          split_tile<false>(reinterpret_cast<float4 *>(st + 2 * C::A_BYTES),
+                            reinterpret_cast<float4 *>(st + 2 * C::A_BYTES + C::B_BYTES),
+                            C::B_BYTES / 16, t_id, 128);
+        }
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv[stage]);
@@ -521,6 +534,10 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   TcArgs g{};
   g.M = M; g.N = N; g.K = K;
   g.alpha = alpha; g.beta = beta; g.relu = (epilogue & AG_GEMM_RELU) ? 1 : 0;
+  {
+    const char *rh = std::getenv("AG_TC_RAWHI");
+    g.raw_hi = rh ? std::atoi(rh) : 0;
+  }
   g.m_tiles = static_cast<int>((M + BM - 1) / BM);
   g.n_tiles = static_cast<int>((N + bn - 1) / bn);
   const int64_t tiles = static_cast<int64_t>(g.m_tiles) * g.n_tiles;

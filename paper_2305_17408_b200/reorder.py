@@ -102,7 +102,7 @@ def apply_reorder(g: Graph, p: Partition) -> Graph:
         raise ValueError(
             f"partition covers {p.num_vertices} vertices, graph has {g.num_vertices}")
     dev = _lib.device()
-    perm = torch.from_numpy(np.ascontiguousarray(p.permutation, dtype=np.int64)).to(dev)
+    perm = torch.from_numpy(np.array(p.permutation, dtype=np.int64, copy=True)).to(dev)
     E = g.num_edges
     d64 = torch.empty(E, dtype=torch.int64, device=dev)
     s64 = torch.empty(E, dtype=torch.int64, device=dev)

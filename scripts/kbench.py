@@ -50,6 +50,11 @@ def main():
     for F in args.feat:
         x = torch.randn((V, F), device="cuda")
         y = torch.empty_like(x)
+        if args.only == "gemm":
+            w = torch.randn((F, 256), device="cuda")
+            K.gemm(x, w)
+            torch.cuda.synchronize()
+            continue
         if args.only == "fused_pair":
             K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM)
             torch.cuda.synchronize()
@@ -92,6 +97,13 @@ def main():
             res[f"gemm_dW_bn{bn}"] = timeit(lambda: K.gemm(x, g256, trans_a=True))
             res[f"gemm_dH_bn{bn}"] = timeit(lambda: K.gemm(g256, w, trans_b=True))
         os.environ.pop("AG_TC_BN")
+        ref_g = K.gemm(x, w)
+        os.environ["AG_TC_RAWHI"] = "1"
+        res["gemm_Fx256_rawhi"] = timeit(lambda: K.gemm(x, w))
+        res["gemm_dW_rawhi"] = timeit(lambda: K.gemm(x, g256, trans_a=True))
+        res["gemm_dH_rawhi"] = timeit(lambda: K.gemm(g256, w, trans_b=True))
+        out.setdefault("rawhi_bitwise", []).append(bool(torch.equal(K.gemm(x, w), ref_g)))
+        os.environ.pop("AG_TC_RAWHI")
         res["gemm_Fx256_simt"] = timeit(lambda: K.gemm(x, w, engine="simt"))
         gbs = {k: round(ba / (v / 1e3) / 1e9, 1) for k, v in res.items() if "gemm" not in k}
         out[f"F{F}"] = {"ms": {k: round(v, 4) for k, v in res.items()}, "alg_GBps": gbs,
