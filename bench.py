@@ -116,6 +116,16 @@ def build_workload(cfg, rank=0, world=1):
     return g, rg, dec, net, prep_s
 
 
+def ncu_traffic():
+    """DRAM bytes of one F=256 aggregation launch from the committed ncu
+    capture (profiles/r01_ncu_slab_gemm.json), or (None, reason)."""
+    p = ROOT / "profiles" / "r01_ncu_slab_gemm.json"
+    if not p.exists():
+        return None, "no ncu capture committed"
+    d = json.loads(p.read_text())
+    return int(d["traffic_bytes_per_launch_f256"]), f"{p.name}: {d['source']}"
+
+
 def bytes_alg(V, E_full, F, weighted):
     """4(V+1) + 4E' + 4wE' + 8VF per full-graph aggregation."""
     return 4 * (V + 1) + 4 * E_full + (4 * E_full if weighted else 0) + 8 * V * F
@@ -206,6 +216,11 @@ def run_ours(args, cfg):
     launches = _lib.launch_count() - launches0
     ms = start.elapsed_time(end) / args.steps
     agg_ms = sum(e0.elapsed_time(e1) for e0, e1, _, _ in timed.events)
+    per_width = {}
+    for e0, e1, f, _ in timed.events:
+        pw = per_width.setdefault(int(f), [0, 0.0])
+        pw[0] += 1
+        pw[1] += e0.elapsed_time(e1)
     E_full = rg.num_edges
     weighted = rg.weights is not None
     # algorithmic bytes of the aggregations THIS rank ran (its rows' share)
@@ -255,6 +270,12 @@ def run_ours(args, cfg):
     h2d = x_host.numel() * 4 + lab_host.numel() * 4 + mask_host.numel()
 
     peak, peak_src = peaks()
+    frac_local = 1.0 if world == 1 else halo["rows_per_rank"] / V
+    widths = {str(f): {"launches_per_step": n // args.steps, "ms_per_launch": round(t / n, 4),
+                       "alg_GBps": round(bytes_alg(V, E_full, f, weighted) * frac_local
+                                         / (t / n / 1e3) / 1e9, 1)}
+              for f, (n, t) in sorted(per_width.items())}
+    traffic, traffic_src = ncu_traffic()
     achieved = agg_bytes / (agg_ms / 1000.0) / 1e9 if agg_ms > 0 else 0.0
     line = {
         "metric": METRIC,
@@ -295,7 +316,10 @@ def run_ours(args, cfg):
             "peak": peak,
             "unit": "GB/s",
             "frac": round(achieved / peak, 4),
-            "traffic": None,
+            "traffic": traffic,
+            "traffic_per": "one F=256 aggregation launch (dram read + write bytes)",
+            "traffic_source": traffic_src,
+            "per_width": widths,
             "kernel": "slab_kernel (ag_fused_spmm: both roles + fused combine, bitwise reduceat order)",
             "aggregations_per_step": n_agg // args.steps,
             "agg_ms_per_step": round(agg_ms / args.steps, 4),
