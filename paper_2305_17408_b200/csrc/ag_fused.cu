@@ -64,6 +64,7 @@ constexpr int kWin = 64;     // topology items per window refill (two per lane)
 constexpr int kSlots = 42;   // X ring capacity in blocks (window H <= (kSlots - 9) / 2 = 16)
 constexpr int kFarSlots = 6; // far ring: staged out-of-window sources of the next blocks
 constexpr int kFarMax = 20;  // staged far sources per block (more: read from global)
+constexpr int kReluSlots = 4;  // ReLU-mask operand tiles staged ahead (backward epilogue)
 constexpr int kReady = 16;   // per-block "ready" barriers (X window + far rows staged)
 constexpr int kDone = 32;    // per-block "done" barriers (every consumer left the block)
 constexpr int kRowSlow = 1;  // rowinfo flag: row has global sources or > kWin pairs
@@ -82,6 +83,7 @@ struct GArgs {
   const int32_t *far_src;   // [nblocks * kFarMax] their source rows
   int weighted;             // 0: every weight is 1.0 (multiplies skipped: exact)
   int has_mid;              // rowinfo.y is the intra-run end (role-ordered layout)
+  int relu;                 // AG_EPI_RELU_MASK: relu_src tiles are staged by the far producer
   const float *x;
   float *y;
   Epi ep;
@@ -553,16 +555,15 @@ constexpr int kModeMax = 2;    // any role mask, max
 // One destination row (both roles, epilogue) for this lane's columns.
 template <int VEC, int MODE, bool W>
 __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64_t r, int32_t s,
-                                       int32_t e, int32_t m, float *yrow, bool act, bool fast) {
+                                       int32_t e, int32_t m, float *yrow, bool act, bool fast,
+                                       uint32_t relu_s) {
   constexpr bool IS_MAX = MODE == kModeMax;
   const int64_t ld = a.feat;
   const int32_t ni = (MODE == kModeSum3 || (a.mask & 1)) ? m - s : 0;
   const int32_t no = (MODE == kModeSum3 || (a.mask & 2)) ? e - m : 0;
   // the ReLU-mask operand is loaded before the reduction so its latency hides
   // behind it
-  const bool relu = (a.ep.flags & AG_EPI_RELU_MASK) && act;
-  Vf<VEC> h = splat<VEC>(0.0f);
-  if (relu) h = ldv<VEC>(a.ep.relu_src + (yrow - a.y));
+  const bool relu = a.relu && act;
   Vf<VEC> I, O;
   if (a.dbg == 1) {
     I = splat<VEC>(0.0f);
@@ -602,6 +603,7 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
     out = vadd<VEC>(vscale<VEC>(a.ep.gin_scale, xr), out);
   }
   if (relu) {
+    const Vf<VEC> h = lv_out<VEC>(lv_lds<VEC>(relu_s));  // staged by the far producer
 #pragma unroll
     for (int i = 0; i < VEC; ++i) out.v[i] = h.v[i] > 0.0f ? out.v[i] : 0.0f;
   }
@@ -614,7 +616,8 @@ struct SlabGeom {
   static constexpr uint32_t kRowBytes = T * 4;
   static constexpr uint32_t kSlotBytes = kRB * kRowBytes;
   static constexpr uint32_t kFarSlotBytes = kFarMax * kRowBytes;
-  static constexpr uint32_t kRingBytes = kSlots * kSlotBytes + kFarSlots * kFarSlotBytes;
+  static constexpr uint32_t kReluOff = kSlots * kSlotBytes + kFarSlots * kFarSlotBytes;
+  static constexpr uint32_t kRingBytes = kReluOff + kReluSlots * kSlotBytes;
   static constexpr uint32_t kBarBytes = (kReady + kDone) * 8;
   static constexpr uint32_t kWinBytes = kCons * kWin * 8;
   static constexpr size_t kSmem = kRingBytes + kBarBytes + kWinBytes;
@@ -763,8 +766,9 @@ __device__ __forceinline__ void produce_x(const GArgs &a, const CUtensorMap *map
 // completing on ready[f].  Look-ahead loads are consumed in place (the loop
 // is unrolled by D): rotating them through moves would wait on each load.
 template <int VEC>
-__device__ __forceinline__ void produce_far(const GArgs &a, uint32_t ring, const BlockSync &bs,
-                                            uint32_t kb0, uint32_t kb1, int tile, int lane) {
+__device__ __forceinline__ void produce_far(const GArgs &a, const CUtensorMap *relu_map,
+                                            uint32_t ring, const BlockSync &bs, uint32_t kb0,
+                                            uint32_t kb1, int tile, int lane) {
   using G = SlabGeom<VEC>;
   constexpr int D = 4;
   const uint32_t far_ring = ring + kSlots * G::kSlotBytes;
@@ -795,17 +799,36 @@ __device__ __forceinline__ void produce_far(const GArgs &a, uint32_t ring, const
       }
       const uint32_t slot_base = far_ring + fslot * G::kFarSlotBytes;
       if (++fslot == kFarSlots) fslot = 0;
+      // far slot reuse: done[f - kFarSlots]; ReLU tile slot reuse: done[f - kReluSlots]
+      const int64_t need = a.relu ? int64_t(f) - kReluSlots : int64_t(f) - kFarSlots;
+      const uint32_t relu_dst = ring + G::kReluOff + (fi % kReluSlots) * G::kSlotBytes;
       if (a.tma) {
         if (lane == 0) {
-          if (fi >= kFarSlots) bs.wait_done(f - kFarSlots);
-          mbar_expect_tx(bs.rdy(f), static_cast<uint32_t>(cnt) * tile_bytes);
+          if (need >= int64_t(kb0)) bs.wait_done(static_cast<uint32_t>(need));
+          mbar_expect_tx(bs.rdy(f), static_cast<uint32_t>(cnt) * tile_bytes +
+                                        (a.relu ? G::kSlotBytes : 0u));
+          if (a.relu)
+            tma_load_2d(relu_dst, relu_map, bs.rdy(f), static_cast<int>(c0),
+                        static_cast<int>(f * kRB));
         }
         __syncwarp();
         if (lane < cnt)
           bulk_g2s(slot_base + lane * G::kRowBytes, a.x + static_cast<int64_t>(src) * a.feat + c0,
                    tile_bytes, bs.rdy(f));
       } else {
-        if (fi >= kFarSlots) bs.wait_done(f - kFarSlots);
+        if (need >= int64_t(kb0)) bs.wait_done(static_cast<uint32_t>(need));
+        if (a.relu) {
+          for (int rr = 0; rr < kRB; ++rr) {
+            const int64_t row = static_cast<int64_t>(f) * kRB + rr;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              const int64_t c = c0 + lane * VEC + v;
+              const bool ok = row < a.rows && c < a.feat;
+              cp_async4(relu_dst + (rr * G::T + lane * VEC + v) * 4,
+                        ok ? a.ep.relu_src + row * a.feat + c : a.ep.relu_src, ok ? 4 : 0);
+            }
+          }
+        }
         for (int j = 0; j < cnt; ++j) {
           const int32_t sj = __shfl_sync(0xffffffffu, src, j);
 #pragma unroll
@@ -828,7 +851,8 @@ __device__ __forceinline__ void produce_far(const GArgs &a, uint32_t ring, const
 
 template <int VEC, int MODE, bool W>
 __global__ void __launch_bounds__(kThreads, 1)
-    slab_kernel(const __grid_constant__ CUtensorMap tmap, GArgs a) {
+    slab_kernel(const __grid_constant__ CUtensorMap tmap,
+                const __grid_constant__ CUtensorMap relu_map, GArgs a) {
   using G = SlabGeom<VEC>;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ int64_t s_kb[2];
@@ -862,7 +886,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (warp == kCons) {
         produce_x<VEC>(a, &tmap, ring, bs, Llo, Lhi, kb0, kb1, H, tile, lane);
       } else if (warp == kCons + 1) {
-        produce_far<VEC>(a, ring, bs, kb0, kb1, tile, lane);
+        produce_far<VEC>(a, &relu_map, ring, bs, kb0, kb1, tile, lane);
       } else {
         RowWarp<VEC, W> w;
         const int64_t fcol = static_cast<int64_t>(tile) * G::T + lane * VEC;
@@ -917,7 +941,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int4 info2 = info_at(rr + 2 * kCons);
           float *yrow;  // ylane + rr * ld as one IMAD.WIDE.U32
           asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(yrow) : "r"(rr), "r"(ld * 4u), "l"(ylane));
-          do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast);
+          const uint32_t relu_s = ring + G::kReluOff + ((k - kb0) % kReluSlots) * G::kSlotBytes +
+                                  (rr % kRB) * G::kRowBytes + lane * VEC * 4;
+          do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, relu_s);
           info = info1;
           info1 = info2;
           q0 = n0;
@@ -996,25 +1022,28 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
   const int64_t units = ranges * a.ntiles;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, sms)));
 
-  CUtensorMap map;
+  CUtensorMap map, relu_map;
   std::memset(&map, 0, sizeof(map));
+  std::memset(&relu_map, 0, sizeof(relu_map));
   a.tma = 0;
-  const bool tma_ok = a.feat % 4 == 0 && (reinterpret_cast<uintptr_t>(a.x) % 16) == 0 &&
-                      env_int("AG_SLAB_NO_TMA", 0) == 0;
-  if (tma_ok) {
+  a.relu = (a.ep.flags & AG_EPI_RELU_MASK) ? 1 : 0;
+  // 2-D fp32 tensor map over [rows, feat] with row stride feat, box 16 x T
+  auto encode = [&](CUtensorMap *m, const float *base, int64_t rows) -> bool {
     TmaEncodeFn enc = tma_encode_fn();
-    if (enc) {
-      cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.feat), static_cast<cuuint64_t>(a.x_rows)};
-      cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.feat) * 4};
-      cuuint32_t box[2] = {static_cast<cuuint32_t>(G::T), static_cast<cuuint32_t>(kRB)};
-      cuuint32_t es[2] = {1, 1};
-      CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(a.x), dims,
-                       strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r == CUDA_SUCCESS) a.tma = 1;
-    }
-  }
-  k<<<grid, kThreads, smem, st>>>(map, a);
+    if (!enc || reinterpret_cast<uintptr_t>(base) % 16 != 0) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.feat), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.feat) * 4};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(G::T), static_cast<cuuint32_t>(kRB)};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides,
+               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  if (a.feat % 4 == 0 && env_int("AG_SLAB_NO_TMA", 0) == 0 && encode(&map, a.x, a.x_rows) &&
+      (!a.relu || encode(&relu_map, a.ep.relu_src, a.rows)))
+    a.tma = 1;
+  k<<<grid, kThreads, smem, st>>>(map, relu_map, a);
   AG_LAUNCH_CHECK("slab_kernel");
   return AG_OK;
 }

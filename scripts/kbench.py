@@ -75,6 +75,14 @@ def main():
         os.environ["AG_SLAB_DEBUG"] = "0"
         out[f"window_F{F}"] = K.to_csr(full_graph(dec)).window()
         res["fused_pair"] = timeit(lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM))
+        dect = net.subject_t
+        hrelu = torch.randn_like(x)
+        res["bwd_pair"] = timeit(lambda: K.run_fused_pair(dect, x, y, ag.AggregateOp.SUM))
+        res["bwd_pair_relu"] = timeit(lambda: K.run_fused_pair(dect, x, y, ag.AggregateOp.SUM,
+                                                               relu_src=hrelu))
+        res["fwd_pair_relu"] = timeit(lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM,
+                                                               relu_src=hrelu))
+        out[f"bwd_window_F{F}"] = K.to_csr(full_graph(dect)).window()
         res["fused_full_O1"] = timeit(lambda: K.launch_fused(full, x, y, ag.AggregateOp.SUM))
         res["inter_csr_fused_raw"] = timeit(lambda: K.launch_fused(inter.csr, x, y,
                                                                    ag.AggregateOp.SUM))
