@@ -60,6 +60,10 @@ extern "C" {
  * into the transposed aggregation (relu_src = that layer's output, same
  * shape and row stride as y). */
 #define AG_EPI_RELU_MASK 8
+/* AG_EPI_RELU (ag_fused_spmm only): y = max(y, 0) after everything else --
+ * the hidden layers' activation when the update GEMM runs before the
+ * aggregation (A (H W) for a narrowing layer). */
+#define AG_EPI_RELU 16
 
 int ag_abi_version(void);
 const char *ag_last_error(void);
@@ -257,10 +261,14 @@ int ag_combine(int64_t num_rows, int64_t feat, const float *a,
 /* C = alpha * op(A) @ op(B) + beta * C, fp32 row-major, optional ReLU on
  * the result (epilogue 1).  op(A) is [M,K], op(B) is [K,N]. */
 #define AG_GEMM_RELU 1
+/* mask (may be NULL): after the epilogue, C[m][n] = mask[m * ldm + n] > 0 ?
+ * C[m][n] : 0 -- the ReLU backward of the layer below, fused into dH = G W^T
+ * (mask = that layer's output, never aliasing C). */
 int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                 int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
                 float *C, int64_t ldc, float alpha, float beta,
-                int32_t epilogue, void *stream);
+                int32_t epilogue, const float *mask, int64_t ldm,
+                void *stream);
 
 /* The same GEMM on the tensor cores: tcgen05.mma kind::tf32 with TMA-fed,
  * 128-byte-swizzled shared-memory operands, TMEM accumulators and 3xTF32
@@ -272,7 +280,8 @@ int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
 int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                    int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
                    float *C, int64_t ldc, float alpha, float beta,
-                   int32_t epilogue, void *stream);
+                   int32_t epilogue, const float *mask, int64_t ldm,
+                   void *stream);
 
 /* ===================== training helpers (composed) ======================= */
 

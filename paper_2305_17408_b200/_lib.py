@@ -21,7 +21,7 @@ LIB_PATH = PKG / "libadaptgear_b200.so"
 
 AG_OK, AG_ERR_VALUE, AG_ERR_KERNEL, AG_ERR_CUDA = 0, 1, 2, 3
 AG_OP = {"sum": 0, "mean": 1, "max": 2}
-AG_EPI_COMBINE, AG_EPI_GIN, AG_EPI_EMPTY_OTHER, AG_EPI_RELU_MASK = 1, 2, 4, 8
+AG_EPI_COMBINE, AG_EPI_GIN, AG_EPI_EMPTY_OTHER, AG_EPI_RELU_MASK, AG_EPI_RELU = 1, 2, 4, 8, 16
 AG_GEMM_RELU = 1
 
 P = ctypes.c_void_p
@@ -59,8 +59,9 @@ SIGNATURES: dict[str, list] = {
     "ag_slab_codes": [I64, P, P, P, P, I32, P, P, P, P, P],
     "ag_slab_far_capacity": [],
     "ag_combine": [I64, I64, P, P, P, P, P, I32, P, P],
-    "ag_gemm_f32": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, F32, F32, I32, P],
-    "ag_gemm_tf32x3": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, F32, F32, I32, P],
+    "ag_gemm_f32": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, F32, F32, I32, P, I64, P],
+    "ag_gemm_tf32x3": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, F32, F32, I32, P, I64,
+                       P],
     "ag_softmax_xent": [I64, I64, I64, P, P, P, I64, P, P, P],
     "ag_relu_backward": [I64, P, P, P],
     "ag_sgd_step": [I64, P, P, F32, P],

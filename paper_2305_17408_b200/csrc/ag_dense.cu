@@ -31,6 +31,8 @@ struct GemmArgs {
   float alpha, beta;
   int epi;
   int64_t k_per_split;
+  const float *mask;  // ReLU-backward mask operand (NULL: none): out = mask > 0 ? out : 0
+  int64_t ldm;
 };
 
 // A(m, k) of op(A) and B(k, n) of op(B)
@@ -125,6 +127,7 @@ __global__ void __launch_bounds__(NT, 2) sgemm_kernel(GemmArgs g, int partial) {
         float v = g.alpha * acc[i][j];
         if (g.beta != 0.0f) v = fmaf(g.beta, g.C[m * g.ldc + n], v);
         if (g.epi & AG_GEMM_RELU) v = fmaxf(v, 0.0f);
+        if (g.mask && !(g.mask[m * g.ldm + n] > 0.0f)) v = 0.0f;
         g.C[m * g.ldc + n] = v;
       }
     }
@@ -132,7 +135,8 @@ __global__ void __launch_bounds__(NT, 2) sgemm_kernel(GemmArgs g, int partial) {
 }
 
 __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const float *part, float *C,
-                                     int64_t ldc, float alpha, float beta, int epi) {
+                                     int64_t ldc, float alpha, float beta, int epi,
+                                     const float *mask, int64_t ldm) {
   const int64_t n = M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -142,6 +146,7 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const flo
     float v = alpha * s;
     if (beta != 0.0f) v = fmaf(beta, C[m * ldc + c], v);
     if (epi & AG_GEMM_RELU) v = fmaxf(v, 0.0f);
+    if (mask && !(mask[m * ldm + c] > 0.0f)) v = 0.0f;
     C[m * ldc + c] = v;
   }
 }
@@ -222,7 +227,7 @@ using namespace ag;
 extern "C" int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                            int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
                            float *C, int64_t ldc, float alpha, float beta, int32_t epilogue,
-                           void *stream) {
+                           const float *mask, int64_t ldm, void *stream) {
   if (M < 0 || N < 0 || K < 0) return fail(AG_ERR_VALUE, "negative GEMM sizes");
   if (M == 0 || N == 0) return AG_OK;
   cudaStream_t st = as_stream(stream);
@@ -239,7 +244,8 @@ extern "C" int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int6
   kps = (kps + BK - 1) / BK * BK;
   splits = static_cast<int>((K + kps - 1) / kps);
   if (splits < 1) splits = 1;
-  GemmArgs g{M, N, K, A, lda, trans_a, B, ldb, trans_b, C, ldc, alpha, beta, epilogue, kps};
+  GemmArgs g{M, N, K, A, lda, trans_a, B, ldb, trans_b, C, ldc, alpha, beta, epilogue, kps,
+             mask, ldm};
   dim3 grid(static_cast<unsigned>(tiles_n), static_cast<unsigned>(tiles_m), splits);
   if (splits == 1) {
     sgemm_kernel<<<grid, NT, 0, st>>>(g, 0);
@@ -252,7 +258,8 @@ extern "C" int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int6
   sgemm_kernel<<<grid, NT, 0, st>>>(g, 1);
   AG_LAUNCH_CHECK("sgemm_kernel(split)");
   splitk_reduce_kernel<<<grid_for(M * N, 256), 256, 0, st>>>(M, N, splits, part.as<float>(), C,
-                                                            ldc, alpha, beta, epilogue);
+                                                            ldc, alpha, beta, epilogue, mask,
+                                                            ldm);
   AG_LAUNCH_CHECK("splitk_reduce_kernel");
   return AG_OK;
 }

@@ -602,6 +602,10 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
     const Vf<VEC> xr = lv_out<VEC>(lv_lds<VEC>(w.ring + rr * (32u * VEC * 4u)));
     out = vadd<VEC>(vscale<VEC>(a.ep.gin_scale, xr), out);
   }
+  if (a.ep.flags & AG_EPI_RELU) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) out.v[i] = fmaxf(out.v[i], 0.0f);
+  }
   if (relu) {
     const Vf<VEC> h = lv_out<VEC>(lv_lds<VEC>(relu_s));  // staged by the far producer
 #pragma unroll
@@ -1243,7 +1247,7 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                   env_int("AG_SLAB_VEC", 2) == 2;
   const int mode = is_max ? kModeMax
                    : (role_mask == 3 && op == AG_OP_SUM &&
-                      (epi_flags & ~(AG_EPI_GIN | AG_EPI_RELU_MASK)) == 0)
+                      (epi_flags & ~(AG_EPI_GIN | AG_EPI_RELU_MASK | AG_EPI_RELU)) == 0)
                        ? kModeSum3
                        : kModeAny;
   if (v2) return launch_slab<2>(a, mode, window, st);

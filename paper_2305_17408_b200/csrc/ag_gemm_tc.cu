@@ -53,6 +53,8 @@ struct TcArgs {
   int relu;
   int m_tiles, n_tiles, splits;
   int raw_hi;  // 1: leave x in place as the hi operand (the MMA reads its tf32 bits)
+  const float *mask;  // ReLU-backward mask operand (NULL: none): out = mask > 0 ? out : 0
+  int64_t ldm;
   int64_t k_per_split;  // multiple of BK
 };
 
@@ -154,7 +156,7 @@ __host__ __device__ constexpr uint32_t instr_desc(bool a_mn, bool b_mn, int n) {
          (static_cast<uint32_t>(BM >> 4) << 24);
 }
 
-template <int BN>
+template <int BN, bool ONE = false>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;   // 16 KB
   static constexpr int B_BYTES = BN * BK * 4;   // BN * 128 B
@@ -162,8 +164,12 @@ struct Cfg {
   static constexpr int STAGES = STAGE * 3 <= 200 * 1024 ? 3 : 2;
   // two fp32 accumulators per tile (hi*hi and the hi*lo + lo*hi correction),
   // double-buffered when TMEM allows
-  static constexpr int ACC_BUFS = 4 * BN <= 512 ? 2 : 1;
-  static constexpr int COLS = ACC_BUFS * 2 * BN;
+  // ONE: the correction and hi*hi products share one accumulator (half the
+  // TMEM, so a 256-wide tile is double-buffered and the epilogue overlaps the
+  // next tile's MMAs); error ~3e-7 relative instead of ~1e-7
+  static constexpr int NACC = ONE ? 1 : 2;
+  static constexpr int ACC_BUFS = 2 * NACC * BN <= 512 ? 2 : 1;
+  static constexpr int COLS = ACC_BUFS * NACC * BN;
   static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128
                                  : COLS <= 256 ? 256 : 512;
   static constexpr int SMEM = STAGES * STAGE + 1024 /* align */ + 256 /* barriers */;
@@ -190,11 +196,11 @@ __device__ __forceinline__ void split_tile(float4 *hi, float4 *lo, int n4, int t
   }
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool ONE>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB, TcArgs g) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, ONE>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -294,8 +300,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nkb = tile_kblocks(t, k0);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d = tmem_base + static_cast<uint32_t>(acc * 2 * BN);  // hi*hi
-      const uint32_t dc = d + BN;                                          // correction
+      const uint32_t d = tmem_base + static_cast<uint32_t>(acc * C::NACC * BN);  // hi*hi
+      const uint32_t dc = ONE ? d : d + BN;                                     // correction
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&conv[stage], phase);
         tc_fence_after();
@@ -320,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
             tc_mma_tf32(dc, dal, dbh, idesc, first);
             tc_mma_tf32(dc, dah, dbl, idesc, 1u);
-            tc_mma_tf32(d, dah, dbh, idesc, first);
+            tc_mma_tf32(d, dah, dbh, idesc, ONE ? 1u : first);
           }
           tc_commit(&empty[stage]);
           if (kb == nkb - 1) tc_commit(&tfull[acc]);
@@ -381,15 +387,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       else crow = g.C + (s * g.M + row) * g.N;
       const bool vec_ok = ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
                           (direct ? (g.ldc % 4 == 0) : (g.N % 4 == 0));
+      const bool mask_vec = g.mask != nullptr && (reinterpret_cast<uintptr_t>(g.mask) & 15) == 0 &&
+                            g.ldm % 4 == 0;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         float v[16], vc[16];
         const uint32_t ta = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                            static_cast<uint32_t>(acc * 2 * BN + c);
+                            static_cast<uint32_t>(acc * C::NACC * BN + c);
         tmem_ld16(ta, v);
-        tmem_ld16(ta + BN, vc);
+        if (!ONE) {
+          tmem_ld16(ta + BN, vc);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], vc[i]);
+          for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], vc[i]);
+        }
         if (row < g.M) {
           const int64_t nb = n0 + c;
           if (direct) {
@@ -399,6 +409,23 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (g.beta != 0.0f && nb + i < g.N) o = fmaf(g.beta, crow[nb + i], o);
               if (g.relu) o = fmaxf(o, 0.0f);
               v[i] = o;
+            }
+            if (g.mask != nullptr) {  // ReLU backward of the layer below
+              const float *mrow = g.mask + row * g.ldm + nb;
+              if (mask_vec && nb + 16 <= g.N) {
+#pragma unroll
+                for (int i = 0; i < 16; i += 4) {
+                  const float4 mk = __ldg(reinterpret_cast<const float4 *>(mrow + i));
+                  v[i] = mk.x > 0.0f ? v[i] : 0.0f;
+                  v[i + 1] = mk.y > 0.0f ? v[i + 1] : 0.0f;
+                  v[i + 2] = mk.z > 0.0f ? v[i + 2] : 0.0f;
+                  v[i + 3] = mk.w > 0.0f ? v[i + 3] : 0.0f;
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                  if (nb + i < g.N && !(mrow[i] > 0.0f)) v[i] = 0.0f;
+              }
             }
           }
           if (vec_ok && nb + 16 <= g.N) {
@@ -431,7 +458,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 __global__ void splitk_sum_kernel(int64_t M, int64_t N, int splits, const float *part, float *C,
-                                  int64_t ldc, float alpha, float beta, int relu) {
+                                  int64_t ldc, float alpha, float beta, int relu,
+                                  const float *mask, int64_t ldm) {
   const int64_t n = M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -441,6 +469,7 @@ __global__ void splitk_sum_kernel(int64_t M, int64_t N, int splits, const float 
     float v = alpha * s;
     if (beta != 0.0f) v = fmaf(beta, C[m * ldc + c], v);
     if (relu) v = fmaxf(v, 0.0f);
+    if (mask && !(mask[m * ldm + c] > 0.0f)) v = 0.0f;
     C[m * ldc + c] = v;
   }
 }
@@ -484,10 +513,10 @@ int make_map(CUtensorMap *m, const float *base, int64_t inner, int64_t outer, in
   return AG_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool ONE>
 int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, TcArgs g, cudaStream_t st) {
-  using C = Cfg<BN>;
-  auto k = tc_gemm_kernel<BN, A_MN, B_MN>;
+  using C = Cfg<BN, ONE>;
+  auto k = tc_gemm_kernel<BN, A_MN, B_MN, ONE>;
   AG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   const int64_t total = static_cast<int64_t>(g.m_tiles) * g.n_tiles * g.splits;
   const int grid = static_cast<int>(std::min<int64_t>(total, sm_count()));
@@ -496,13 +525,20 @@ int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, TcArgs g, cudaStream
   return AG_OK;
 }
 
+template <int BN, bool ONE>
+int launch_bn1(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &mb,
+               const TcArgs &g, cudaStream_t st) {
+  if (!a_mn && b_mn) return launch_tc<BN, false, true, ONE>(ma, mb, g, st);
+  if (!a_mn && !b_mn) return launch_tc<BN, false, false, ONE>(ma, mb, g, st);
+  if (a_mn && b_mn) return launch_tc<BN, true, true, ONE>(ma, mb, g, st);
+  return launch_tc<BN, true, false, ONE>(ma, mb, g, st);
+}
 template <int BN>
 int launch_bn(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &mb,
               const TcArgs &g, cudaStream_t st) {
-  if (!a_mn && b_mn) return launch_tc<BN, false, true>(ma, mb, g, st);
-  if (!a_mn && !b_mn) return launch_tc<BN, false, false>(ma, mb, g, st);
-  if (a_mn && b_mn) return launch_tc<BN, true, true>(ma, mb, g, st);
-  return launch_tc<BN, true, false>(ma, mb, g, st);
+  const char *e = std::getenv("AG_TC_ONEACC");
+  if (e && std::atoi(e)) return launch_bn1<BN, true>(a_mn, b_mn, ma, mb, g, st);
+  return launch_bn1<BN, false>(a_mn, b_mn, ma, mb, g, st);
 }
 
 }  // namespace
@@ -513,7 +549,7 @@ using namespace ag;
 extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                               int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
                               float *C, int64_t ldc, float alpha, float beta, int32_t epilogue,
-                              void *stream) {
+                              const float *mask, int64_t ldm, void *stream) {
   if (M < 0 || N < 0 || K < 0) return fail(AG_ERR_VALUE, "negative GEMM sizes");
   if (M == 0 || N == 0) return AG_OK;
   const bool a_mn = trans_a != 0;  // A stored [K][M]
@@ -534,6 +570,8 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   TcArgs g{};
   g.M = M; g.N = N; g.K = K;
   g.alpha = alpha; g.beta = beta; g.relu = (epilogue & AG_GEMM_RELU) ? 1 : 0;
+  g.mask = mask;
+  g.ldm = ldm;
   {
     const char *rh = std::getenv("AG_TC_RAWHI");
     g.raw_hi = rh ? std::atoi(rh) : 0;
@@ -578,7 +616,7 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   if (rc) return rc;
   if (splits > 1) {
     splitk_sum_kernel<<<grid_for(M * N, 256), 256, 0, st>>>(M, N, splits, g.C, C, ldc, alpha,
-                                                            beta, g.relu);
+                                                            beta, g.relu, mask, ldm);
     AG_LAUNCH_CHECK("splitk_sum_kernel");
   }
   return AG_OK;

@@ -252,13 +252,15 @@ def _tc_ok(t: torch.Tensor) -> bool:
 
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
          trans_a: bool = False, trans_b: bool = False, alpha: float = 1.0, beta: float = 0.0,
-         relu: bool = False, engine: str = "auto") -> torch.Tensor:
+         relu: bool = False, relu_mask: torch.Tensor | None = None,
+         engine: str = "auto") -> torch.Tensor:
     """out = alpha * op(a) @ op(b) + beta * out (the layers' update GEMM).
 
     engine "auto" runs the tcgen05 3xTF32 tensor-core kernel (ag_gemm_tf32x3)
     whenever the operands are 16-byte aligned with row strides that are
     multiples of 4 floats, else the fp32 SIMT kernel (ag_gemm_f32); "tc" /
-    "simt" force one of them.
+    "simt" force one of them.  relu_mask fuses the ReLU backward of the layer
+    below: out = relu_mask > 0 ? out : 0 (same shape as out).
     """
     M = a.shape[1] if trans_a else a.shape[0]
     K = a.shape[0] if trans_a else a.shape[1]
@@ -272,7 +274,8 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
     fn = "ag_gemm_tf32x3" if tc else "ag_gemm_f32"
     _lib.call(fn, M, N, K, _lib.ptr(a), a.stride(0), int(trans_a), _lib.ptr(b),
               b.stride(0), int(trans_b), _lib.ptr(out), out.stride(0), float(alpha), float(beta),
-              _lib.AG_GEMM_RELU if relu else 0, _lib.stream())
+              _lib.AG_GEMM_RELU if relu else 0, _lib.ptr(relu_mask),
+              0 if relu_mask is None else relu_mask.stride(0), _lib.stream())
     return out
 
 
@@ -396,11 +399,12 @@ def fusable(kernel_intra: KernelKind, kernel_inter: KernelKind) -> bool:
 
 
 def run_fused_pair(d: DecomposedGraph, x: torch.Tensor, y: torch.Tensor, op: AggregateOp,
-                   gin_scale: float | None = None, relu_src: torch.Tensor | None = None) -> None:
-    """y = combine(intra, inter) [+ gin] [* (relu_src > 0)] in one pass over the
-    full reordered CSR."""
+                   gin_scale: float | None = None, relu_src: torch.Tensor | None = None,
+                   relu: bool = False) -> None:
+    """y = combine(intra, inter) [+ gin] [relu] [* (relu_src > 0)] in one pass
+    over the full reordered CSR."""
     full = full_graph(d)
-    flags = _lib.AG_EPI_GIN if gin_scale is not None else 0
+    flags = (_lib.AG_EPI_GIN if gin_scale is not None else 0) | (_lib.AG_EPI_RELU if relu else 0)
     launch_fused(to_csr(full), x, y, op, block=d.block_size, mask=3, flags=flags,
                  deg=d.full_in_degree, gin_scale=0.0 if gin_scale is None else gin_scale,
                  relu_src=relu_src)

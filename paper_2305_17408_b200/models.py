@@ -223,6 +223,9 @@ class GNN:
     weights: list = field(default_factory=list)
     gin_eps: float = 0.0
     kernels: dict = field(default_factory=dict)
+    # narrowing layers (F_out < F_in) run the update GEMM first and aggregate
+    # at the output width: A_hat (H W) == (A_hat H) W, the cheaper association
+    reassociate: bool = True
     default_pair: tuple = (KernelKind.CSR_INTRA_BLOCKED, KernelKind.CSR_INTER)
     # when a list, every aggregation appends (start_event, end_event, F, subject)
     events: list | None = None
@@ -270,8 +273,11 @@ class GNN:
         from .selector import SelectorState, run_training_loop
         if not hasattr(self, "selector_choice"):
             self.selector_choice = {}
-        for direction, subj in (("fwd", self.subject), ("bwd", self.subject_t)):
-            widths = self.dims[:-1] if direction == "fwd" else self.dims[1:-1]
+        L = self.num_layers
+        fwd = [_pad4(self.dims[l + 1]) if self.gemm_first(l) else self.dims[l] for l in range(L)]
+        bwd = [_pad4(self.dims[l + 1]) if self.gemm_first(l) else self.dims[l]
+               for l in range(L) if self.gemm_first(l) or l > 0]
+        for direction, subj, widths in (("fwd", self.subject, fwd), ("bwd", self.subject_t, bwd)):
             for f in sorted(set(widths)):
                 if (direction, f) in self.kernels:
                     continue
@@ -291,11 +297,17 @@ class GNN:
                 self.kernels[(direction, f)] = pair
         return dict(self.kernels)
 
+    def gemm_first(self, l: int) -> bool:
+        return self.reassociate and self.dims[l + 1] < self.dims[l]
+
     def _aggregate(self, subj: DecomposedGraph, h: torch.Tensor, direction: str,
-                   relu_src: torch.Tensor | None = None):
+                   relu_src: torch.Tensor | None = None, relu: bool = False):
         """Aggregation of one layer; relu_src fuses the ReLU backward of the
-        layer below into the (transposed) aggregation's epilogue."""
+        layer below into the (transposed) aggregation's epilogue, relu the
+        forward activation (gemm-first layers)."""
         ki, ke = self.pair(direction, h.shape[1])
+        if relu_src is not None and relu_src.stride(0) != relu_src.shape[1]:
+            relu_src = relu_src.contiguous()  # the kernel reads it with row stride F
         e0 = e1 = None
         if self.events is not None:
             e0 = torch.cuda.Event(enable_timing=True)
@@ -305,12 +317,16 @@ class GNN:
             h = _check_features(subj.num_vertices, h)
             out = torch.empty((subj.num_vertices, h.shape[1]), dtype=torch.float32,
                               device=h.device)
-            run_fused_pair(subj, h, out, AggregateOp.SUM, self.gin_scale(), relu_src=relu_src)
+            run_fused_pair(subj, h, out, AggregateOp.SUM, self.gin_scale(), relu_src=relu_src,
+                           relu=relu)
         else:
             out = aggregate_decomposed(subj, h, AggregateOp.SUM, kernel_intra=ki,
                                        kernel_inter=ke, gin_scale=self.gin_scale())
             if relu_src is not None:
                 _lib.call("ag_relu_backward", out.numel(), _lib.ptr(relu_src), _lib.ptr(out),
+                          _lib.stream())
+            if relu:  # out = out > 0 ? out : 0
+                _lib.call("ag_relu_backward", out.numel(), _lib.ptr(out), _lib.ptr(out),
                           _lib.stream())
         if e0 is not None:
             e1.record()
@@ -318,37 +334,59 @@ class GNN:
         return out
 
     def forward(self, x: torch.Tensor):
-        """Returns (logits, saved) with saved = per-layer (agg/h input, output)."""
+        """Returns (logits, saved) with saved[l] = (kind, operand, output):
+        kind "agg" -- operand is A_hat H_l (agg first, models.py:86-112 order);
+        kind "gemm" -- operand is H_l itself (gemm first, narrowing layers)."""
         saved = []
         h = x
         for l in range(self.num_layers):
-            agg = self._aggregate(self.subject, h, "fwd")
             last = l == self.num_layers - 1
-            out = _padded_empty(agg.shape[0], self.dims[l + 1], agg.device)
-            gemm(agg, self.weights[l], out, relu=not last)
-            saved.append((agg, out))
+            if self.gemm_first(l):
+                # P = H W over the zero-padded output width, then A_hat P (+ GIN
+                # (1+eps) P) with the activation fused into the aggregation
+                p = _padded_empty(h.shape[0], self.dims[l + 1], h.device)
+                gemm(h, self.weights[l], p)
+                out = self._aggregate(self.subject, _base(p), "fwd", relu=not last)
+                out = out[:, :self.dims[l + 1]]
+                saved.append(("gemm", h, out))
+            else:
+                agg = self._aggregate(self.subject, h, "fwd")
+                out = _padded_empty(agg.shape[0], self.dims[l + 1], agg.device)
+                gemm(agg, self.weights[l], out, relu=not last)
+                saved.append(("agg", agg, out))
             h = out
         return h, saved
 
     def backward(self, saved, d_logits: torch.Tensor):
-        """Returns the list of dW (layer order)."""
+        """Returns the list of dW (layer order).  g is dL/d(pre-activation)."""
         grads = [None] * self.num_layers
         g = d_logits
         for l in range(self.num_layers - 1, -1, -1):
-            agg, _ = saved[l]
-            grads[l] = torch.zeros((agg.shape[1], _pad4(self.dims[l + 1])), dtype=torch.float32,
-                                   device=agg.device)[:, :self.dims[l + 1]]
-            gemm(agg, g, grads[l], trans_a=True)
-            if l == 0:
-                break
-            d_in = gemm(g, self.weights[l], trans_b=True)
-            _, h_prev = saved[l - 1]
-            g = self._aggregate(self.subject_t, d_in, "bwd", relu_src=h_prev)
+            kind, operand, _ = saved[l]
+            grads[l] = torch.zeros((self.dims[l], _pad4(self.dims[l + 1])), dtype=torch.float32,
+                                   device=g.device)[:, :self.dims[l + 1]]
+            h_prev = saved[l - 1][2] if l > 0 else None
+            if kind == "agg":
+                gemm(operand, g, grads[l], trans_a=True)                 # dW = (A H)^T g
+                if l == 0:
+                    break
+                d_in = gemm(g, self.weights[l], trans_b=True)          # d(A H) = g W^T
+                g = self._aggregate(self.subject_t, d_in, "bwd", relu_src=h_prev)
+            else:
+                # q = A_hat^T g (+ (1+eps) g), at the layer's (narrow) output width
+                q = self._aggregate(self.subject_t, _base(g), "bwd")[:, :self.dims[l + 1]]
+                gemm(operand, q, grads[l], trans_a=True)                 # dW = H^T q
+                if l == 0:
+                    break
+                g = _padded_empty(q.shape[0], self.dims[l], q.device)
+                gemm(q, self.weights[l], g, trans_b=True, relu_mask=h_prev)  # dH, ReLU bwd
         return grads
 
     def loss_and_grad(self, logits, labels, mask, num_masked: int):
         loss = torch.empty(1, dtype=torch.float32, device=logits.device)
-        d_logits = _padded_empty(logits.shape[0], logits.shape[1], logits.device)
+        # zero pad columns: a gemm-first last layer aggregates the padded width
+        d_logits = torch.zeros((logits.shape[0], _pad4(logits.shape[1])), dtype=torch.float32,
+                               device=logits.device)[:, :logits.shape[1]]
         _lib.call("ag_softmax_xent", logits.shape[0], logits.shape[1], logits.stride(0),
                   _lib.ptr(logits), _lib.ptr(labels), _lib.ptr(mask), int(num_masked),
                   _lib.ptr(loss), _lib.ptr(d_logits), _lib.stream())

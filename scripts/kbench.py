@@ -112,6 +112,17 @@ def main():
         res["gemm_dH_rawhi"] = timeit(lambda: K.gemm(g256, w, trans_b=True))
         out.setdefault("rawhi_bitwise", []).append(bool(torch.equal(K.gemm(x, w), ref_g)))
         os.environ.pop("AG_TC_RAWHI")
+        ref64 = x.double() @ w.double()
+        def relerr(t):
+            return float(((t.double() - ref64).abs() / ref64.abs().clamp(min=1.0)).max())
+        out.setdefault("gemm_relerr_twoacc", []).append(relerr(K.gemm(x, w)))
+        os.environ["AG_TC_ONEACC"] = "1"
+        out.setdefault("gemm_relerr_oneacc", []).append(relerr(K.gemm(x, w)))
+        res["gemm_Fx256_oneacc"] = timeit(lambda: K.gemm(x, w))
+        res["gemm_dW_oneacc"] = timeit(lambda: K.gemm(x, g256, trans_a=True))
+        res["gemm_dH_oneacc"] = timeit(lambda: K.gemm(g256, w, trans_b=True))
+        os.environ.pop("AG_TC_ONEACC")
+        del ref64
         res["gemm_Fx256_simt"] = timeit(lambda: K.gemm(x, w, engine="simt"))
         gbs = {k: round(ba / (v / 1e3) / 1e9, 1) for k, v in res.items() if "gemm" not in k}
         out[f"F{F}"] = {"ms": {k: round(v, 4) for k, v in res.items()}, "alg_GBps": gbs,

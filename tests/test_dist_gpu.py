@@ -70,6 +70,7 @@ def test_world1_distgnn_equals_gnn(model, monkeypatch):
     rg, dec = _setup(model, V=3000, E=30000)
     dims = [32, 24, 16, 5]
     ref = ag.GNN.build(model, dims, dec, seed=4, gin_eps=0.1)
+    ref.reassociate = False  # DistGNN keeps the reference's aggregate-first order
     net = D.DistGNN.build(model, dims, dec, rank=0, world=1, seed=4, gin_eps=0.1)
     V = rg.num_vertices
     g = torch.Generator(device="cuda").manual_seed(3)
