@@ -254,15 +254,23 @@ def run_ours(args, cfg):
     del xd
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_steps = max(1, min(args.steps, 5))
+    # one untimed step through the same path: the caching allocator grows its
+    # pool for the host-fed inputs once, as any steady-state run does
+    loss, _ = step_from_host(x_host, lab_host, mask_host)
+    float(loss.item())
     if world > 1:
         dist.barrier()
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps + 1)]
     e_start.record()
-    for _ in range(e2e_steps):
+    step_ev[0].record()
+    for i in range(e2e_steps):
         loss, _ = step_from_host(x_host, lab_host, mask_host)
         loss_val = float(loss.item())  # D2H of the step's result
+        step_ev[i + 1].record()
     e_end.record()
     torch.cuda.synchronize()
     e2e_ms = e_start.elapsed_time(e_end) / e2e_steps
+    e2e_each = [round(step_ev[i].elapsed_time(step_ev[i + 1]), 2) for i in range(e2e_steps)]
     if world > 1:
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -309,7 +317,7 @@ def run_ours(args, cfg):
         },
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms/epoch", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4, "loss": loss_val,
-                "h2d_x_GBps": round(h2d_gbs, 1)},
+                "h2d_x_GBps": round(h2d_gbs, 1), "steps_ms": e2e_each},
         "roofline": {
             "bound": "hbm",
             "achieved": round(achieved, 1),

@@ -112,6 +112,18 @@ def main():
         res["gemm_dH_rawhi"] = timeit(lambda: K.gemm(g256, w, trans_b=True))
         out.setdefault("rawhi_bitwise", []).append(bool(torch.equal(K.gemm(x, w), ref_g)))
         os.environ.pop("AG_TC_RAWHI")
+        q48 = torch.randn((V, 48), device="cuda")
+        w48 = torch.randn((256, 48), device="cuda")
+        mk = torch.randn((V, 256), device="cuda")
+        x100 = torch.randn((V, 100), device="cuda")
+        w100 = torch.randn((100, 256), device="cuda")
+        for bn in ("256", "128"):
+            os.environ["AG_TC_BN"] = bn
+            res[f"gemm_dH48_mask_bn{bn}"] = timeit(lambda: K.gemm(q48, w48, trans_b=True,
+                                                                  relu_mask=mk))
+            res[f"gemm_fwd100_bn{bn}"] = timeit(lambda: K.gemm(x100, w100))
+        os.environ.pop("AG_TC_BN")
+        del q48, mk, x100
         ref64 = x.double() @ w.double()
         def relerr(t):
             return float(((t.double() - ref64).abs() / ref64.abs().clamp(min=1.0)).max())

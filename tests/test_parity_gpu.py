@@ -310,3 +310,21 @@ def test_training_step_vs_composed_oracle(model, rng):
     assert abs(float(loss.item()) - oloss) <= 1e-5 * max(1.0, abs(oloss))
     for l, (gw, ow) in enumerate(zip(grads, ograds)):
         assert rel_error(to_np(gw), ow) < 1e-5, l
+
+
+def test_prepare_matches_manual_pipeline(rng):
+    """bench.prepare (bench.py:128-151): normalise, reorder, decompose + timings."""
+    from conftest import random_graph_arrays
+    V, d, s, _ = random_graph_arrays(rng, num_vertices=300, density=0.03)
+    g = ag.Graph.from_edges(V, d, s)
+    for reorder in ("bfs", "none"):
+        cfg = ag.RunConfig(model="gcn", reorder=reorder, comm_size=8)
+        run = ag.prepare(cfg, g)
+        gn = ag.gcn_normalize(g)
+        part = ag.cluster_bfs(gn, 8) if reorder == "bfs" else ag.identity_partition(V, 8)
+        rg = ag.apply_reorder(gn, part)
+        assert torch.equal(run.graph.dst, rg.dst) and torch.equal(run.graph.src, rg.src)
+        assert run.decomposed.intra.num_edges == ag.decompose(rg, 8).intra.num_edges
+        assert run.reorder_ms >= 0 and run.decompose_ms >= 0
+    with pytest.raises(ValueError, match="unknown reorder"):
+        ag.prepare(ag.RunConfig(reorder="metis"), g)
