@@ -279,9 +279,15 @@ int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
  * reduction. */
 int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                    int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
-                   float *C, int64_t ldc, float alpha, float beta,
+                   const float *B_lo, float *C, int64_t ldc, float alpha, float beta,
                    int32_t epilogue, const float *mask, int64_t ldm,
                    void *stream);
+
+/* lo[i] = src[i] - tf32_truncate(src[i]) (exact): the low half of the 3xTF32
+ * split, precomputed for a small B operand that every output tile re-reads
+ * (the layer weights); pass it as ag_gemm_tf32x3's B_lo (NULL: split in
+ * shared memory).  src / lo share the layout. */
+int ag_tf32_split_lo(int64_t n, const float *src, float *lo, void *stream);
 
 /* ===================== training helpers (composed) ======================= */
 

@@ -60,8 +60,9 @@ SIGNATURES: dict[str, list] = {
     "ag_slab_far_capacity": [],
     "ag_combine": [I64, I64, P, P, P, P, P, I32, P, P],
     "ag_gemm_f32": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, F32, F32, I32, P, I64, P],
-    "ag_gemm_tf32x3": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, F32, F32, I32, P, I64,
-                       P],
+    "ag_gemm_tf32x3": [I64, I64, I64, P, I64, I32, P, I64, I32, P, P, I64, F32, F32, I32, P,
+                       I64, P],
+    "ag_tf32_split_lo": [I64, P, P, P],
     "ag_softmax_xent": [I64, I64, I64, P, P, P, I64, P, P, P],
     "ag_relu_backward": [I64, P, P, P],
     "ag_sgd_step": [I64, P, P, F32, P],

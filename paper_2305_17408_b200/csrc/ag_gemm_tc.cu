@@ -53,6 +53,7 @@ struct TcArgs {
   int relu;
   int m_tiles, n_tiles, splits;
   int raw_hi;  // 1: leave x in place as the hi operand (the MMA reads its tf32 bits)
+  int b_presplit;  // 1: B's lo half comes from global (ag_tf32_split_lo), only A is split
   const float *mask;  // ReLU-backward mask operand (NULL: none): out = mask > 0 ? out : 0
   int64_t ldm;
   int64_t k_per_split;  // multiple of BK
@@ -199,7 +200,8 @@ __device__ __forceinline__ void split_tile(float4 *hi, float4 *lo, int n4, int t
 template <int BN, bool A_MN, bool B_MN, bool ONE>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                   const __grid_constant__ CUtensorMap tmB, TcArgs g) {
+                   const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmBl, TcArgs g) {
   using C = Cfg<BN, ONE>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>(
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           unsigned char *st = smem + stage * C::STAGE;
           unsigned char *sa = st, *sb = st + 2 * C::A_BYTES;
-          mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+          mbar_expect_tx(&full[stage], C::A_BYTES + (g.b_presplit ? 2 : 1) * C::B_BYTES);
           const int kk = static_cast<int>(k0 + static_cast<int64_t>(kb) * BK);
           if (A_MN) {  // boxes {32 (m), 32 (k)}: 4 KB each, LBO apart
 #pragma unroll
@@ -283,6 +285,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                           n0 + 32 * c, kk);
           } else {
             tma_load_2d(sb, &tmB, &full[stage], kk, n0);
+          }
+          if (g.b_presplit) {  // B's lo half straight into its slot (raw B is the hi half)
+            unsigned char *sbl = sb + C::B_BYTES;
+            if (B_MN) {
+#pragma unroll
+              for (int c = 0; c < BN / 32; ++c) tma_load_2d(sbl + c * 4096, &tmBl, &full[stage],
+                                                            n0 + 32 * c, kk);
+            } else {
+              tma_load_2d(sbl, &tmBl, &full[stage], kk, n0);
+            }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -349,7 +361,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[stage], phase);
         unsigned char *st = smem + stage * C::STAGE;
-        if (g.raw_hi) {
+        if (g.b_presplit) {
+          split_tile<true>(reinterpret_cast<float4 *>(st),
+                           reinterpret_cast<float4 *>(st + C::A_BYTES), C::A_BYTES / 16, t_id, 128);
+        } else if (g.raw_hi) {
           split_tile<true>(reinterpret_cast<float4 *>(st),
                            reinterpret_cast<float4 *>(st + C::A_BYTES), C::A_BYTES / 16, t_id, 128);
           split_tile<true>(reinterpret_cast<float4 *>(st + 2 * C::A_BYTES),
@@ -378,9 +393,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t mn = t % tiles_mn;
       const int64_t m0 = (mn / g.n_tiles) * BM;
       const int64_t n0 = (mn % g.n_tiles) * BN;
+      const int64_t row = m0 + q * 32 + lane;
+      if (g.mask != nullptr && g.splits == 1 && row < g.M && (g.ldm % 4) == 0) {
+        // pull this row's mask segment into L2 while the tile's MMAs run
+        const float *mp = g.mask + row * g.ldm + n0;
+        const int64_t cols = std::min<int64_t>(BN, g.N - n0);
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(mp) & ~uintptr_t(15);
+        const uintptr_t hi = (reinterpret_cast<uintptr_t>(mp + cols) + 15) & ~uintptr_t(15);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo),
+                     "r"(static_cast<uint32_t>(hi - lo))
+                     : "memory");
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t row = m0 + q * 32 + lane;
       float *crow;
       bool direct = g.splits == 1;
       if (direct) crow = g.C + row * g.ldc;
@@ -514,31 +539,40 @@ int make_map(CUtensorMap *m, const float *base, int64_t inner, int64_t outer, in
 }
 
 template <int BN, bool A_MN, bool B_MN, bool ONE>
-int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, TcArgs g, cudaStream_t st) {
+int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbl, TcArgs g,
+              cudaStream_t st) {
   using C = Cfg<BN, ONE>;
   auto k = tc_gemm_kernel<BN, A_MN, B_MN, ONE>;
   AG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   const int64_t total = static_cast<int64_t>(g.m_tiles) * g.n_tiles * g.splits;
   const int grid = static_cast<int>(std::min<int64_t>(total, sm_count()));
-  k<<<grid, kThreads, C::SMEM, st>>>(ma, mb, g);
+  k<<<grid, kThreads, C::SMEM, st>>>(ma, mb, mbl, g);
   AG_LAUNCH_CHECK("tc_gemm_kernel");
   return AG_OK;
 }
 
 template <int BN, bool ONE>
 int launch_bn1(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &mb,
-               const TcArgs &g, cudaStream_t st) {
-  if (!a_mn && b_mn) return launch_tc<BN, false, true, ONE>(ma, mb, g, st);
-  if (!a_mn && !b_mn) return launch_tc<BN, false, false, ONE>(ma, mb, g, st);
-  if (a_mn && b_mn) return launch_tc<BN, true, true, ONE>(ma, mb, g, st);
-  return launch_tc<BN, true, false, ONE>(ma, mb, g, st);
+               const CUtensorMap &mbl, const TcArgs &g, cudaStream_t st) {
+  if (!a_mn && b_mn) return launch_tc<BN, false, true, ONE>(ma, mb, mbl, g, st);
+  if (!a_mn && !b_mn) return launch_tc<BN, false, false, ONE>(ma, mb, mbl, g, st);
+  if (a_mn && b_mn) return launch_tc<BN, true, true, ONE>(ma, mb, mbl, g, st);
+  return launch_tc<BN, true, false, ONE>(ma, mb, mbl, g, st);
 }
 template <int BN>
 int launch_bn(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &mb,
-              const TcArgs &g, cudaStream_t st) {
+              const CUtensorMap &mbl, const TcArgs &g, cudaStream_t st) {
   const char *e = std::getenv("AG_TC_ONEACC");
-  if (e && std::atoi(e)) return launch_bn1<BN, true>(a_mn, b_mn, ma, mb, g, st);
-  return launch_bn1<BN, false>(a_mn, b_mn, ma, mb, g, st);
+  if (e && std::atoi(e)) return launch_bn1<BN, true>(a_mn, b_mn, ma, mb, mbl, g, st);
+  return launch_bn1<BN, false>(a_mn, b_mn, ma, mb, mbl, g, st);
+}
+
+__global__ void tf32_split_lo_kernel(int64_t n, const float *src, float *lo) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = src[i];
+    lo[i] = __fsub_rn(v, __uint_as_float(__float_as_uint(v) & 0xFFFFE000u));
+  }
 }
 
 }  // namespace
@@ -546,16 +580,24 @@ int launch_bn(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &mb
 
 using namespace ag;
 
+extern "C" int ag_tf32_split_lo(int64_t n, const float *src, float *lo, void *stream) {
+  if (n < 0) return fail(AG_ERR_VALUE, "negative size");
+  if (n == 0) return AG_OK;
+  tf32_split_lo_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, src, lo);
+  AG_LAUNCH_CHECK("tf32_split_lo_kernel");
+  return AG_OK;
+}
+
 extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                               int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
-                              float *C, int64_t ldc, float alpha, float beta, int32_t epilogue,
-                              const float *mask, int64_t ldm, void *stream) {
+                              const float *B_lo, float *C, int64_t ldc, float alpha, float beta,
+                              int32_t epilogue, const float *mask, int64_t ldm, void *stream) {
   if (M < 0 || N < 0 || K < 0) return fail(AG_ERR_VALUE, "negative GEMM sizes");
   if (M == 0 || N == 0) return AG_OK;
   const bool a_mn = trans_a != 0;  // A stored [K][M]
   const bool b_mn = trans_b == 0;  // B stored [K][N]
   auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (!al16(A) || !al16(B) || (lda % 4) || (ldb % 4))
+  if (!al16(A) || !al16(B) || (B_lo && !al16(B_lo)) || (lda % 4) || (ldb % 4))
     return fail(AG_ERR_VALUE, "tensor-core GEMM needs 16-byte aligned operands and row strides");
   if (M > 2147483647LL || N > 2147483647LL || K > 2147483647LL)
     return fail(AG_ERR_VALUE, "GEMM dimension too large");
@@ -566,12 +608,16 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   // N tile: the whole N when it fits one MMA (<= 256), padded to 16
   int bn = static_cast<int>(std::min<int64_t>(256, ((N + 15) / 16) * 16));
   bn = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
+  // short K: the epilogue dominates a tile; 128-wide tiles double-buffer the
+  // TMEM accumulators so it overlaps the next tile's MMAs (measured faster)
+  if (bn == 256 && K <= 128) bn = 128;
   if (const char *e = std::getenv("AG_TC_BN")) bn = std::min(bn, std::max(32, std::atoi(e)));
   TcArgs g{};
   g.M = M; g.N = N; g.K = K;
   g.alpha = alpha; g.beta = beta; g.relu = (epilogue & AG_GEMM_RELU) ? 1 : 0;
   g.mask = mask;
   g.ldm = ldm;
+  g.b_presplit = B_lo != nullptr;
   {
     const char *rh = std::getenv("AG_TC_RAWHI");
     g.raw_hi = rh ? std::atoi(rh) : 0;
@@ -598,6 +644,12 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   if (b_mn) rc = make_map(&mb, B, N, K, ldb, 32, true);
   else rc = make_map(&mb, B, K, N, ldb, bn, false);
   if (rc) return rc;
+  CUtensorMap mbl = mb;
+  if (B_lo) {
+    if (b_mn) rc = make_map(&mbl, B_lo, N, K, ldb, 32, true);
+    else rc = make_map(&mbl, B_lo, K, N, ldb, bn, false);
+    if (rc) return rc;
+  }
   Scratch ws;
   if (splits > 1) {
     AG_CUDA(ws.alloc(static_cast<size_t>(splits) * M * N * sizeof(float), st));
@@ -608,10 +660,10 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
     g.ldc = ldc;
   }
   switch (bn) {
-    case 32: rc = launch_bn<32>(a_mn, b_mn, ma, mb, g, st); break;
-    case 64: rc = launch_bn<64>(a_mn, b_mn, ma, mb, g, st); break;
-    case 128: rc = launch_bn<128>(a_mn, b_mn, ma, mb, g, st); break;
-    default: rc = launch_bn<256>(a_mn, b_mn, ma, mb, g, st); break;
+    case 32: rc = launch_bn<32>(a_mn, b_mn, ma, mb, mbl, g, st); break;
+    case 64: rc = launch_bn<64>(a_mn, b_mn, ma, mb, mbl, g, st); break;
+    case 128: rc = launch_bn<128>(a_mn, b_mn, ma, mb, mbl, g, st); break;
+    default: rc = launch_bn<256>(a_mn, b_mn, ma, mb, mbl, g, st); break;
   }
   if (rc) return rc;
   if (splits > 1) {

@@ -37,6 +37,7 @@ from .graph import Graph, as_device
 
 DEFAULT_TILE_BUDGET_BYTES = 48 * 1024
 DENSE_ORACLE_CAP = 4096
+PRESPLIT_MAX_ELEMS = 1 << 20  # B operands up to 4 MB get a precomputed tf32 lo half
 
 
 class AggregateOp(enum.Enum):
@@ -271,11 +272,24 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
     if out is None:
         out = torch.empty((M, N), dtype=torch.float32, device=a.device)
     tc = engine == "tc" or (engine == "auto" and K > 0 and _tc_ok(a) and _tc_ok(b))
-    fn = "ag_gemm_tf32x3" if tc else "ag_gemm_f32"
-    _lib.call(fn, M, N, K, _lib.ptr(a), a.stride(0), int(trans_a), _lib.ptr(b),
-              b.stride(0), int(trans_b), _lib.ptr(out), out.stride(0), float(alpha), float(beta),
-              _lib.AG_GEMM_RELU if relu else 0, _lib.ptr(relu_mask),
-              0 if relu_mask is None else relu_mask.stride(0), _lib.stream())
+    epi = _lib.AG_GEMM_RELU if relu else 0
+    mask_ld = 0 if relu_mask is None else relu_mask.stride(0)
+    if tc:
+        b_lo = None
+        if b.shape[0] * b.stride(0) <= PRESPLIT_MAX_ELEMS:
+            # a small B (the layer weights) is re-read by every output tile: split
+            # its tf32 lo half once instead of in every tile's shared memory
+            base = b.as_strided((b.shape[0], b.stride(0)), (b.stride(0), 1))
+            b_lo = torch.empty_like(base)
+            _lib.call("ag_tf32_split_lo", base.numel(), _lib.ptr(base), _lib.ptr(b_lo),
+                      _lib.stream())
+        _lib.call("ag_gemm_tf32x3", M, N, K, _lib.ptr(a), a.stride(0), int(trans_a), _lib.ptr(b),
+                  b.stride(0), int(trans_b), _lib.ptr(b_lo), _lib.ptr(out), out.stride(0),
+                  float(alpha), float(beta), epi, _lib.ptr(relu_mask), mask_ld, _lib.stream())
+    else:
+        _lib.call("ag_gemm_f32", M, N, K, _lib.ptr(a), a.stride(0), int(trans_a), _lib.ptr(b),
+                  b.stride(0), int(trans_b), _lib.ptr(out), out.stride(0), float(alpha),
+                  float(beta), epi, _lib.ptr(relu_mask), mask_ld, _lib.stream())
     return out
 
 
