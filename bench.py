@@ -116,6 +116,50 @@ def build_workload(cfg, rank=0, world=1):
     return g, rg, dec, net, prep_s
 
 
+class HostFeeder:
+    """Double-buffered pinned-host -> device inputs on a side stream: step i+1's
+    inputs cross PCIe while step i computes (the usual pin_memory /
+    non_blocking DataLoader overlap).  Every step's bytes are still copied
+    inside the timed region; only their latency is hidden."""
+
+    def __init__(self, host):
+        import torch
+        self.host = host
+        self.bufs = [[torch.empty(t.shape, dtype=t.dtype, device="cuda") for t in host]
+                     for _ in range(2)]
+        self.stream = torch.cuda.Stream()
+        self.ready = [torch.cuda.Event(), torch.cuda.Event()]
+        self.free = [torch.cuda.Event(), torch.cuda.Event()]
+        self.reset()
+
+    def reset(self):
+        import torch
+        self.i = 0
+        for e in self.free:
+            e.record(torch.cuda.current_stream())
+
+    def issue(self, k):
+        import torch
+        with torch.cuda.stream(self.stream):
+            self.stream.wait_event(self.free[k])  # the step that used buffer k is done
+            for d, h in zip(self.bufs[k], self.host):
+                d.copy_(h, non_blocking=True)
+            self.ready[k].record(self.stream)
+
+    def get(self, prefetch_next=True):
+        import torch
+        k = self.i % 2
+        torch.cuda.current_stream().wait_event(self.ready[k])
+        if prefetch_next:
+            self.issue(1 - k)
+        self.i += 1
+        return self.bufs[k], k
+
+    def release(self, k):
+        import torch
+        self.free[k].record(torch.cuda.current_stream())
+
+
 def ncu_traffic():
     """DRAM bytes of one F=256 aggregation launch from the committed ncu
     capture (profiles/r01_ncu_slab_gemm.json), or (None, reason)."""
@@ -168,10 +212,8 @@ def run_ours(args, cfg):
         def step():
             return dnet.train_step(x_ext, labels, mask, n_mask, lr)
 
-        def step_from_host(xh, lh, mh):
-            xe = dnet.input_ext(xh.to("cuda", non_blocking=True))
-            return dnet.train_step(xe, lh.to("cuda", non_blocking=True),
-                                   mh.to("cuda", non_blocking=True), n_mask, lr)
+        def step_on(xd, ld, md):
+            return dnet.train_step(dnet.input_ext(xd), ld, md, n_mask, lr)
         timed = dnet
         host_x = x_local
         halo = {"fwd_halo_rows_per_rank": dnet.fwd.plan.max_send,
@@ -185,10 +227,8 @@ def run_ours(args, cfg):
         def step():
             return net.train_step(x, labels, mask, n_mask, lr)
 
-        def step_from_host(xh, lh, mh):
-            return net.train_step(xh.to("cuda", non_blocking=True),
-                                  lh.to("cuda", non_blocking=True),
-                                  mh.to("cuda", non_blocking=True), n_mask, lr)
+        def step_on(xd, ld, md):
+            return net.train_step(xd, ld, md, n_mask, lr)
         timed = net
         host_x = x
         halo = None
@@ -253,20 +293,33 @@ def run_ours(args, cfg):
     h2d_gbs = x_host.numel() * 4 / (h0.elapsed_time(h1) / 1e3) / 1e9
     del xd
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(1, min(args.steps, 5))
+    e2e_steps = max(1, min(args.steps, 10))
+    feeder = HostFeeder([x_host, lab_host, mask_host])
     # one untimed step through the same path: the caching allocator grows its
     # pool for the host-fed inputs once, as any steady-state run does
-    loss, _ = step_from_host(x_host, lab_host, mask_host)
+    feeder.issue(0)
+    (xd, ld, md), k = feeder.get()
+    loss, _ = step_on(xd, ld, md)
+    feeder.release(k)
     float(loss.item())
+    torch.cuda.synchronize()
+    feeder.reset()
     if world > 1:
         dist.barrier()
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps + 1)]
     e_start.record()
     step_ev[0].record()
+    feeder.issue(0)
+    host_ms = []
     for i in range(e2e_steps):
-        loss, _ = step_from_host(x_host, lab_host, mask_host)
+        t_h = time.perf_counter()
+        (xd, ld, md), k = feeder.get(prefetch_next=i + 1 < e2e_steps)
+        loss, _ = step_on(xd, ld, md)
+        t_l = time.perf_counter()
+        feeder.release(k)
         loss_val = float(loss.item())  # D2H of the step's result
         step_ev[i + 1].record()
+        host_ms.append((round((t_l - t_h) * 1e3, 2), round((time.perf_counter() - t_h) * 1e3, 2)))
     e_end.record()
     torch.cuda.synchronize()
     e2e_ms = e_start.elapsed_time(e_end) / e2e_steps
@@ -316,8 +369,11 @@ def run_ours(args, cfg):
             **({"halo": halo} if halo else {}),
         },
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms/epoch", "h2d_bytes_per_step": h2d,
+                "input_pipeline": "pinned host -> device on a side stream, double-buffered "
+                                  "(step i+1's copy overlaps step i)",
                 "d2h_bytes_per_step": 4, "loss": loss_val,
-                "h2d_x_GBps": round(h2d_gbs, 1), "steps_ms": e2e_each},
+                "h2d_x_GBps": round(h2d_gbs, 1), "steps_ms": e2e_each,
+                "host_launch_ms_total_ms": host_ms},
         "roofline": {
             "bound": "hbm",
             "achieved": round(achieved, 1),
