@@ -54,6 +54,8 @@ struct TcArgs {
   int m_tiles, n_tiles, splits;
   int raw_hi;  // 1: leave x in place as the hi operand (the MMA reads its tf32 bits)
   int b_presplit;  // 1: B's lo half comes from global (ag_tf32_split_lo), only A is split
+  int exp;         // timing experiments (AG_TC_EXP bits; results invalid): 1 no split,
+                   // 2 one MMA per k-step, 4 no epilogue stores
   const float *mask;  // ReLU-backward mask operand (NULL: none): out = mask > 0 ? out : 0
   int64_t ldm;
   int64_t k_per_split;  // multiple of BK
@@ -68,7 +70,9 @@ __device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t n) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
   uint32_t done = 0;
+  uint32_t spins = 0;
   while (!done) {
+    if (++spins > (1u << 24)) __trap();  // a lost arrival: fail instead of hanging
     asm volatile(
         "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
@@ -96,6 +100,27 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
       : "memory");
+}
+// the same load delivered to the same shared-memory offset (and mbarrier) of
+// every CTA in `mask` of the cluster
+__device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                               int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint64_t *bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(su32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
 }
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap *map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -197,7 +222,11 @@ __device__ __forceinline__ void split_tile(float4 *hi, float4 *lo, int n4, int t
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, bool ONE>
+// CL > 1: a cluster of CL CTAs computes CL vertically adjacent 128-row tiles
+// of the same N tile in lockstep; each CTA TMA-loads 1/CL of every B k-block
+// and multicasts it to all of them, so B crosses L2 once per cluster, and the
+// MMA completions free the stage in every CTA (multicast commit).
+template <int BN, bool A_MN, bool B_MN, bool ONE, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB,
@@ -214,15 +243,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tiles_mn = static_cast<int64_t>(g.m_tiles) * g.n_tiles;
+  // cluster tiles: CL consecutive M tiles x one N tile x one K split
+  const int rank = static_cast<int>(blockIdx.x % CL);
+  const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  const int64_t msup = (g.m_tiles + CL - 1) / CL;
+  const int64_t tiles_mn = msup * g.n_tiles;
   const int64_t total = tiles_mn * g.splits;
   const int nkb_full = static_cast<int>(g.k_per_split / BK);
+  constexpr uint16_t kAll = static_cast<uint16_t>((1u << CL) - 1u);
+  auto tile_m0 = [&](int64_t t) -> int64_t {
+    return (((t % tiles_mn) / g.n_tiles) * CL + rank) * BM;
+  };
+  auto tile_n0 = [&](int64_t t) -> int64_t { return ((t % tiles_mn) % g.n_tiles) * BN; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&conv[s], 4);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -243,6 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync();  // every CTA's barriers exist before any multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -260,10 +299,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-        const int64_t mn = t % tiles_mn;
-        const int m0 = static_cast<int>((mn / g.n_tiles) * BM);
-        const int n0 = static_cast<int>((mn % g.n_tiles) * BN);
+      for (int64_t t = cid; t < total; t += ncl) {
+        const int m0 = static_cast<int>(tile_m0(t));
+        const int n0 = static_cast<int>(tile_n0(t));
         int64_t k0;
         const int nkb = tile_kblocks(t, k0);
         for (int kb = 0; kb < nkb; ++kb) {
@@ -279,23 +317,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {  // box {32 (k), 128 (m)}
             tma_load_2d(sa, &tmA, &full[stage], kk, m0);
           }
-          if (B_MN) {
+          // B (and its presplit lo half): this CTA's 1/CL share, multicast
+          auto load_b = [&](unsigned char *dst, const CUtensorMap *map) {
+            if (B_MN) {  // BN/32 boxes {32 (n), 32 (k)}: box c from CTA c % CL
 #pragma unroll
-            for (int c = 0; c < BN / 32; ++c) tma_load_2d(sb + c * 4096, &tmB, &full[stage],
-                                                          n0 + 32 * c, kk);
-          } else {
-            tma_load_2d(sb, &tmB, &full[stage], kk, n0);
-          }
-          if (g.b_presplit) {  // B's lo half straight into its slot (raw B is the hi half)
-            unsigned char *sbl = sb + C::B_BYTES;
-            if (B_MN) {
-#pragma unroll
-              for (int c = 0; c < BN / 32; ++c) tma_load_2d(sbl + c * 4096, &tmBl, &full[stage],
-                                                            n0 + 32 * c, kk);
-            } else {
-              tma_load_2d(sbl, &tmBl, &full[stage], kk, n0);
+              for (int c = 0; c < BN / 32; ++c) {
+                if (CL == 1) tma_load_2d(dst + c * 4096, map, &full[stage], n0 + 32 * c, kk);
+                else if (c % CL == rank)
+                  tma_load_2d_mc(dst + c * 4096, map, &full[stage], n0 + 32 * c, kk, kAll);
+              }
+            } else {  // box {32 (k), BN / CL rows}: rows of 128 B, 8-row swizzle atoms
+              constexpr int R = BN / CL;
+              if (CL == 1) tma_load_2d(dst, map, &full[stage], kk, n0);
+              else tma_load_2d_mc(dst + rank * R * 128, map, &full[stage], kk, n0 + rank * R, kAll);
             }
-          }
+          };
+          load_b(sb, &tmB);
+          if (g.b_presplit) load_b(sb + C::B_BYTES, &tmBl);  // raw B is the hi half
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -307,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int64_t t = cid; t < total; t += ncl) {
       int64_t k0;
       const int nkb = tile_kblocks(t, k0);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -336,11 +374,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t dbh = smem_desc(b_hi + bo, blbo, bsbo, B_MN);
             const uint64_t dbl = smem_desc(b_lo + bo, blbo, bsbo, B_MN);
             const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
-            tc_mma_tf32(dc, dal, dbh, idesc, first);
-            tc_mma_tf32(dc, dah, dbl, idesc, 1u);
+            if (!(g.exp & 2)) {
+              tc_mma_tf32(dc, dal, dbh, idesc, first);
+              tc_mma_tf32(dc, dah, dbl, idesc, 1u);
+            }
             tc_mma_tf32(d, dah, dbh, idesc, ONE ? 1u : first);
           }
-          tc_commit(&empty[stage]);
+          if (CL == 1) tc_commit(&empty[stage]);
+          else tc_commit_mc(&empty[stage], kAll);  // the stage is free in every CTA's view
           if (kb == nkb - 1) tc_commit(&tfull[acc]);
         }
         __syncwarp();
@@ -355,13 +396,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int t_id = threadIdx.x - kConvWarp0 * 32;
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int64_t t = cid; t < total; t += ncl) {
       int64_t k0;
       const int nkb = tile_kblocks(t, k0);
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[stage], phase);
         unsigned char *st = smem + stage * C::STAGE;
-        if (g.b_presplit) {
+        if (g.exp & 1) {
+        } else if (g.b_presplit) {
           split_tile<true>(reinterpret_cast<float4 *>(st),
                            reinterpret_cast<float4 *>(st + C::A_BYTES), C::A_BYTES / 16, t_id, 128);
         } else if (g.raw_hi) {
@@ -388,11 +430,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int64_t t = cid; t < total; t += ncl) {
       const int64_t s = t / tiles_mn;
-      const int64_t mn = t % tiles_mn;
-      const int64_t m0 = (mn / g.n_tiles) * BM;
-      const int64_t n0 = (mn % g.n_tiles) * BN;
+      const int64_t m0 = tile_m0(t);
+      const int64_t n0 = tile_n0(t);
       const int64_t row = m0 + q * 32 + lane;
       if (g.mask != nullptr && g.splits == 1 && row < g.M && (g.ldm % 4) == 0) {
         // pull this row's mask segment into L2 while the tile's MMAs run
@@ -453,7 +494,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
-          if (vec_ok && nb + 16 <= g.N) {
+          if (g.exp & 4) {
+          } else if (vec_ok && nb + 16 <= g.N) {
 #pragma unroll
             for (int i = 0; i < 16; i += 4)
               *reinterpret_cast<float4 *>(crow + nb + i) =
@@ -474,6 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync();  // no CTA leaves while a peer may still signal / write it
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -538,33 +581,57 @@ int make_map(CUtensorMap *m, const float *base, int64_t inner, int64_t outer, in
   return AG_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool ONE>
+template <int BN, bool A_MN, bool B_MN, bool ONE, int CL>
 int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbl, TcArgs g,
               cudaStream_t st) {
   using C = Cfg<BN, ONE>;
-  auto k = tc_gemm_kernel<BN, A_MN, B_MN, ONE>;
+  auto k = tc_gemm_kernel<BN, A_MN, B_MN, ONE, CL>;
   AG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-  const int64_t total = static_cast<int64_t>(g.m_tiles) * g.n_tiles * g.splits;
-  const int grid = static_cast<int>(std::min<int64_t>(total, sm_count()));
-  k<<<grid, kThreads, C::SMEM, st>>>(ma, mb, mbl, g);
+  const int64_t msup = (g.m_tiles + CL - 1) / CL;
+  const int64_t total = msup * g.n_tiles * g.splits;
+  const int grid = static_cast<int>(std::min<int64_t>(total, sm_count() / CL)) * CL;
+  if (CL == 1) {
+    k<<<grid, kThreads, C::SMEM, st>>>(ma, mb, mbl, g);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    AG_CUDA(cudaLaunchKernelEx(&cfg, k, ma, mb, mbl, g));
+  }
   AG_LAUNCH_CHECK("tc_gemm_kernel");
   return AG_OK;
 }
 
-template <int BN, bool ONE>
+template <int BN, bool ONE, int CL>
 int launch_bn1(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &mb,
                const CUtensorMap &mbl, const TcArgs &g, cudaStream_t st) {
-  if (!a_mn && b_mn) return launch_tc<BN, false, true, ONE>(ma, mb, mbl, g, st);
-  if (!a_mn && !b_mn) return launch_tc<BN, false, false, ONE>(ma, mb, mbl, g, st);
-  if (a_mn && b_mn) return launch_tc<BN, true, true, ONE>(ma, mb, mbl, g, st);
-  return launch_tc<BN, true, false, ONE>(ma, mb, mbl, g, st);
+  if (!a_mn && b_mn) return launch_tc<BN, false, true, ONE, CL>(ma, mb, mbl, g, st);
+  if (!a_mn && !b_mn) return launch_tc<BN, false, false, ONE, CL>(ma, mb, mbl, g, st);
+  if (a_mn && b_mn) return launch_tc<BN, true, true, ONE, CL>(ma, mb, mbl, g, st);
+  return launch_tc<BN, true, false, ONE, CL>(ma, mb, mbl, g, st);
 }
 template <int BN>
 int launch_bn(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &mb,
-              const CUtensorMap &mbl, const TcArgs &g, cudaStream_t st) {
+              const CUtensorMap &mbl, const TcArgs &g, int cl, cudaStream_t st) {
   const char *e = std::getenv("AG_TC_ONEACC");
-  if (e && std::atoi(e)) return launch_bn1<BN, true>(a_mn, b_mn, ma, mb, mbl, g, st);
-  return launch_bn1<BN, false>(a_mn, b_mn, ma, mb, mbl, g, st);
+  const bool one = e && std::atoi(e);
+  if constexpr (BN >= 64) {
+    if (cl == 2) {
+      return one ? launch_bn1<BN, true, 2>(a_mn, b_mn, ma, mb, mbl, g, st)
+                 : launch_bn1<BN, false, 2>(a_mn, b_mn, ma, mb, mbl, g, st);
+    }
+  }
+  return one ? launch_bn1<BN, true, 1>(a_mn, b_mn, ma, mb, mbl, g, st)
+             : launch_bn1<BN, false, 1>(a_mn, b_mn, ma, mb, mbl, g, st);
 }
 
 __global__ void tf32_split_lo_kernel(int64_t n, const float *src, float *lo) {
@@ -618,6 +685,7 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   g.mask = mask;
   g.ldm = ldm;
   g.b_presplit = B_lo != nullptr;
+  if (const char *e = std::getenv("AG_TC_EXP")) g.exp = std::atoi(e);
   {
     const char *rh = std::getenv("AG_TC_RAWHI");
     g.raw_hi = rh ? std::atoi(rh) : 0;
@@ -635,6 +703,10 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   g.k_per_split = kb_per * BK;
   splits = static_cast<int>((kblocks + kb_per - 1) / kb_per);
   g.splits = splits;
+  // clusters of 2 CTAs share (multicast) every B k-block
+  // (not for the M-major, split-K dW products: measured slower there)
+  int cl = (bn >= 64 && g.m_tiles >= 2 && !a_mn) ? 2 : 1;
+  if (const char *e = std::getenv("AG_TC_CL")) cl = std::atoi(e) == 2 && bn >= 64 ? 2 : 1;
   CUtensorMap ma, mb;
   int rc;
   // A: K-major [M][K] (inner K) or M-major [K][M] (inner M)
@@ -642,12 +714,12 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   else rc = make_map(&ma, A, K, M, lda, BM, false);
   if (rc) return rc;
   if (b_mn) rc = make_map(&mb, B, N, K, ldb, 32, true);
-  else rc = make_map(&mb, B, K, N, ldb, bn, false);
+  else rc = make_map(&mb, B, K, N, ldb, bn / cl, false);
   if (rc) return rc;
   CUtensorMap mbl = mb;
   if (B_lo) {
     if (b_mn) rc = make_map(&mbl, B_lo, N, K, ldb, 32, true);
-    else rc = make_map(&mbl, B_lo, K, N, ldb, bn, false);
+    else rc = make_map(&mbl, B_lo, K, N, ldb, bn / cl, false);
     if (rc) return rc;
   }
   Scratch ws;
@@ -660,10 +732,10 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
     g.ldc = ldc;
   }
   switch (bn) {
-    case 32: rc = launch_bn<32>(a_mn, b_mn, ma, mb, mbl, g, st); break;
-    case 64: rc = launch_bn<64>(a_mn, b_mn, ma, mb, mbl, g, st); break;
-    case 128: rc = launch_bn<128>(a_mn, b_mn, ma, mb, mbl, g, st); break;
-    default: rc = launch_bn<256>(a_mn, b_mn, ma, mb, mbl, g, st); break;
+    case 32: rc = launch_bn<32>(a_mn, b_mn, ma, mb, mbl, g, cl, st); break;
+    case 64: rc = launch_bn<64>(a_mn, b_mn, ma, mb, mbl, g, cl, st); break;
+    case 128: rc = launch_bn<128>(a_mn, b_mn, ma, mb, mbl, g, cl, st); break;
+    default: rc = launch_bn<256>(a_mn, b_mn, ma, mb, mbl, g, cl, st); break;
   }
   if (rc) return rc;
   if (splits > 1) {

@@ -124,6 +124,14 @@ def main():
             res[f"gemm_fwd100_bn{bn}"] = timeit(lambda: K.gemm(x100, w100))
         os.environ.pop("AG_TC_BN")
         del q48, mk, x100
+        os.environ["AG_TC_EXP"] = "7"
+        res["gemm_Fx256_exp7"] = timeit(lambda: K.gemm(x, w))
+        os.environ.pop("AG_TC_EXP")
+        os.environ["AG_TC_CL"] = "1"
+        res["gemm_Fx256_cl1"] = timeit(lambda: K.gemm(x, w))
+        res["gemm_dW_cl1"] = timeit(lambda: K.gemm(x, g256, trans_a=True))
+        res["gemm_dH_cl1"] = timeit(lambda: K.gemm(g256, w, trans_b=True))
+        os.environ.pop("AG_TC_CL")
         ref64 = x.double() @ w.double()
         def relerr(t):
             return float(((t.double() - ref64).abs() / ref64.abs().clamp(min=1.0)).max())
