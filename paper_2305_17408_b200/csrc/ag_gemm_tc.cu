@@ -41,7 +41,14 @@ namespace ag {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BK = 32;  // fp32 elements per k-block: one 128-byte swizzle row
+// fp32 elements per k-block: one 128-byte swizzle row (SWIZZLE_128B).  BK = 16
+// (SWIZZLE_64B, 4 stages of 48 KB) also works and was measured: no faster for
+// K = 256 and slower for short K (twice the per-k-block barrier round trips).
+constexpr int BK = 32;
+constexpr int kKRow = BK * 4;                       // bytes per K-major row
+constexpr uint64_t kKLayout = BK == 32 ? 2ull : 4ull;  // SWIZZLE_128B / SWIZZLE_64B
+constexpr uint32_t kKSbo = 8 * kKRow;               // 8-row swizzle atom
+constexpr uint32_t kMnBox = 128 * BK;               // MN-major TMA box {32 mn, BK k} bytes
 constexpr int kThreads = 320;
 constexpr int kConvWarp0 = 2, kEpiWarp0 = 6;
 
@@ -172,7 +179,7 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
   return (static_cast<uint64_t>((addr >> 4) & 0x3FFFu)) |
          (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) |
-         ((mn ? 1ull : 2ull) << 61);
+         ((mn ? 1ull : kKLayout) << 61);
 }
 
 // Instruction descriptor: D f32, A/B tf32, majors, N, M = 128.
@@ -187,7 +194,8 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;   // 16 KB
   static constexpr int B_BYTES = BN * BK * 4;   // BN * 128 B
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int STAGES = STAGE * 3 <= 200 * 1024 ? 3 : 2;
+  static constexpr int STAGES =
+      STAGE * 4 <= 200 * 1024 ? 4 : STAGE * 3 <= 200 * 1024 ? 3 : 2;
   // two fp32 accumulators per tile (hi*hi and the hi*lo + lo*hi correction),
   // double-buffered when TMEM allows
   // ONE: the correction and hi*hi products share one accumulator (half the
@@ -312,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int kk = static_cast<int>(k0 + static_cast<int64_t>(kb) * BK);
           if (A_MN) {  // boxes {32 (m), 32 (k)}: 4 KB each, LBO apart
 #pragma unroll
-            for (int c = 0; c < BM / 32; ++c) tma_load_2d(sa + c * 4096, &tmA, &full[stage],
+            for (int c = 0; c < BM / 32; ++c) tma_load_2d(sa + c * kMnBox, &tmA, &full[stage],
                                                           m0 + 32 * c, kk);
           } else {  // box {32 (k), 128 (m)}
             tma_load_2d(sa, &tmA, &full[stage], kk, m0);
@@ -322,14 +330,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (B_MN) {  // BN/32 boxes {32 (n), 32 (k)}: box c from CTA c % CL
 #pragma unroll
               for (int c = 0; c < BN / 32; ++c) {
-                if (CL == 1) tma_load_2d(dst + c * 4096, map, &full[stage], n0 + 32 * c, kk);
+                if (CL == 1) tma_load_2d(dst + c * kMnBox, map, &full[stage], n0 + 32 * c, kk);
                 else if (c % CL == rank)
-                  tma_load_2d_mc(dst + c * 4096, map, &full[stage], n0 + 32 * c, kk, kAll);
+                  tma_load_2d_mc(dst + c * kMnBox, map, &full[stage], n0 + 32 * c, kk, kAll);
               }
             } else {  // box {32 (k), BN / CL rows}: rows of 128 B, 8-row swizzle atoms
               constexpr int R = BN / CL;
               if (CL == 1) tma_load_2d(dst, map, &full[stage], kk, n0);
-              else tma_load_2d_mc(dst + rank * R * 128, map, &full[stage], kk, n0 + rank * R, kAll);
+              else tma_load_2d_mc(dst + rank * R * kKRow, map, &full[stage], kk, n0 + rank * R,
+                                  kAll);
             }
           };
           load_b(sb, &tmB);
@@ -367,8 +376,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t bo = B_MN ? ks * 1024 : ks * 32;
             // MN-major: LBO = next 32-element MN chunk (one 4 KB TMA box),
             // SBO = next 4-row K atom (512 B); K-major: SBO = next 8-row group
-            const uint32_t albo = A_MN ? 4096 : 16, asbo = A_MN ? 512 : 1024;
-            const uint32_t blbo = B_MN ? 4096 : 16, bsbo = B_MN ? 512 : 1024;
+            const uint32_t albo = A_MN ? kMnBox : 16, asbo = A_MN ? 512 : kKSbo;
+            const uint32_t blbo = B_MN ? kMnBox : 16, bsbo = B_MN ? 512 : kKSbo;
             const uint64_t dah = smem_desc(a_hi + ao, albo, asbo, A_MN);
             const uint64_t dal = smem_desc(a_lo + ao, albo, asbo, A_MN);
             const uint64_t dbh = smem_desc(b_hi + bo, blbo, bsbo, B_MN);
@@ -571,11 +580,13 @@ int make_map(CUtensorMap *m, const float *base, int64_t inner, int64_t outer, in
   if (!enc) return fail(AG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
-  cuuint32_t box[2] = {32, static_cast<cuuint32_t>(box_outer)};
+  // MN-major: box {32 (mn), BK (k)}; K-major: box {BK (k), box_outer rows}
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(mn ? 32 : BK), static_cast<cuuint32_t>(box_outer)};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims,
                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                      : (BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B),
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(AG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return AG_OK;
@@ -710,15 +721,15 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   CUtensorMap ma, mb;
   int rc;
   // A: K-major [M][K] (inner K) or M-major [K][M] (inner M)
-  if (a_mn) rc = make_map(&ma, A, M, K, lda, 32, true);
+  if (a_mn) rc = make_map(&ma, A, M, K, lda, BK, true);
   else rc = make_map(&ma, A, K, M, lda, BM, false);
   if (rc) return rc;
-  if (b_mn) rc = make_map(&mb, B, N, K, ldb, 32, true);
+  if (b_mn) rc = make_map(&mb, B, N, K, ldb, BK, true);
   else rc = make_map(&mb, B, K, N, ldb, bn / cl, false);
   if (rc) return rc;
   CUtensorMap mbl = mb;
   if (B_lo) {
-    if (b_mn) rc = make_map(&mbl, B_lo, N, K, ldb, 32, true);
+    if (b_mn) rc = make_map(&mbl, B_lo, N, K, ldb, BK, true);
     else rc = make_map(&mbl, B_lo, K, N, ldb, bn / cl, false);
     if (rc) return rc;
   }
