@@ -212,12 +212,19 @@ int ag_role_csr_build(int64_t num_rows, const int32_t *row_ptr,
  * sources (bulk copies), and 14 consumer warps take the range's rows
  * round-robin, reducing out of shared memory.  `window` only affects speed,
  * never values (ag_slab_window picks it per graph).  Any F (TMA when
- * F % 4 == 0 and x is 16-byte aligned, cp.async otherwise). */
+ * F % 4 == 0 and x is 16-byte aligned, cp.async otherwise).
+ * blk_w (NULL: bitwise intra role): the pair (dense_block, csr_inter) of the
+ * reference's selector in one pass -- the intra role of every 16-row block as
+ * a dense 16 x 16 block product (ag_slab_dense_blocks; the reference's
+ * dense_block kernel, kernels.py:228-250, order-unpinned like its BLAS
+ * matmul) computed once per block by a dedicated warp, the inter role bitwise;
+ * needs role_mask 3, op sum and the B = 16 role-ordered layout. */
 int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                   const int32_t *row_ptr, const int32_t *role_mid,
                   const int32_t *cv, const int32_t *rowinfo,
                   const int32_t *far_cnt, const int32_t *far_src,
-                  int32_t weighted, int64_t num_edges, const float *x, float *y,
+                  int32_t weighted, const float *blk_w, int64_t num_edges,
+                  const float *x, float *y,
                   int32_t op, int32_t epi_flags, const uint8_t *other_touched,
                   const int64_t *deg, float gin_scale, const float *relu_src,
                   int64_t x_rows, int32_t window, void *stream);
@@ -247,6 +254,13 @@ int ag_slab_codes(int64_t num_rows, const int32_t *row_ptr,
                   const int32_t *role_mid, int32_t window, int32_t *cv,
                   int32_t *rowinfo, int32_t *far_cnt, int32_t *far_src,
                   void *stream);
+/* Dense 16 x 16 intra weights per 16-row block for ag_fused_spmm's blk_w:
+ * blk_w[b][i][j] = weight of edge (16b + i <- 16b + j) from the role-ordered
+ * CSR's intra runs [row_ptr[r], role_mid[r]) (role_val NULL: 1.0), zeros
+ * elsewhere.  blk_w: float[ceil(num_rows / 16) * 256]. */
+int ag_slab_dense_blocks(int64_t num_rows, const int32_t *row_ptr,
+                         const int32_t *role_mid, const int32_t *role_col,
+                         const float *role_val, float *blk_w, void *stream);
 /* Staged far sources per 16-row block (the far-ring capacity). */
 int ag_slab_far_capacity(void);
 

@@ -61,10 +61,11 @@ constexpr int kRB = 16;      // rows per ring block
 constexpr int kCons = 14;    // consumer warps; + 2 producer warps = 16 (4 per SMSP, 128 regs)
 constexpr int kThreads = (kCons + 2) * 32;
 constexpr int kWin = 64;     // topology items per window refill (two per lane)
-constexpr int kSlots = 42;   // X ring capacity in blocks (window H <= (kSlots - 9) / 2 = 16)
-constexpr int kFarSlots = 6; // far ring: staged out-of-window sources of the next blocks
+constexpr int kSlots = 41;   // X ring capacity in blocks (window H <= (kSlots - 9) / 2 = 16)
+constexpr int kFarSlots = 4; // far ring: staged out-of-window sources of the next blocks
 constexpr int kFarMax = 20;  // staged far sources per block (more: read from global)
 constexpr int kReluSlots = 4;  // ReLU-mask operand tiles staged ahead (backward epilogue)
+constexpr int kISlots = 4;   // dense-intra mode: per-block intra results (16 rows x tile)
 constexpr int kReady = 16;   // per-block "ready" barriers (X window + far rows staged)
 constexpr int kDone = 32;    // per-block "done" barriers (every consumer left the block)
 constexpr int kRowSlow = 1;  // rowinfo flag: row has global sources or > kWin pairs
@@ -84,6 +85,7 @@ struct GArgs {
   int weighted;             // 0: every weight is 1.0 (multiplies skipped: exact)
   int has_mid;              // rowinfo.y is the intra-run end (role-ordered layout)
   int relu;                 // AG_EPI_RELU_MASK: relu_src tiles are staged by the far producer
+  const float *blk_w;       // dense-intra mode: [nblocks][16][16] intra weights (dst, src)
   const float *x;
   float *y;
   Epi ep;
@@ -551,16 +553,22 @@ __device__ __forceinline__ Vf<VEC> combine2(int op, const Vf<VEC> &I, bool ti, c
 constexpr int kModeSum3 = 0;   // role_mask 3, op sum (flags: GIN / RELU_MASK only)
 constexpr int kModeAny = 1;    // any role mask, sum or mean, any flags
 constexpr int kModeMax = 2;    // any role mask, max
+// role mask 3, op sum, the intra role as a dense 16 x 16 block product (the
+// reference's dense_block kernel, order-unpinned like its BLAS matmul) computed
+// once per block by a dedicated warp; the inter role stays bitwise csr_inter
+constexpr int kModeDense3 = 3;
 
 // One destination row (both roles, epilogue) for this lane's columns.
 template <int VEC, int MODE, bool W>
 __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64_t r, int32_t s,
                                        int32_t e, int32_t m, float *yrow, bool act, bool fast,
-                                       uint32_t relu_s) {
+                                       uint32_t relu_s, uint32_t intra_s) {
   constexpr bool IS_MAX = MODE == kModeMax;
+  constexpr bool SUM3 = MODE == kModeSum3 || MODE == kModeDense3;
   const int64_t ld = a.feat;
-  const int32_t ni = (MODE == kModeSum3 || (a.mask & 1)) ? m - s : 0;
-  const int32_t no = (MODE == kModeSum3 || (a.mask & 2)) ? e - m : 0;
+  // dense-intra mode: the intra role comes from the dense warp's block product
+  const int32_t ni = MODE == kModeDense3 ? 0 : (SUM3 || (a.mask & 1)) ? m - s : 0;
+  const int32_t no = (SUM3 || (a.mask & 2)) ? e - m : 0;
   // the ReLU-mask operand is loaded before the reduction so its latency hides
   // behind it
   const bool relu = a.relu && act;
@@ -578,7 +586,9 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
   if (!act) return;
   float *yp = yrow;
   Vf<VEC> out;
-  if constexpr (MODE == kModeSum3) {
+  if constexpr (MODE == kModeDense3) {
+    out = vadd<VEC>(lv_out<VEC>(lv_lds<VEC>(intra_s)), O);
+  } else if constexpr (MODE == kModeSum3) {
     out = vadd<VEC>(I, O);
   } else if (a.mask == 3) {
     const int64_t d = (a.ep.op == AG_OP_MEAN && a.ep.deg) ? a.ep.deg[r] : 1;
@@ -621,8 +631,10 @@ struct SlabGeom {
   static constexpr uint32_t kSlotBytes = kRB * kRowBytes;
   static constexpr uint32_t kFarSlotBytes = kFarMax * kRowBytes;
   static constexpr uint32_t kReluOff = kSlots * kSlotBytes + kFarSlots * kFarSlotBytes;
-  static constexpr uint32_t kRingBytes = kReluOff + kReluSlots * kSlotBytes;
-  static constexpr uint32_t kBarBytes = (kReady + kDone) * 8;
+  static constexpr uint32_t kIOff = kReluOff + kReluSlots * kSlotBytes;
+  static constexpr uint32_t kWOff = kIOff + kISlots * kSlotBytes;  // 2 x 1 KB block weights
+  static constexpr uint32_t kRingBytes = kWOff + 2 * 1024;
+  static constexpr uint32_t kBarBytes = (kReady + kDone + kISlots) * 8;
   static constexpr uint32_t kWinBytes = kCons * kWin * 8;
   static constexpr size_t kSmem = kRingBytes + kBarBytes + kWinBytes;
 };
@@ -853,6 +865,84 @@ __device__ __forceinline__ void produce_far(const GArgs &a, const CUtensorMap *r
   }
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+// Dense-intra warp (kModeDense3): for every block f in [kb0, kb1), the 16 x 16
+// intra weight block (cp.async, one block ahead) times the block's 16 X rows
+// (already in the ring) -> the 16 intra partials of this column tile, into
+// I-slot f % kISlots for the consumers' epilogues.  Register-blocked: each X
+// row is read from shared memory once per block instead of once per edge.
+constexpr int kDenseWarps = 2;  // each takes 16 / kDenseWarps rows of every block (measured: 2 > 1, 4)
+
+template <int VEC>
+__device__ __forceinline__ void dense_intra(const GArgs &a, uint32_t ring, const BlockSync &bs,
+                                            uint32_t ivalid, uint32_t kb0, uint32_t kb1,
+                                            int lane, int half) {
+  using G = SlabGeom<VEC>;
+  const uint32_t wbuf = ring + G::kWOff;
+  auto fetch_w = [&](uint32_t f, int buf) {  // 1 KB: 32 bytes per lane
+    if (f < kb1) {
+      const float *src = a.blk_w + static_cast<int64_t>(f) * 256 + lane * 8;
+      cp_async16(wbuf + buf * 1024 + lane * 32, src);
+      cp_async16(wbuf + buf * 1024 + lane * 32 + 16, src + 4);
+    }
+    cp_async_commit();
+  };
+  fetch_w(kb0, 0);
+#pragma unroll 1
+  for (uint32_t f = kb0; f < kb1; ++f) {
+    const uint32_t fi = f - kb0;
+    const int buf = static_cast<int>(fi & 1u);
+    fetch_w(f + 1, buf ^ 1);
+    cp_async_wait<1>();  // this block's weights have landed
+    __syncwarp();
+    mbar_wait(bs.rdy(f), bs.rdy_phase(f));  // X block f is in the ring
+    if (fi >= kISlots) bs.wait_done(f - kISlots);  // the I slot's previous block is consumed
+    const uint32_t xs = ring + (f % kSlots) * G::kSlotBytes + lane * VEC * 4;
+    Lv<VEC> xr[kRB];
+#pragma unroll
+    for (int j = 0; j < kRB; ++j) xr[j] = lv_lds<VEC>(xs + j * G::kRowBytes);
+    const uint32_t is = ring + G::kIOff + (fi % kISlots) * G::kSlotBytes + lane * VEC * 4;
+    const uint32_t wrow = wbuf + buf * 1024;
+#pragma unroll 2
+    for (int i = half * (kRB / kDenseWarps); i < (half + 1) * (kRB / kDenseWarps); ++i) {
+      float wv[kRB];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(wv[4 * q]), "=f"(wv[4 * q + 1]), "=f"(wv[4 * q + 2]),
+                       "=f"(wv[4 * q + 3])
+                     : "r"(wrow + i * 64 + q * 16));
+      Lv<VEC> acc = lv_scale<VEC>(xr[0], wv[0]);
+#pragma unroll
+      for (int j = 1; j < kRB; ++j) {
+        if constexpr (VEC == 1) {
+          acc.s = __fmaf_rn(xr[j].s, wv[j], acc.s);
+        } else {
+          const uint64_t ww = pk(wv[j], wv[j]);
+#pragma unroll
+          for (int pp = 0; pp < Lv<VEC>::NP; ++pp)
+            asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc.p[pp]) : "l"(xr[j].p[pp]), "l"(ww));
+        }
+      }
+      if constexpr (VEC == 1) {
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(is + i * G::kRowBytes), "f"(acc.s) : "memory");
+      } else {
+        asm volatile("st.shared.b64 [%0], %1;" ::"r"(is + i * G::kRowBytes), "l"(acc.p[0])
+                     : "memory");
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(ivalid + (fi % kISlots) * 8);
+      mbar_arrive(bs.done + (fi % kDone) * 8);
+    }
+  }
+  cp_async_wait<0>();
+}
+
 template <int VEC, int MODE, bool W>
 __global__ void __launch_bounds__(kThreads, 1)
     slab_kernel(const __grid_constant__ CUtensorMap tmap,
@@ -863,7 +953,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t ring = su32(smem);
   const uint32_t ready = ring + G::kRingBytes;
   const uint32_t done = ready + kReady * 8;
-  const uint32_t wins = done + kDone * 8;
+  const uint32_t ivalid = done + kDone * 8;  // dense-intra mode: I slot of block k written
+  const uint32_t wins = ivalid + kISlots * 8;
+  constexpr bool DENSE = MODE == kModeDense3;
+  constexpr int NC = DENSE ? kCons - kDenseWarps : kCons;  // consumer warps (dense warps last)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t H = static_cast<uint32_t>(a.H);
@@ -878,7 +971,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       s_kb[0] = range_block(a, range);
       s_kb[1] = range_block(a, range + 1);
       for (int s = 0; s < kReady; ++s) mbar_init(ready + s * 8, 2);
-      for (int s = 0; s < kDone; ++s) mbar_init(done + s * 8, kCons);
+      for (int s = 0; s < kDone; ++s) mbar_init(done + s * 8, kCons);  // (+ the dense warp)
+      for (int s = 0; s < kISlots; ++s) mbar_init(ivalid + s * 8, kDenseWarps);
       fence_mbar_init();
     }
     __syncthreads();
@@ -891,6 +985,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         produce_x<VEC>(a, &tmap, ring, bs, Llo, Lhi, kb0, kb1, H, tile, lane);
       } else if (warp == kCons + 1) {
         produce_far<VEC>(a, &relu_map, ring, bs, kb0, kb1, tile, lane);
+      } else if (DENSE && warp >= kCons - kDenseWarps) {
+        dense_intra<VEC>(a, ring, bs, ivalid, kb0, kb1, lane, warp - (kCons - kDenseWarps));
       } else {
         RowWarp<VEC, W> w;
         const int64_t fcol = static_cast<int64_t>(tile) * G::T + lane * VEC;
@@ -922,32 +1018,41 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t rr = r0 + warp;
         int4 info = info_at(rr);
         int2 q0 = pairs_at(info, 0), q1 = pairs_at(info, 1);
-        int4 info1 = info_at(rr + kCons);
+        int4 info1 = info_at(rr + NC);
         uint32_t kcur = kb0;
-        mbar_wait(bs.rdy(kb0), 0);
+        // entering block k: its X window and far rows (ready), and in
+        // dense-intra mode its intra partials
+        auto enter = [&](uint32_t k) {
+          mbar_wait(bs.rdy(k), bs.rdy_phase(k));
+          if (DENSE) mbar_wait(ivalid + ((k - kb0) % kISlots) * 8, ((k - kb0) / kISlots) & 1u);
+        };
+        enter(kb0);
 #pragma unroll 1
-        for (; rr < r1; rr += kCons) {
+        for (; rr < r1; rr += NC) {
           const uint32_t k = rr / kRB;
           while (kcur != k) {  // leave block kcur, enter the next
             __syncwarp();
             if (lane == 0) mbar_arrive(done + ((kcur - kb0) % kDone) * 8);
             ++kcur;
-            mbar_wait(bs.rdy(kcur), bs.rdy_phase(kcur));
+            enter(kcur);
           }
           const int32_t s = info.x, e = info.z;
-          const int32_t m = (MODE == kModeSum3 || a.has_mid) ? info.y : (a.mask == 1 ? e : s);
+          const int32_t m =
+              (MODE == kModeSum3 || DENSE || a.has_mid) ? info.y : (a.mask == 1 ? e : s);
           const bool fast = !(info.w & kRowSlow);
           w.end = e;
           if (fast) w.template install<true>(s, q0, q1);
           else w.template install<false>(s, q0, q1);
           // next row's pairs and the row after next's bounds
           const int2 n0 = pairs_at(info1, 0), n1 = pairs_at(info1, 1);
-          const int4 info2 = info_at(rr + 2 * kCons);
+          const int4 info2 = info_at(rr + 2 * NC);
           float *yrow;  // ylane + rr * ld as one IMAD.WIDE.U32
           asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(yrow) : "r"(rr), "r"(ld * 4u), "l"(ylane));
           const uint32_t relu_s = ring + G::kReluOff + ((k - kb0) % kReluSlots) * G::kSlotBytes +
                                   (rr % kRB) * G::kRowBytes + lane * VEC * 4;
-          do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, relu_s);
+          const uint32_t intra_s = ring + G::kIOff + ((k - kb0) % kISlots) * G::kSlotBytes +
+                                   (rr % kRB) * G::kRowBytes + lane * VEC * 4;
+          do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, relu_s, intra_s);
           info = info1;
           info1 = info2;
           q0 = n0;
@@ -957,7 +1062,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(done + ((kcur - kb0) % kDone) * 8);
           if (++kcur >= kb1) break;
-          mbar_wait(bs.rdy(kcur), bs.rdy_phase(kcur));
+          enter(kcur);
         }
       }
     }
@@ -965,6 +1070,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
       for (int s = 0; s < kReady; ++s) mbar_inval(ready + s * 8);
       for (int s = 0; s < kDone; ++s) mbar_inval(done + s * 8);
+      for (int s = 0; s < kISlots; ++s) mbar_inval(ivalid + s * 8);
     }
     __syncthreads();
   }
@@ -1007,6 +1113,8 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
   const bool wt = a.weighted != 0;
   auto k = mode == kModeMax
                ? (wt ? slab_kernel<VEC, kModeMax, true> : slab_kernel<VEC, kModeMax, false>)
+           : mode == kModeDense3
+               ? (wt ? slab_kernel<VEC, kModeDense3, true> : slab_kernel<VEC, kModeDense3, false>)
            : mode == kModeSum3
                ? (wt ? slab_kernel<VEC, kModeSum3, true> : slab_kernel<VEC, kModeSum3, false>)
                : (wt ? slab_kernel<VEC, kModeAny, true> : slab_kernel<VEC, kModeAny, false>);
@@ -1123,12 +1231,43 @@ __global__ void slab_code_kernel(int64_t rows, const int32_t *row_ptr, const int
   }
 }
 
+// The intra run of each row of a 16-row block as a dense 16 x 16 matrix
+// (row = destination within the block, column = source within it; the
+// reference's to_dense_blocks layout, formats.py:118-140), one thread per block.
+__global__ void dense_block_weights_kernel(int64_t rows, const int32_t *row_ptr,
+                                           const int32_t *mid, const int32_t *col,
+                                           const float *val, float *blk_w) {
+  const int64_t nb = (rows + kRB - 1) / kRB;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    float *w = blk_w + b * kRB * kRB;
+    for (int i = 0; i < kRB * kRB; ++i) w[i] = 0.0f;
+    const int64_t r1 = std::min<int64_t>(b * kRB + kRB, rows);
+    for (int64_t r = b * kRB; r < r1; ++r)
+      for (int32_t e = row_ptr[r]; e < mid[r]; ++e)
+        w[(r - b * kRB) * kRB + (col[e] - b * kRB)] = val ? val[e] : 1.0f;
+  }
+}
+
 }  // namespace
 }  // namespace ag
 
 using namespace ag;
 
 extern "C" int ag_slab_far_capacity(void) { return kFarMax; }
+
+extern "C" int ag_slab_dense_blocks(int64_t num_rows, const int32_t *row_ptr,
+                                    const int32_t *role_mid, const int32_t *role_col,
+                                    const float *role_val, float *blk_w, void *stream) {
+  if (num_rows < 0) return fail(AG_ERR_VALUE, "negative sizes");
+  if (role_mid == nullptr) return fail(AG_ERR_VALUE, "role_mid (block size 16) is required");
+  if (num_rows == 0) return AG_OK;
+  const int64_t nb = (num_rows + kRB - 1) / kRB;
+  dense_block_weights_kernel<<<grid_for(nb, 128), 128, 0, as_stream(stream)>>>(
+      num_rows, row_ptr, role_mid, role_col, role_val, blk_w);
+  AG_LAUNCH_CHECK("dense_block_weights_kernel");
+  return AG_OK;
+}
 
 extern "C" int ag_slab_codes(int64_t num_rows, const int32_t *row_ptr, const int32_t *col_idx,
                              const float *val, const int32_t *role_mid, int32_t window,
@@ -1197,7 +1336,7 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                              const int32_t *row_ptr, const int32_t *role_mid,
                              const int32_t *cv, const int32_t *rowinfo,
                              const int32_t *far_cnt, const int32_t *far_src, int32_t weighted,
-                             int64_t num_edges,
+                             const float *blk_w, int64_t num_edges,
                              const float *x, float *y, int32_t op, int32_t epi_flags,
                              const uint8_t *other_touched, const int64_t *deg, float gin_scale,
                              const float *relu_src, int64_t x_rows, int32_t window,
@@ -1235,6 +1374,11 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
     return fail(AG_ERR_VALUE, "cv must be 8-byte and rowinfo 16-byte aligned");
   a.weighted = weighted != 0;
   a.has_mid = role_mid != nullptr;
+  a.blk_w = blk_w;
+  if (blk_w != nullptr &&
+      (role_mask != 3 || op != AG_OP_SUM || role_mid == nullptr ||
+       (epi_flags & ~(AG_EPI_GIN | AG_EPI_RELU_MASK | AG_EPI_RELU)) != 0))
+    return fail(AG_ERR_VALUE, "dense intra blocks need role_mask 3, op sum and role_mid");
   a.x = x;
   a.y = y;
   a.ep = Epi{op, epi_flags, other_touched, deg, x, feat, gin_scale, relu_src};
@@ -1245,7 +1389,8 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                   (reinterpret_cast<uintptr_t>(y) % 8) == 0 &&
                   (relu_src == nullptr || (reinterpret_cast<uintptr_t>(relu_src) % 8) == 0) &&
                   env_int("AG_SLAB_VEC", 2) == 2;
-  const int mode = is_max ? kModeMax
+  const int mode = blk_w != nullptr ? kModeDense3
+                 : is_max ? kModeMax
                    : (role_mask == 3 && op == AG_OP_SUM &&
                       (epi_flags & ~(AG_EPI_GIN | AG_EPI_RELU_MASK | AG_EPI_RELU)) == 0)
                        ? kModeSum3

@@ -288,7 +288,7 @@ class DistGNN:
             e0.record()
         _lib.call("ag_fused_spmm", op.num_rows, F, 3 if op.mid is not None else 2,
                   _lib.ptr(op.row_ptr), _lib.ptr(op.mid), *map(_lib.ptr, op.codes()),
-                  int(op.val is not None),
+                  int(op.val is not None), None,
                   op.num_edges, _lib.ptr(x_ext), _lib.ptr(out), _lib.AG_OP["sum"], flags, None,
                   _lib.ptr(op.deg), 0.0 if gs is None else gs, _lib.ptr(relu_src), x_ext.shape[0], op.window(),
                   _lib.stream())

@@ -68,7 +68,7 @@ class CsrMatrix:
     """Compressed sparse rows over destination vertices."""
 
     __slots__ = ("num_vertices", "row_ptr", "col_idx", "_val", "_ones", "_rows", "_touched",
-                 "_off_block", "_long", "_window", "_codes")
+                 "_off_block", "_long", "_window", "_codes", "_dense16")
 
     def __init__(self, num_vertices: int, row_ptr: torch.Tensor, col_idx: torch.Tensor,
                  val: torch.Tensor | None, rows: torch.Tensor | None = None):
@@ -80,6 +80,7 @@ class CsrMatrix:
         self._long = None
         self._window = None
         self._codes = {}
+        self._dense16 = None
 
     @property
     def val(self) -> torch.Tensor:
@@ -169,6 +170,18 @@ class CsrMatrix:
             lay = (mid, cv, rowinfo, far_cnt, far_src, int(val is not None))
             self._codes[key] = lay
         return lay
+
+    def dense_blocks16(self) -> torch.Tensor:
+        """The intra runs of the B = 16 role layout as dense 16 x 16 blocks
+        (ag_slab_dense_blocks), cached: the dense-intra fused pair's operand."""
+        if self._dense16 is None:
+            mid, col, val = self.role_layout(16)
+            nb = (self.num_vertices + 15) // 16
+            w = torch.empty(max(nb, 1) * 256, dtype=torch.float32, device=self.row_ptr.device)
+            _lib.call("ag_slab_dense_blocks", self.num_vertices, _lib.ptr(self.row_ptr),
+                      _lib.ptr(mid), _lib.ptr(col), _lib.ptr(val), _lib.ptr(w), _lib.stream())
+            self._dense16 = w
+        return self._dense16
 
     def rows(self) -> torch.Tensor:
         """Destination of every edge (the COO row array)."""

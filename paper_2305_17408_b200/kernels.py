@@ -95,7 +95,8 @@ def launch_csr(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp, 
 def launch_fused(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp,
                  block: int = 0, mask: int = 2, flags: int = 0,
                  other_touched: torch.Tensor | None = None, deg: torch.Tensor | None = None,
-                 gin_scale: float = 0.0, relu_src: torch.Tensor | None = None) -> None:
+                 gin_scale: float = 0.0, relu_src: torch.Tensor | None = None,
+                 dense_intra: bool = False) -> None:
     """ag_fused_spmm: slab (smem X ring) row gather, reduceat-order reduction (+ role split).
 
     block > 0 splits every row into its intra run and inter edges (role-ordered
@@ -104,7 +105,8 @@ def launch_fused(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp
     mid, cv, rowinfo, far_cnt, far_src, weighted = a.slab_layout(block)
     _lib.call("ag_fused_spmm", a.num_vertices, x.shape[1], int(mask), _lib.ptr(a.row_ptr),
               _lib.ptr(mid), _lib.ptr(cv), _lib.ptr(rowinfo), _lib.ptr(far_cnt),
-              _lib.ptr(far_src), weighted, a.num_edges, _lib.ptr(x), _lib.ptr(y),
+              _lib.ptr(far_src), weighted,
+              _lib.ptr(a.dense_blocks16() if dense_intra else None), a.num_edges, _lib.ptr(x), _lib.ptr(y),
               _opcode(op), flags | (_lib.AG_EPI_RELU_MASK if relu_src is not None else 0),
               _lib.ptr(other_touched), _lib.ptr(deg), float(gin_scale), _lib.ptr(relu_src),
               x.shape[0], a.window(), _lib.stream())
@@ -407,21 +409,34 @@ def decomposed_execs(d: DecomposedGraph) -> tuple[SubgraphExec, SubgraphExec]:
 CSR_KINDS = (KernelKind.CSR_INTRA_BLOCKED, KernelKind.CSR_INTER)
 
 
-def fusable(kernel_intra: KernelKind, kernel_inter: KernelKind) -> bool:
-    """A CSR x CSR pair runs as ONE fused launch over the full CSR (same bits)."""
-    return kernel_intra in CSR_KINDS and kernel_inter is KernelKind.CSR_INTER
+def fusable(kernel_intra: KernelKind, kernel_inter: KernelKind, block_size: int = 16) -> bool:
+    """A CSR x CSR pair runs as ONE fused launch over the full CSR (same bits);
+    so does (dense_block, csr_inter) for 16-row blocks (the slab kernel's
+    dense-intra mode)."""
+    if kernel_inter is not KernelKind.CSR_INTER:
+        return False
+    return kernel_intra in CSR_KINDS or (kernel_intra is KernelKind.DENSE_BLOCK
+                                         and block_size == 16)
+
+
+def fused_ok(kernel_intra: KernelKind, kernel_inter: KernelKind, block_size: int,
+             op: AggregateOp) -> bool:
+    """fusable(), restricted to what the fused kernel computes for `op` (the
+    dense-intra mode is sum-only; dense_block rejects max anyway)."""
+    return fusable(kernel_intra, kernel_inter, block_size) and (
+        kernel_intra is not KernelKind.DENSE_BLOCK or op is AggregateOp.SUM)
 
 
 def run_fused_pair(d: DecomposedGraph, x: torch.Tensor, y: torch.Tensor, op: AggregateOp,
                    gin_scale: float | None = None, relu_src: torch.Tensor | None = None,
-                   relu: bool = False) -> None:
+                   relu: bool = False, dense_intra: bool = False) -> None:
     """y = combine(intra, inter) [+ gin] [relu] [* (relu_src > 0)] in one pass
     over the full reordered CSR."""
     full = full_graph(d)
     flags = (_lib.AG_EPI_GIN if gin_scale is not None else 0) | (_lib.AG_EPI_RELU if relu else 0)
     launch_fused(to_csr(full), x, y, op, block=d.block_size, mask=3, flags=flags,
                  deg=d.full_in_degree, gin_scale=0.0 if gin_scale is None else gin_scale,
-                 relu_src=relu_src)
+                 relu_src=relu_src, dense_intra=dense_intra)
 
 
 def aggregate_full(g: Graph, x, op: AggregateOp, kernel: KernelKind = KernelKind.CSR_INTER,
@@ -453,8 +468,9 @@ def aggregate_decomposed(d: DecomposedGraph, x, op: AggregateOp,
     del threads
     x = _check_features(d.num_vertices, x)
     y = torch.empty((d.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
-    if fusable(kernel_intra, kernel_inter):
-        run_fused_pair(d, x, y, op, gin_scale)
+    if fused_ok(kernel_intra, kernel_inter, d.block_size, op):
+        run_fused_pair(d, x, y, op, gin_scale,
+                       dense_intra=kernel_intra is KernelKind.DENSE_BLOCK)
         return y
     intra, inter = decomposed_execs(d)
     inter.run_raw_into(kernel_inter, x, y, op, tile_budget_bytes)

@@ -32,7 +32,7 @@ from .kernels import (
     _check_features,
     aggregate_decomposed,
     aggregate_full,
-    fusable,
+    fused_ok,
     gemm,
     run_fused_pair,
 )
@@ -286,14 +286,18 @@ class GNN:
                 _, s, _ = run_training_loop(subj, x, AggregateOp.SUM, s.total_profiling_iters, s)
                 pair = (s.choice_intra, s.choice_inter)
                 self.selector_choice[(direction, f)] = pair
-                if not fusable(*pair):
-                    fused = (KernelKind.CSR_INTRA_BLOCKED, KernelKind.CSR_INTER)
-                    t_sel = _time_ms(lambda: aggregate_decomposed(
-                        subj, x, AggregateOp.SUM, kernel_intra=pair[0], kernel_inter=pair[1]))
-                    y = torch.empty_like(x)
-                    t_fused = _time_ms(lambda: run_fused_pair(subj, x, y, AggregateOp.SUM))
-                    if t_fused <= t_sel:
-                        pair = fused
+                # what actually runs: the fastest of the selector's pair and the
+                # fused pairs (CSR x CSR bitwise, dense_block x csr_inter)
+                cands = [pair, (KernelKind.CSR_INTRA_BLOCKED, KernelKind.CSR_INTER)]
+                if subj.block_size == 16:
+                    cands.append((KernelKind.DENSE_BLOCK, KernelKind.CSR_INTER))
+                best, best_t = pair, None
+                for cand in dict.fromkeys(cands):
+                    t = _time_ms(lambda: aggregate_decomposed(
+                        subj, x, AggregateOp.SUM, kernel_intra=cand[0], kernel_inter=cand[1]))
+                    if best_t is None or t < best_t:
+                        best, best_t = cand, t
+                pair = best
                 self.kernels[(direction, f)] = pair
         return dict(self.kernels)
 
@@ -313,12 +317,12 @@ class GNN:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-        if fusable(ki, ke):
+        if fused_ok(ki, ke, subj.block_size, AggregateOp.SUM):
             h = _check_features(subj.num_vertices, h)
             out = torch.empty((subj.num_vertices, h.shape[1]), dtype=torch.float32,
                               device=h.device)
             run_fused_pair(subj, h, out, AggregateOp.SUM, self.gin_scale(), relu_src=relu_src,
-                           relu=relu)
+                           relu=relu, dense_intra=ki is KernelKind.DENSE_BLOCK)
         else:
             out = aggregate_decomposed(subj, h, AggregateOp.SUM, kernel_intra=ki,
                                        kernel_inter=ke, gin_scale=self.gin_scale())

@@ -75,6 +75,8 @@ def main():
         os.environ["AG_SLAB_DEBUG"] = "0"
         out[f"window_F{F}"] = K.to_csr(full_graph(dec)).window()
         res["fused_pair"] = timeit(lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM))
+        res["fused_pair_dense"] = timeit(lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM,
+                                                                 dense_intra=True))
         dect = net.subject_t
         hrelu = torch.randn_like(x)
         res["bwd_pair"] = timeit(lambda: K.run_fused_pair(dect, x, y, ag.AggregateOp.SUM))

@@ -127,3 +127,30 @@ def test_gemm_raw_hi_is_bitwise_masked_split(monkeypatch):
     want = K.gemm(a, b)
     monkeypatch.setenv("AG_TC_RAWHI", "1")
     assert torch.equal(K.gemm(a, b), want)
+
+
+@pytest.mark.parametrize("F", [64, 100, 256])
+def test_dense_intra_pair_within_tolerance(F):
+    """(dense_block, csr_inter) in one slab launch: the intra role as a dense
+    16 x 16 block product (order-unpinned like the reference's BLAS matmul,
+    kernels.py:247), the inter role bitwise -- against the reference pair."""
+    from conftest import rel_error
+    rg, dec = _community(6000, 90000, window=6, p_global=0.05)
+    x = np.random.default_rng(F).standard_normal((rg.num_vertices, F)).astype(np.float32)
+    got = to_np(ag.aggregate_decomposed(dec, x, ag.AggregateOp.SUM,
+                                        kernel_intra=ag.KernelKind.DENSE_BLOCK,
+                                        kernel_inter=ag.KernelKind.CSR_INTER))
+    assert rel_error(got, _oracle_pair(rg, 16, x, "sum")) < 1e-5
+
+
+def test_dense_intra_epilogues():
+    from conftest import rel_error
+    rg, dec = _community(4000, 50000, window=5, p_global=0.05, model="gin")
+    rng = np.random.default_rng(4)
+    x = torch.from_numpy(rng.standard_normal((rg.num_vertices, 64)).astype(np.float32)).cuda()
+    h = torch.from_numpy(rng.standard_normal((rg.num_vertices, 64)).astype(np.float32)).cuda()
+    y = torch.empty_like(x)
+    K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM, 1.25, relu_src=h, dense_intra=True)
+    want = np.float32(1.25) * to_np(x) + _oracle_pair(rg, 16, to_np(x), "sum")
+    want = np.where(to_np(h) > 0, want, np.float32(0.0))
+    assert rel_error(to_np(y), want) < 1e-5
