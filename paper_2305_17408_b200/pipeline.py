@@ -12,6 +12,7 @@ from dataclasses import dataclass
 import torch
 
 from .decompose import DecomposedGraph, decompose
+from .generators import generate_planted_partition, generate_rmat
 from .graph import Graph, load_edge_list
 from .kernels import AggregateOp
 from .models import gcn_normalize
@@ -50,6 +51,16 @@ class RunConfig:
     def aggregate_op(self) -> AggregateOp:
         return AggregateOp(self.op)
 
+    def as_dict(self) -> dict:
+        """The report's `config` object (bench.py:86-101), same keys and order."""
+        return {"graph": self.graph_path,
+                "rmat": list(self.rmat) if self.rmat else None,
+                "planted": list(self.planted) if self.planted else None,
+                "comm_size": self.comm_size, "reorder": self.reorder, "mode": self.mode,
+                "op": self.op, "model": self.model, "feat_dim": self.feat_dim,
+                "iters": self.iters, "profile_iters": self.profile_iters, "seed": self.seed,
+                "threads": self.threads}
+
 
 @dataclass
 class PreparedRun:
@@ -60,13 +71,20 @@ class PreparedRun:
 
 
 def build_graph(cfg: RunConfig) -> Graph:
-    """The edge-list source of the reference (bench.py:103-107); the RMAT /
-    planted generators do not scale to the benchmark shapes:
-    use paper_2305_17408_b200.synth for synthetic graphs."""
+    """The graph source of a run (bench.py:104-117): edge-list file, RMAT,
+    planted partition, or by default a planted graph of 8 groups of
+    comm_size vertices (p_in 0.5, p_out 0.01).  The generators are the
+    reference's, seed for seed; benchmark-scale synthetic graphs come from
+    paper_2305_17408_b200.synth.community_graph."""
     if cfg.graph_path is not None:
         return load_edge_list(cfg.graph_path)
-    raise ValueError("build_graph needs graph_path here; synthetic graphs come from "
-                     "paper_2305_17408_b200.synth.community_graph")
+    if cfg.rmat is not None:
+        v, e = cfg.rmat
+        return generate_rmat(v, e, seed=cfg.seed)
+    if cfg.planted is not None:
+        groups, size, p_in, p_out = cfg.planted
+        return generate_planted_partition(int(groups), int(size), p_in, p_out, seed=cfg.seed)[0]
+    return generate_planted_partition(8, cfg.comm_size, 0.5, 0.01, seed=cfg.seed)[0]
 
 
 def prepare(cfg: RunConfig, graph: Graph) -> PreparedRun:
