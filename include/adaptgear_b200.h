@@ -64,6 +64,15 @@ extern "C" {
  * the hidden layers' activation when the update GEMM runs before the
  * aggregation (A (H W) for a narrowing layer). */
 #define AG_EPI_RELU 16
+/* AG_EPI_INTER_COO (ag_fused_spmm, role_mask 3, op sum only): the inter role
+ * is the selector's coo_atomic kernel (kernels.py:192-225), whose summation
+ * order the reference leaves open (fp64 bincount over scrambled edges, tested
+ * at 1e-4): the inter edges of a row are accumulated with fused fp32
+ * multiply-adds in any order instead of the reduceat order.  The intra role
+ * keeps its own kernel's semantics (bitwise csr_intra_blocked, or dense_block
+ * with blk_w) -- the selector pairs (csr_intra_blocked | dense_block,
+ * coo_atomic) in one pass. */
+#define AG_EPI_INTER_COO 32
 
 int ag_abi_version(void);
 const char *ag_last_error(void);

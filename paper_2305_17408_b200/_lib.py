@@ -22,6 +22,7 @@ LIB_PATH = PKG / "libadaptgear_b200.so"
 AG_OK, AG_ERR_VALUE, AG_ERR_KERNEL, AG_ERR_CUDA = 0, 1, 2, 3
 AG_OP = {"sum": 0, "mean": 1, "max": 2}
 AG_EPI_COMBINE, AG_EPI_GIN, AG_EPI_EMPTY_OTHER, AG_EPI_RELU_MASK, AG_EPI_RELU = 1, 2, 4, 8, 16
+AG_EPI_INTER_COO = 32
 AG_GEMM_RELU = 1
 
 P = ctypes.c_void_p

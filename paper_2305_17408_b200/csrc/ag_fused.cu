@@ -98,7 +98,8 @@ struct GArgs {
   int64_t x_rows;           // rows of x (>= rows: a rank's halo rows follow its own)
   int64_t xblocks;          // ceil(x_rows / 16)
   int tma;                  // 1: TMA tensor loads; 0: cp.async element copies
-  int dbg;                  // development knob (AG_SLAB_DEBUG): 1 = skip the reductions
+  int dbg;                  // development knob (AG_SLAB_DEBUG bits, values then garbage): 1 skip the
+                            // reductions, 2 far copies, 4 dense products, 8 X tiles
 };
 
 // ---------------------------------------------------------- packed fp32x2 --
@@ -120,9 +121,8 @@ __device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
 // which otherwise contracts mul.rn.f32x2 + add.rn.f32x2 into one FFMA2 and
 // changes the rounding of c = fl(val * x).
 __device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b, uint64_t one) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(one), "l"(b));
-  return d;
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(b), "l"(one));
+  return a;
 }
 __device__ __forceinline__ uint64_t add2_if(uint64_t acc, uint64_t c, uint64_t one, bool on) {
   asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q fma.rn.f32x2 %0, %0, %1, %2;\n\t}"
@@ -188,6 +188,19 @@ __device__ __forceinline__ Lv<VEC> lv_scale(const Lv<VEC> &a, float v) {
     for (int i = 0; i < Lv<VEC>::NP; ++i) r.p[i] = mul2(a.p[i], vv);
   }
   return r;
+}
+// acc + x * v with one rounding (order-free roles only: AG_EPI_INTER_COO)
+template <int VEC>
+__device__ __forceinline__ Lv<VEC> lv_fma(const Lv<VEC> &x, float v, Lv<VEC> acc) {
+  if constexpr (VEC == 1) {
+    acc.s = __fmaf_rn(x.s, v, acc.s);
+  } else {
+    const uint64_t vv = pk(v, v);
+#pragma unroll
+    for (int i = 0; i < Lv<VEC>::NP; ++i)
+      asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc.p[i]) : "l"(x.p[i]), "l"(vv));
+  }
+  return acc;
 }
 template <int VEC>
 __device__ __forceinline__ Lv<VEC> lv_max(const Lv<VEC> &a, const Lv<VEC> &b) {
@@ -380,6 +393,78 @@ struct RowWarp {
     }
   }
 
+  // ---- order-free inter role (AG_EPI_INTER_COO: the selector's coo_atomic,
+  // any summation order): fused multiply-adds into two accumulators.
+  __device__ __forceinline__ void acc_it(Lv<VEC> &acc, int j) const {
+    int32_t cd;
+    float v;
+    win_ld(win + static_cast<uint32_t>(j) * 8u, cd, v);
+    const Lv<VEC> xv = lv_lds<VEC>(ring + static_cast<uint32_t>(cd) * (32u * VEC * 4u));
+    acc = W ? lv_fma<VEC>(xv, v, acc) : lv_add<VEC>(acc, xv, one);
+  }
+  __device__ __forceinline__ Lv<VEC> role_coo_fast(int o, int n) const {
+    Lv<VEC> a0 = lv_splat<VEC>(0.0f), a1 = a0;
+    int j = o;
+    const int e = o + n;
+    // fully unrolled (n <= kWin): no loop-carried accumulator copies
+#pragma unroll
+    for (int c = 0; c < kWin / 8; ++c) {
+      if (j + 8 > e) break;
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        acc_it(a0, j + i);
+        acc_it(a1, j + i + 1);
+      }
+      j += 8;
+    }
+    if (j + 4 <= e) {
+      acc_it(a0, j);
+      acc_it(a1, j + 1);
+      acc_it(a0, j + 2);
+      acc_it(a1, j + 3);
+      j += 4;
+    }
+    if (j + 2 <= e) {
+      acc_it(a0, j);
+      acc_it(a1, j + 1);
+      j += 2;
+    }
+    if (j < e) acc_it(a0, j);
+    return lv_add<VEC>(a0, a1, one);
+  }
+  // general path: window refills and global (far) sources
+  __device__ __forceinline__ void acc_item(Lv<VEC> &acc, int32_t e) const {
+    int32_t cd;
+    float v;
+    win_ld(win + static_cast<uint32_t>(e - p) * 8u, cd, v);
+    Lv<VEC> xv;
+    if (cd >= 0) {
+      xv = lv_lds<VEC>(ring + static_cast<uint32_t>(cd) * (32u * VEC * 4u));
+    } else {
+      const float *ptr;
+      asm("mad.wide.u32 %0, %1, %2, %3;"
+          : "=l"(ptr)
+          : "r"(static_cast<uint32_t>(~cd)), "r"(feat * 4u), "l"(xl));
+      xv = lv_ldg<VEC>(ptr);
+    }
+    acc = W ? lv_fma<VEC>(xv, v, acc) : lv_add<VEC>(acc, xv, one);
+  }
+  __device__ __forceinline__ Lv<VEC> role_coo(int32_t e0, int32_t n) {
+    Lv<VEC> a0 = lv_splat<VEC>(0.0f), a1 = a0;
+    const int32_t rend = e0 + n;
+#pragma unroll 1
+    for (int32_t b = e0; b < rend; b += 8) {
+      const int cnt = rend - b < 8 ? rend - b : 8;
+      ensure(b, cnt);
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        if (j < cnt) acc_item(a0, b + j);
+        if (j + 1 < cnt) acc_item(a1, b + j + 1);
+      }
+    }
+    return lv_add<VEC>(a0, a1, one);
+  }
+
   // N consecutive items [e, e + N) of the window: one uniform branch picks
   // the all-in-ring path (shared loads only) or the mixed one
   template <int N, bool RAW>
@@ -557,6 +642,14 @@ constexpr int kModeMax = 2;    // any role mask, max
 // reference's dense_block kernel, order-unpinned like its BLAS matmul) computed
 // once per block by a dedicated warp; the inter role stays bitwise csr_inter
 constexpr int kModeDense3 = 3;
+// kModeSum3 / kModeDense3 with the inter role order-free (AG_EPI_INTER_COO)
+constexpr int kModeSum3Coo = 4;
+constexpr int kModeDense3Coo = 5;
+__host__ __device__ constexpr bool mode_dense(int m) { return m == kModeDense3 || m == kModeDense3Coo; }
+__host__ __device__ constexpr bool mode_coo(int m) { return m == kModeSum3Coo || m == kModeDense3Coo; }
+__host__ __device__ constexpr bool mode_sum3(int m) {
+  return m == kModeSum3 || m == kModeDense3 || mode_coo(m);
+}
 
 // One destination row (both roles, epilogue) for this lane's columns.
 template <int VEC, int MODE, bool W>
@@ -564,31 +657,32 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
                                        int32_t e, int32_t m, float *yrow, bool act, bool fast,
                                        uint32_t relu_s, uint32_t intra_s) {
   constexpr bool IS_MAX = MODE == kModeMax;
-  constexpr bool SUM3 = MODE == kModeSum3 || MODE == kModeDense3;
-  const int64_t ld = a.feat;
+  constexpr bool SUM3 = mode_sum3(MODE);
+  constexpr bool DENSE = mode_dense(MODE);
+  constexpr bool COO = mode_coo(MODE);
   // dense-intra mode: the intra role comes from the dense warp's block product
-  const int32_t ni = MODE == kModeDense3 ? 0 : (SUM3 || (a.mask & 1)) ? m - s : 0;
+  const int32_t ni = DENSE ? 0 : (SUM3 || (a.mask & 1)) ? m - s : 0;
   const int32_t no = (SUM3 || (a.mask & 2)) ? e - m : 0;
   // the ReLU-mask operand is loaded before the reduction so its latency hides
   // behind it
   const bool relu = a.relu && act;
   Vf<VEC> I, O;
-  if (a.dbg == 1) {
+  if (a.dbg & 1) {
     I = splat<VEC>(0.0f);
     O = I;
   } else if (fast) {
     I = lv_out<VEC>(w.template role_fast<IS_MAX>(0, ni));
-    O = lv_out<VEC>(w.template role_fast<IS_MAX>(m - s, no));
+    O = lv_out<VEC>(COO ? w.role_coo_fast(m - s, no) : w.template role_fast<IS_MAX>(m - s, no));
   } else {
     I = lv_out<VEC>(w.template role<IS_MAX>(s, ni));
-    O = lv_out<VEC>(w.template role<IS_MAX>(m, no));
+    O = lv_out<VEC>(COO ? w.role_coo(m, no) : w.template role<IS_MAX>(m, no));
   }
   if (!act) return;
   float *yp = yrow;
   Vf<VEC> out;
-  if constexpr (MODE == kModeDense3) {
+  if constexpr (DENSE) {
     out = vadd<VEC>(lv_out<VEC>(lv_lds<VEC>(intra_s)), O);
-  } else if constexpr (MODE == kModeSum3) {
+  } else if constexpr (SUM3) {
     out = vadd<VEC>(I, O);
   } else if (a.mask == 3) {
     const int64_t d = (a.ep.op == AG_OP_MEAN && a.ep.deg) ? a.ep.deg[r] : 1;
@@ -632,7 +726,7 @@ struct SlabGeom {
   static constexpr uint32_t kFarSlotBytes = kFarMax * kRowBytes;
   static constexpr uint32_t kReluOff = kSlots * kSlotBytes + kFarSlots * kFarSlotBytes;
   static constexpr uint32_t kIOff = kReluOff + kReluSlots * kSlotBytes;
-  static constexpr uint32_t kWOff = kIOff + kISlots * kSlotBytes;  // 2 x 1 KB block weights
+  static constexpr uint32_t kWOff = kIOff + kISlots * kSlotBytes;  // 2 warps x 2 x 512 B weights
   static constexpr uint32_t kRingBytes = kWOff + 2 * 1024;
   static constexpr uint32_t kBarBytes = (kReady + kDone + kISlots) * 8;
   static constexpr uint32_t kWinBytes = kCons * kWin * 8;
@@ -739,9 +833,10 @@ __device__ __forceinline__ void produce_x(const GArgs &a, const CUtensorMap *map
     if (a.tma) {
       if (lane == 0) {
         if (need >= 0) bs.wait_done(static_cast<uint32_t>(need));
-        if (last) mbar_expect_tx(bs.rdy(kt), G::kSlotBytes);
-        else mbar_expect_tx_only(bs.rdy(kt), G::kSlotBytes);
-        tma_load_2d(dst, map, bs.rdy(kt), static_cast<int>(c0), static_cast<int>(t * kRB));
+        const uint32_t xb = (a.dbg & 8) ? 0u : G::kSlotBytes;
+        if (last) mbar_expect_tx(bs.rdy(kt), xb);
+        else if (xb) mbar_expect_tx_only(bs.rdy(kt), xb);
+        if (xb) tma_load_2d(dst, map, bs.rdy(kt), static_cast<int>(c0), static_cast<int>(t * kRB));
       }
     } else {
       if (need >= 0) bs.wait_done(static_cast<uint32_t>(need));
@@ -821,14 +916,15 @@ __device__ __forceinline__ void produce_far(const GArgs &a, const CUtensorMap *r
       if (a.tma) {
         if (lane == 0) {
           if (need >= int64_t(kb0)) bs.wait_done(static_cast<uint32_t>(need));
-          mbar_expect_tx(bs.rdy(f), static_cast<uint32_t>(cnt) * tile_bytes +
-                                        (a.relu ? G::kSlotBytes : 0u));
-          if (a.relu)
+          mbar_expect_tx(bs.rdy(f), (a.dbg & 2) ? 0u
+                                                : static_cast<uint32_t>(cnt) * tile_bytes +
+                                                      (a.relu ? G::kSlotBytes : 0u));
+          if (a.relu && !(a.dbg & 2))
             tma_load_2d(relu_dst, relu_map, bs.rdy(f), static_cast<int>(c0),
                         static_cast<int>(f * kRB));
         }
         __syncwarp();
-        if (lane < cnt)
+        if (lane < cnt && !(a.dbg & 2))
           bulk_g2s(slot_base + lane * G::kRowBytes, a.x + static_cast<int64_t>(src) * a.feat + c0,
                    tile_bytes, bs.rdy(f));
       } else {
@@ -881,13 +977,15 @@ __device__ __forceinline__ void dense_intra(const GArgs &a, uint32_t ring, const
                                             uint32_t ivalid, uint32_t kb0, uint32_t kb1,
                                             int lane, int half) {
   using G = SlabGeom<VEC>;
-  const uint32_t wbuf = ring + G::kWOff;
-  auto fetch_w = [&](uint32_t f, int buf) {  // 1 KB: 32 bytes per lane
-    if (f < kb1) {
-      const float *src = a.blk_w + static_cast<int64_t>(f) * 256 + lane * 8;
-      cp_async16(wbuf + buf * 1024 + lane * 32, src);
-      cp_async16(wbuf + buf * 1024 + lane * 32 + 16, src + 4);
-    }
+  // this warp's own double buffer of its kRB / kDenseWarps weight rows (the
+  // warps drift apart by a block, so they must not share one)
+  constexpr int kRows = kRB / kDenseWarps;
+  constexpr uint32_t kBuf = kRows * kRB * 4;  // 512 B
+  const uint32_t wbuf = ring + G::kWOff + half * 2 * kBuf;
+  auto fetch_w = [&](uint32_t f, int buf) {  // 16 bytes per lane
+    if (f < kb1)
+      cp_async16(wbuf + buf * kBuf + lane * 16,
+                 a.blk_w + static_cast<int64_t>(f) * 256 + half * kRows * kRB + lane * 4);
     cp_async_commit();
   };
   fetch_w(kb0, 0);
@@ -900,21 +998,29 @@ __device__ __forceinline__ void dense_intra(const GArgs &a, uint32_t ring, const
     __syncwarp();
     mbar_wait(bs.rdy(f), bs.rdy_phase(f));  // X block f is in the ring
     if (fi >= kISlots) bs.wait_done(f - kISlots);  // the I slot's previous block is consumed
+    if (a.dbg & 4) {
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(ivalid + (fi % kISlots) * 8);
+        mbar_arrive(bs.done + (fi % kDone) * 8);
+      }
+      continue;
+    }
     const uint32_t xs = ring + (f % kSlots) * G::kSlotBytes + lane * VEC * 4;
     Lv<VEC> xr[kRB];
 #pragma unroll
     for (int j = 0; j < kRB; ++j) xr[j] = lv_lds<VEC>(xs + j * G::kRowBytes);
     const uint32_t is = ring + G::kIOff + (fi % kISlots) * G::kSlotBytes + lane * VEC * 4;
-    const uint32_t wrow = wbuf + buf * 1024;
+    const uint32_t wrow = wbuf + buf * kBuf;
 #pragma unroll 2
-    for (int i = half * (kRB / kDenseWarps); i < (half + 1) * (kRB / kDenseWarps); ++i) {
+    for (int i = half * kRows; i < (half + 1) * kRows; ++i) {
       float wv[kRB];
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(wv[4 * q]), "=f"(wv[4 * q + 1]), "=f"(wv[4 * q + 2]),
                        "=f"(wv[4 * q + 3])
-                     : "r"(wrow + i * 64 + q * 16));
+                     : "r"(wrow + (i - half * kRows) * 64 + q * 16));
       Lv<VEC> acc = lv_scale<VEC>(xr[0], wv[0]);
 #pragma unroll
       for (int j = 1; j < kRB; ++j) {
@@ -955,7 +1061,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t done = ready + kReady * 8;
   const uint32_t ivalid = done + kDone * 8;  // dense-intra mode: I slot of block k written
   const uint32_t wins = ivalid + kISlots * 8;
-  constexpr bool DENSE = MODE == kModeDense3;
+  constexpr bool DENSE = mode_dense(MODE);
   constexpr int NC = DENSE ? kCons - kDenseWarps : kCons;  // consumer warps (dense warps last)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -1038,7 +1144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const int32_t s = info.x, e = info.z;
           const int32_t m =
-              (MODE == kModeSum3 || DENSE || a.has_mid) ? info.y : (a.mask == 1 ? e : s);
+              (mode_sum3(MODE) || a.has_mid) ? info.y : (a.mask == 1 ? e : s);
           const bool fast = !(info.w & kRowSlow);
           w.end = e;
           if (fast) w.template install<true>(s, q0, q1);
@@ -1113,6 +1219,10 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
   const bool wt = a.weighted != 0;
   auto k = mode == kModeMax
                ? (wt ? slab_kernel<VEC, kModeMax, true> : slab_kernel<VEC, kModeMax, false>)
+           : mode == kModeDense3Coo
+               ? (wt ? slab_kernel<VEC, kModeDense3Coo, true> : slab_kernel<VEC, kModeDense3Coo, false>)
+           : mode == kModeSum3Coo
+               ? (wt ? slab_kernel<VEC, kModeSum3Coo, true> : slab_kernel<VEC, kModeSum3Coo, false>)
            : mode == kModeDense3
                ? (wt ? slab_kernel<VEC, kModeDense3, true> : slab_kernel<VEC, kModeDense3, false>)
            : mode == kModeSum3
@@ -1375,10 +1485,14 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
   a.weighted = weighted != 0;
   a.has_mid = role_mid != nullptr;
   a.blk_w = blk_w;
+  constexpr int32_t kSum3Flags = AG_EPI_GIN | AG_EPI_RELU_MASK | AG_EPI_RELU | AG_EPI_INTER_COO;
   if (blk_w != nullptr &&
-      (role_mask != 3 || op != AG_OP_SUM || role_mid == nullptr ||
-       (epi_flags & ~(AG_EPI_GIN | AG_EPI_RELU_MASK | AG_EPI_RELU)) != 0))
+      (role_mask != 3 || op != AG_OP_SUM || role_mid == nullptr || (epi_flags & ~kSum3Flags) != 0))
     return fail(AG_ERR_VALUE, "dense intra blocks need role_mask 3, op sum and role_mid");
+  const bool coo = (epi_flags & AG_EPI_INTER_COO) != 0;
+  if (coo && (role_mask != 3 || op != AG_OP_SUM || role_mid == nullptr ||
+              (epi_flags & ~kSum3Flags) != 0))
+    return fail(AG_ERR_VALUE, "AG_EPI_INTER_COO needs role_mask 3, op sum and role_mid");
   a.x = x;
   a.y = y;
   a.ep = Epi{op, epi_flags, other_touched, deg, x, feat, gin_scale, relu_src};
@@ -1389,10 +1503,10 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                   (reinterpret_cast<uintptr_t>(y) % 8) == 0 &&
                   (relu_src == nullptr || (reinterpret_cast<uintptr_t>(relu_src) % 8) == 0) &&
                   env_int("AG_SLAB_VEC", 2) == 2;
-  const int mode = blk_w != nullptr ? kModeDense3
+  const int mode = blk_w != nullptr ? (coo ? kModeDense3Coo : kModeDense3)
+                 : coo ? kModeSum3Coo
                  : is_max ? kModeMax
-                   : (role_mask == 3 && op == AG_OP_SUM &&
-                      (epi_flags & ~(AG_EPI_GIN | AG_EPI_RELU_MASK | AG_EPI_RELU)) == 0)
+                   : (role_mask == 3 && op == AG_OP_SUM && (epi_flags & ~kSum3Flags) == 0)
                        ? kModeSum3
                        : kModeAny;
   if (v2) return launch_slab<2>(a, mode, window, st);

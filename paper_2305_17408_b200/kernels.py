@@ -411,9 +411,11 @@ CSR_KINDS = (KernelKind.CSR_INTRA_BLOCKED, KernelKind.CSR_INTER)
 
 def fusable(kernel_intra: KernelKind, kernel_inter: KernelKind, block_size: int = 16) -> bool:
     """A CSR x CSR pair runs as ONE fused launch over the full CSR (same bits);
-    so does (dense_block, csr_inter) for 16-row blocks (the slab kernel's
-    dense-intra mode)."""
-    if kernel_inter is not KernelKind.CSR_INTER:
+    so do (dense_block, csr_inter) for 16-row blocks (the slab kernel's
+    dense-intra mode) and either intra kernel with coo_atomic as the inter
+    role (AG_EPI_INTER_COO: the inter edges in any order, like the reference's
+    scrambled fp64 bincount)."""
+    if kernel_inter not in (KernelKind.CSR_INTER, KernelKind.COO_ATOMIC):
         return False
     return kernel_intra in CSR_KINDS or (kernel_intra is KernelKind.DENSE_BLOCK
                                          and block_size == 16)
@@ -422,21 +424,33 @@ def fusable(kernel_intra: KernelKind, kernel_inter: KernelKind, block_size: int 
 def fused_ok(kernel_intra: KernelKind, kernel_inter: KernelKind, block_size: int,
              op: AggregateOp) -> bool:
     """fusable(), restricted to what the fused kernel computes for `op` (the
-    dense-intra mode is sum-only; dense_block rejects max anyway)."""
+    dense-intra and order-free inter modes are sum-only; dense_block rejects
+    max anyway)."""
     return fusable(kernel_intra, kernel_inter, block_size) and (
-        kernel_intra is not KernelKind.DENSE_BLOCK or op is AggregateOp.SUM)
+        op is AggregateOp.SUM or (kernel_intra is not KernelKind.DENSE_BLOCK
+                                  and kernel_inter is not KernelKind.COO_ATOMIC))
 
 
 def run_fused_pair(d: DecomposedGraph, x: torch.Tensor, y: torch.Tensor, op: AggregateOp,
                    gin_scale: float | None = None, relu_src: torch.Tensor | None = None,
-                   relu: bool = False, dense_intra: bool = False) -> None:
+                   relu: bool = False, dense_intra: bool = False,
+                   kernel_intra: KernelKind | None = None,
+                   kernel_inter: KernelKind = KernelKind.CSR_INTER) -> None:
     """y = combine(intra, inter) [+ gin] [relu] [* (relu_src > 0)] in one pass
-    over the full reordered CSR."""
+    over the full reordered CSR for the selector pair (kernel_intra,
+    kernel_inter); `dense_intra` is shorthand for kernel_intra=dense_block."""
+    if kernel_intra is None:
+        kernel_intra = KernelKind.DENSE_BLOCK if dense_intra else KernelKind.CSR_INTRA_BLOCKED
+    if not fused_ok(kernel_intra, kernel_inter, d.block_size, op):
+        raise KernelError(f"no fused kernel for ({kernel_intra.value}, {kernel_inter.value}, "
+                          f"{op.value}, block_size={d.block_size})")
     full = full_graph(d)
-    flags = (_lib.AG_EPI_GIN if gin_scale is not None else 0) | (_lib.AG_EPI_RELU if relu else 0)
+    flags = ((_lib.AG_EPI_GIN if gin_scale is not None else 0)
+             | (_lib.AG_EPI_RELU if relu else 0)
+             | (_lib.AG_EPI_INTER_COO if kernel_inter is KernelKind.COO_ATOMIC else 0))
     launch_fused(to_csr(full), x, y, op, block=d.block_size, mask=3, flags=flags,
                  deg=d.full_in_degree, gin_scale=0.0 if gin_scale is None else gin_scale,
-                 relu_src=relu_src, dense_intra=dense_intra)
+                 relu_src=relu_src, dense_intra=kernel_intra is KernelKind.DENSE_BLOCK)
 
 
 def aggregate_full(g: Graph, x, op: AggregateOp, kernel: KernelKind = KernelKind.CSR_INTER,
@@ -469,8 +483,8 @@ def aggregate_decomposed(d: DecomposedGraph, x, op: AggregateOp,
     x = _check_features(d.num_vertices, x)
     y = torch.empty((d.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
     if fused_ok(kernel_intra, kernel_inter, d.block_size, op):
-        run_fused_pair(d, x, y, op, gin_scale,
-                       dense_intra=kernel_intra is KernelKind.DENSE_BLOCK)
+        run_fused_pair(d, x, y, op, gin_scale, kernel_intra=kernel_intra,
+                       kernel_inter=kernel_inter)
         return y
     intra, inter = decomposed_execs(d)
     inter.run_raw_into(kernel_inter, x, y, op, tile_budget_bytes)

@@ -265,10 +265,12 @@ class GNN:
 
         The selector itself is the reference's (per-role argmin of separately
         timed kernels, selector.py:109-154); its locked pair is kept in
-        `selector_choice`.  Because a CSR x CSR pair runs as ONE fused launch
-        here (both roles + combine + the ReLU-backward epilogue, one pass
-        over x), the pair actually executed is whichever of {selector pair,
-        fused CSR pair} is faster end to end, timed once more on the device.
+        `selector_choice`.  Because a pair of the selector's candidates runs
+        as ONE fused launch here (both roles + combine + the ReLU-backward
+        epilogue, one pass over x: csr_intra_blocked or dense_block with
+        csr_inter or coo_atomic), the pair actually executed is the fastest
+        of the selector's pair and the fused pairs, timed once more on the
+        device.
         """
         from .selector import SelectorState, run_training_loop
         if not hasattr(self, "selector_choice"):
@@ -287,10 +289,13 @@ class GNN:
                 pair = (s.choice_intra, s.choice_inter)
                 self.selector_choice[(direction, f)] = pair
                 # what actually runs: the fastest of the selector's pair and the
-                # fused pairs (CSR x CSR bitwise, dense_block x csr_inter)
-                cands = [pair, (KernelKind.CSR_INTRA_BLOCKED, KernelKind.CSR_INTER)]
+                # fused pairs (CSR x CSR bitwise, dense_block x csr_inter, and
+                # either intra kernel x coo_atomic)
+                intra = [KernelKind.CSR_INTRA_BLOCKED]
                 if subj.block_size == 16:
-                    cands.append((KernelKind.DENSE_BLOCK, KernelKind.CSR_INTER))
+                    intra.append(KernelKind.DENSE_BLOCK)
+                cands = [pair] + [(ki, ke) for ki in intra
+                                  for ke in (KernelKind.CSR_INTER, KernelKind.COO_ATOMIC)]
                 best, best_t = pair, None
                 for cand in dict.fromkeys(cands):
                     t = _time_ms(lambda: aggregate_decomposed(
@@ -322,7 +327,7 @@ class GNN:
             out = torch.empty((subj.num_vertices, h.shape[1]), dtype=torch.float32,
                               device=h.device)
             run_fused_pair(subj, h, out, AggregateOp.SUM, self.gin_scale(), relu_src=relu_src,
-                           relu=relu, dense_intra=ki is KernelKind.DENSE_BLOCK)
+                           relu=relu, kernel_intra=ki, kernel_inter=ke)
         else:
             out = aggregate_decomposed(subj, h, AggregateOp.SUM, kernel_intra=ki,
                                        kernel_inter=ke, gin_scale=self.gin_scale())

@@ -35,6 +35,9 @@ def main():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--feat", type=int, nargs="+", default=[256, 100])
     ap.add_argument("--only", default=None, help="run just this kernel once (for ncu)")
+    ap.add_argument("--pair", default="csr_intra_blocked,csr_inter",
+                    help="intra,inter kernel pair of --only fused_pair / --suite agg")
+    ap.add_argument("--suite", default="all", help="all | agg (fused aggregation pairs only)")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     g, rg, dec, net, prep = bench.build_workload(cfg)
@@ -55,9 +58,32 @@ def main():
             K.gemm(x, w)
             torch.cuda.synchronize()
             continue
+        ki, ke = (ag.KernelKind(k) for k in args.pair.split(","))
         if args.only == "fused_pair":
-            K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM)
+            K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM, kernel_intra=ki, kernel_inter=ke)
             torch.cuda.synchronize()
+            continue
+        if args.suite == "agg":
+            ba = bench.bytes_alg(V, E, F, rg.weights is not None)
+            ref = torch.empty_like(x)
+            K.run_fused_pair(dec, x, ref, ag.AggregateOp.SUM)
+            refd = ref.double()
+            res, err = {}, {}
+            hrelu = torch.randn_like(x)
+            for pki in (ag.KernelKind.CSR_INTRA_BLOCKED, ag.KernelKind.DENSE_BLOCK):
+                for pke in (ag.KernelKind.CSR_INTER, ag.KernelKind.COO_ATOMIC):
+                    name = f"{pki.value}+{pke.value}"
+                    run = lambda d=dec, **kw: K.run_fused_pair(d, x, y, ag.AggregateOp.SUM,
+                                                               kernel_intra=pki,
+                                                               kernel_inter=pke, **kw)
+                    res[name] = timeit(run)
+                    err[name] = float(((y.double() - refd).abs()
+                                       / refd.abs().clamp(min=1.0)).max())
+                    res[name + ":bwd_relu"] = timeit(lambda: run(net.subject_t,
+                                                                 relu_src=hrelu))
+            gbs = {k: round(ba / (v / 1e3) / 1e9, 1) for k, v in res.items()}
+            out[f"F{F}"] = {"ms": {k: round(v, 4) for k, v in res.items()}, "alg_GBps": gbs,
+                            "max_rel_vs_bitwise_pair": err, "bytes_alg": ba}
             continue
         ba = bench.bytes_alg(V, E, F, rg.weights is not None)
         res = {}

@@ -59,5 +59,8 @@ tot = sum(v[0] for v in agg.values())
 tots = sum(v[1] for v in agg.values())
 print("instructions", tot, "samples", tots)
 print("line  %instr  %stall  source")
-for ln, (n, s) in sorted(agg.items(), key=lambda kv: -kv[1][0] - kv[1][1] * tot / max(tots, 1))[:N]:
+ORDER = os.environ.get("ORDER")
+items = sorted(agg.items(), key=lambda kv: -kv[1][0] - kv[1][1] * tot / max(tots, 1))[:N]
+if ORDER: items.sort()
+for ln, (n, s) in items:
     print(f"{ln:5d} {n / tot * 100:6.1f} {s / tots * 100:6.1f}  " + (lines[ln - 1].strip()[:90] if ln > 0 else "?"))

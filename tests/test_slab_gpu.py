@@ -143,6 +143,23 @@ def test_dense_intra_pair_within_tolerance(F):
     assert rel_error(got, _oracle_pair(rg, 16, x, "sum")) < 1e-5
 
 
+@pytest.mark.parametrize("F", [48, 100, 256])
+def test_dense_intra_large_graph(F):
+    """Enough blocks per CTA that the two dense warps drift apart (each has its
+    own weight staging buffer); against the bitwise CSR pair."""
+    from conftest import rel_error
+    rg, dec = _community(300000, 4000000, window=12, p_global=0.05)
+    x = torch.randn((rg.num_vertices, F), device="cuda")
+    want = torch.empty_like(x)
+    K.run_fused_pair(dec, x, want, ag.AggregateOp.SUM)
+    for ke in (ag.KernelKind.CSR_INTER, ag.KernelKind.COO_ATOMIC):
+        y = torch.empty_like(x)
+        for _ in range(3):
+            K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM, kernel_intra=ag.KernelKind.DENSE_BLOCK,
+                             kernel_inter=ke)
+            assert rel_error(to_np(y), to_np(want)) < 1e-5, ke
+
+
 def test_dense_intra_epilogues():
     from conftest import rel_error
     rg, dec = _community(4000, 50000, window=5, p_global=0.05, model="gin")
@@ -154,3 +171,72 @@ def test_dense_intra_epilogues():
     want = np.float32(1.25) * to_np(x) + _oracle_pair(rg, 16, to_np(x), "sum")
     want = np.where(to_np(h) > 0, want, np.float32(0.0))
     assert rel_error(to_np(y), want) < 1e-5
+
+
+COO_PAIRS = [(ag.KernelKind.CSR_INTRA_BLOCKED, ag.KernelKind.COO_ATOMIC),
+             (ag.KernelKind.DENSE_BLOCK, ag.KernelKind.COO_ATOMIC)]
+
+
+@pytest.mark.parametrize("F", [7, 64, 100, 256])
+@pytest.mark.parametrize("pair", COO_PAIRS, ids=lambda p: p[0].value)
+def test_coo_inter_pair_within_tolerance(F, pair):
+    """(intra, coo_atomic) in one slab launch: the inter role in any order
+    (AG_EPI_INTER_COO, like the reference's scrambled bincount) -- within the
+    reference's 1e-4 (checked at 1e-5) of the bitwise pair."""
+    from conftest import rel_error
+    rg, dec = _community(6000, 90000, window=6, p_global=0.05)
+    x = np.random.default_rng(F).standard_normal((rg.num_vertices, F)).astype(np.float32)
+    got = to_np(ag.aggregate_decomposed(dec, x, ag.AggregateOp.SUM, kernel_intra=pair[0],
+                                        kernel_inter=pair[1]))
+    assert rel_error(got, _oracle_pair(rg, 16, x, "sum")) < 1e-5
+
+
+@pytest.mark.parametrize("pair", COO_PAIRS, ids=lambda p: p[0].value)
+def test_coo_inter_general_path_and_unweighted(pair):
+    """Far-ring overflow, hub rows past the window (general path) and an
+    unweighted (GIN) graph."""
+    from conftest import rel_error
+    rng = np.random.default_rng(3)
+    V = 3000
+    keys = rng.choice(V * V, size=60000, replace=False)
+    d, s = keys // V, keys % V
+    hub = rng.choice(V, size=900, replace=False)
+    d = np.concatenate([d, np.full(hub.size, 5)])
+    s = np.concatenate([s, hub])
+    for g in (ag.gcn_normalize(ag.Graph.from_edges(V, d, s)), ag.Graph.from_edges(V, d, s)):
+        dec = ag.decompose(g, 16)
+        for F in (32, 100):
+            x = rng.standard_normal((V, F)).astype(np.float32)
+            got = to_np(ag.aggregate_decomposed(dec, x, ag.AggregateOp.SUM,
+                                                kernel_intra=pair[0], kernel_inter=pair[1]))
+            # a 900-edge hub row summed in fp32: the reference's coo bar (1e-4)
+            assert rel_error(got, _oracle_pair(g, 16, x, "sum")) < 1e-4, F
+
+
+@pytest.mark.parametrize("pair", COO_PAIRS, ids=lambda p: p[0].value)
+def test_coo_inter_epilogues(pair):
+    from conftest import rel_error
+    rg, dec = _community(4000, 50000, window=5, p_global=0.05, model="gin")
+    rng = np.random.default_rng(4)
+    x = torch.from_numpy(rng.standard_normal((rg.num_vertices, 64)).astype(np.float32)).cuda()
+    h = torch.from_numpy(rng.standard_normal((rg.num_vertices, 64)).astype(np.float32)).cuda()
+    y = torch.empty_like(x)
+    K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM, 1.25, relu_src=h, kernel_intra=pair[0],
+                     kernel_inter=pair[1])
+    want = np.float32(1.25) * to_np(x) + _oracle_pair(rg, 16, to_np(x), "sum")
+    want = np.where(to_np(h) > 0, want, np.float32(0.0))
+    assert rel_error(to_np(y), want) < 1e-5
+
+
+def test_coo_inter_needs_sum():
+    rg, dec = _community(2000, 20000, window=4, p_global=0.05)
+    x = torch.randn((rg.num_vertices, 16), device="cuda")
+    y = torch.empty_like(x)
+    with pytest.raises(ag.KernelError, match="no fused kernel"):
+        K.run_fused_pair(dec, x, y, ag.AggregateOp.MEAN, kernel_inter=ag.KernelKind.COO_ATOMIC)
+    # the unfused pair still serves mean / max
+    for op in (ag.AggregateOp.MEAN, ag.AggregateOp.MAX):
+        got = to_np(ag.aggregate_decomposed(dec, x, op,
+                                            kernel_inter=ag.KernelKind.COO_ATOMIC))
+        from conftest import rel_error
+        assert rel_error(got, _oracle_pair(rg, 16, to_np(x), op.value)) < 1e-4
