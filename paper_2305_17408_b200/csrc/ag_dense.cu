@@ -199,6 +199,61 @@ __global__ void __launch_bounds__(kXentThreads) xent_kernel(
   }
 }
 
+// Narrow logits (ld <= kXentLd): a thread per row.  Each CTA stages a chunk of
+// kXentThreads consecutive rows (contiguous: row stride ld) in shared memory
+// with coalesced float4 loads, every thread reduces its own row there (max,
+// sum of exp, gradient written back in place), and the chunk is stored back
+// coalesced.  Loss partials as in xent_kernel: fp64 per thread in a fixed row
+// order, then a fixed-order CTA sum.
+constexpr int kXentLd = 64;
+
+__global__ void __launch_bounds__(kXentThreads) xent_rows_kernel(
+    int64_t rows, int64_t C, int64_t ld, const float *logits, const int32_t *labels,
+    const uint8_t *mask, float inv_n, double *partial, float *dlogits) {
+  extern __shared__ float zs[];  // kXentThreads * ld
+  __shared__ double tsum[kXentThreads];
+  const int t = threadIdx.x;
+  double acc = 0.0;
+  for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * kXentThreads; r0 < rows;
+       r0 += static_cast<int64_t>(gridDim.x) * kXentThreads) {
+    const int64_t nr = rows - r0 < kXentThreads ? rows - r0 : static_cast<int64_t>(kXentThreads);
+    const int64_t n = nr * ld;  // multiple of 4 (ld % 4 == 0)
+    const float4 *src = reinterpret_cast<const float4 *>(logits + r0 * ld);
+    for (int64_t i = t; i < n / 4; i += kXentThreads) reinterpret_cast<float4 *>(zs)[i] = src[i];
+    __syncthreads();
+    if (t < nr) {
+      float *z = zs + static_cast<int64_t>(t) * ld;
+      const int64_t r = r0 + t;
+      if (mask && mask[r] == 0) {
+        for (int64_t c = 0; c < C; ++c) z[c] = 0.0f;
+      } else {
+        float mx = -INFINITY;
+        for (int64_t c = 0; c < C; ++c) mx = fmaxf(mx, z[c]);
+        float se = 0.0f;
+        for (int64_t c = 0; c < C; ++c) se += expf(z[c] - mx);
+        const int32_t y = labels[r];
+        acc += static_cast<double>(mx + logf(se) - z[y]);
+        const float inv_se = 1.0f / se;
+        for (int64_t c = 0; c < C; ++c) {
+          const float pr = expf(z[c] - mx) * inv_se;
+          z[c] = (pr - (c == y ? 1.0f : 0.0f)) * inv_n;
+        }
+      }
+    }
+    __syncthreads();
+    float4 *dst = reinterpret_cast<float4 *>(dlogits + r0 * ld);
+    for (int64_t i = t; i < n / 4; i += kXentThreads) dst[i] = reinterpret_cast<float4 *>(zs)[i];
+    __syncthreads();
+  }
+  tsum[t] = acc;
+  __syncthreads();
+  if (t == 0) {
+    double s = 0.0;
+    for (int i = 0; i < kXentThreads; ++i) s += tsum[i];
+    partial[blockIdx.x] = s;
+  }
+}
+
 __global__ void loss_final_kernel(int n, const double *partial, double inv_n, float *out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double t = 0.0;
@@ -270,15 +325,32 @@ extern "C" int ag_softmax_xent(int64_t rows, int64_t C, int64_t ld, const float 
   if (rows < 0 || C < 1 || ld < C) return fail(AG_ERR_VALUE, "bad loss sizes");
   cudaStream_t st = as_stream(stream);
   const float inv_n = num_masked > 0 ? 1.0f / static_cast<float>(num_masked) : 0.0f;
-  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64,
-                                                              static_cast<int64_t>(sm_count()) * 8));
-  const int64_t per = (rows + ctas - 1) / ctas;
+  const bool narrow = ld <= kXentLd && ld % 4 == 0 &&
+                      (reinterpret_cast<uintptr_t>(logits) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(dlogits) & 15) == 0;
+  int64_t ctas;
   Scratch part;
-  AG_CUDA(part.alloc(ctas * sizeof(double), st));
-  xent_kernel<<<static_cast<unsigned>(ctas), kXentThreads, 0, st>>>(
-      rows, C, ld, logits, labels, mask, inv_n, std::max<int64_t>(per, 1), part.as<double>(),
-      dlogits);
-  AG_LAUNCH_CHECK("xent_kernel");
+  if (narrow) {
+    // rows per CTA chunk = kXentThreads; ~2 chunks per CTA in flight per SM slot
+    const size_t smem = static_cast<size_t>(kXentThreads) * ld * sizeof(float);
+    ctas = std::max<int64_t>(1, std::min<int64_t>((rows + kXentThreads - 1) / kXentThreads,
+                                                  static_cast<int64_t>(sm_count()) * 4));
+    AG_CUDA(part.alloc(ctas * sizeof(double), st));
+    AG_CUDA(cudaFuncSetAttribute(xent_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kXentThreads * kXentLd * sizeof(float))));
+    xent_rows_kernel<<<static_cast<unsigned>(ctas), kXentThreads, smem, st>>>(
+        rows, C, ld, logits, labels, mask, inv_n, part.as<double>(), dlogits);
+    AG_LAUNCH_CHECK("xent_rows_kernel");
+  } else {
+    ctas = std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64,
+                                                  static_cast<int64_t>(sm_count()) * 8));
+    const int64_t per = (rows + ctas - 1) / ctas;
+    AG_CUDA(part.alloc(ctas * sizeof(double), st));
+    xent_kernel<<<static_cast<unsigned>(ctas), kXentThreads, 0, st>>>(
+        rows, C, ld, logits, labels, mask, inv_n, std::max<int64_t>(per, 1), part.as<double>(),
+        dlogits);
+    AG_LAUNCH_CHECK("xent_kernel");
+  }
   loss_final_kernel<<<1, 32, 0, st>>>(static_cast<int>(ctas), part.as<double>(),
                                       num_masked > 0 ? 1.0 / num_masked : 0.0, loss_out);
   AG_LAUNCH_CHECK("loss_final_kernel");

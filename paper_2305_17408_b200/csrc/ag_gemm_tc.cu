@@ -169,6 +169,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 consecutive fp32 columns of this lane's TMEM row, no wait (the caller
+// issues tmem_wait_ld() once for several loads)
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // Shared-memory matrix descriptor (sm_100 version 1).  K-major operands use
 // SWIZZLE_128B (layout 2: 8 rows x 128 B atoms, 16-byte chunks XOR row%8);
 // tf32 MN-major operands must use SWIZZLE_128B_BASE32B (layout 1: 4 K-rows x
@@ -206,7 +218,9 @@ struct Cfg {
   static constexpr int COLS = ACC_BUFS * NACC * BN;
   static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128
                                  : COLS <= 256 ? 256 : 512;
-  static constexpr int SMEM = STAGES * STAGE + 1024 /* align */ + 256 /* barriers */;
+  // epilogue transpose buffers: 4 warps x (32 rows x 32 fp32)
+  static constexpr int EPI = 4 * 32 * 32 * 4;
+  static constexpr int SMEM = STAGES * STAGE + 1024 /* align */ + 256 /* barriers */ + EPI;
 };
 
 // split x (fp32) into hi (in place) and lo, n4 float4s.  RAW: only lo is
@@ -214,9 +228,16 @@ struct Cfg {
 // just the top 19 bits of each fp32 operand (verified bitwise against the
 // masked split by tests/test_gemm_gpu.py).
 template <bool RAW>
-__device__ __forceinline__ void split_tile(float4 *hi, float4 *lo, int n4, int t, int nt) {
+__device__ __forceinline__ void split_tile(uint32_t hi, uint32_t lo, int n4, int t, int nt) {
+  // shared-space addresses: generic pointers here compile to LD.E / ST.E
+  // through the generic path (long-scoreboard latency)
+#pragma unroll 4
   for (int i = t; i < n4; i += nt) {
-    float4 v = hi[i], h, l;
+    float4 v, h, l;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(hi + i * 16)
+                 : "memory");
     h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
     h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
     h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
@@ -225,8 +246,13 @@ __device__ __forceinline__ void split_tile(float4 *hi, float4 *lo, int n4, int t
     l.y = __fsub_rn(v.y, h.y);
     l.z = __fsub_rn(v.z, h.z);
     l.w = __fsub_rn(v.w, h.w);
-    if (!RAW) hi[i] = h;
-    lo[i] = l;
+    if (!RAW)
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(hi + i * 16), "f"(h.x),
+                   "f"(h.y), "f"(h.z), "f"(h.w)
+                   : "memory");
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lo + i * 16), "f"(l.x),
+                 "f"(l.y), "f"(l.z), "f"(l.w)
+                 : "memory");
   }
 }
 
@@ -249,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *tfull = empty + C::STAGES;  // [2]
   uint64_t *tempty = tfull + 2;         // [2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  unsigned char *epi_buf = smem + C::STAGES * C::STAGE + 256;  // C::EPI bytes
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // cluster tiles: CL consecutive M tiles x one N tile x one K split
@@ -410,23 +437,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nkb = tile_kblocks(t, k0);
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[stage], phase);
-        unsigned char *st = smem + stage * C::STAGE;
+        const uint32_t st = su32(smem + stage * C::STAGE);
         if (g.exp & 1) {
         } else if (g.b_presplit) {
-          split_tile<true>(reinterpret_cast<float4 *>(st),
-                           reinterpret_cast<float4 *>(st + C::A_BYTES), C::A_BYTES / 16, t_id, 128);
+          split_tile<true>(st, st + C::A_BYTES, C::A_BYTES / 16, t_id, 128);
         } else if (g.raw_hi) {
-          split_tile<true>(reinterpret_cast<float4 *>(st),
-                           reinterpret_cast<float4 *>(st + C::A_BYTES), C::A_BYTES / 16, t_id, 128);
-          split_tile<true>(reinterpret_cast<float4 *>(st + 2 * C::A_BYTES),
-                           reinterpret_cast<float4 *>(st + 2 * C::A_BYTES + C::B_BYTES),
-                           C::B_BYTES / 16, t_id, 128);
+          split_tile<true>(st, st + C::A_BYTES, C::A_BYTES / 16, t_id, 128);
+          split_tile<true>(st + 2 * C::A_BYTES, st + 2 * C::A_BYTES + C::B_BYTES, C::B_BYTES / 16,
+                           t_id, 128);
         } else {
-          split_tile<false>(reinterpret_cast<float4 *>(st),
-                            reinterpret_cast<float4 *>(st + C::A_BYTES), C::A_BYTES / 16, t_id, 128);
-          split_tile<false>(reinterpret_cast<float4 *>(st + 2 * C::A_BYTES),
-                            reinterpret_cast<float4 *>(st + 2 * C::A_BYTES + C::B_BYTES),
-                            C::B_BYTES / 16, t_id, 128);
+          split_tile<false>(st, st + C::A_BYTES, C::A_BYTES / 16, t_id, 128);
+          split_tile<false>(st + 2 * C::A_BYTES, st + 2 * C::A_BYTES + C::B_BYTES, C::B_BYTES / 16,
+                            t_id, 128);
         }
         fence_proxy_async();
         __syncwarp();
@@ -444,77 +466,149 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t m0 = tile_m0(t);
       const int64_t n0 = tile_n0(t);
       const int64_t row = m0 + q * 32 + lane;
-      if (g.mask != nullptr && g.splits == 1 && row < g.M && (g.ldm % 4) == 0) {
-        // pull this row's mask segment into L2 while the tile's MMAs run
-        const float *mp = g.mask + row * g.ldm + n0;
-        const int64_t cols = std::min<int64_t>(BN, g.N - n0);
-        const uintptr_t lo = reinterpret_cast<uintptr_t>(mp) & ~uintptr_t(15);
-        const uintptr_t hi = (reinterpret_cast<uintptr_t>(mp + cols) + 15) & ~uintptr_t(15);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo),
-                     "r"(static_cast<uint32_t>(hi - lo))
-                     : "memory");
+      if (g.mask != nullptr && g.splits == 1 && (g.ldm % 4) == 0) {
+        // pull this row's mask segment of the NEXT tile into L2 (a whole tile
+        // period ahead of its use; the first tile's own segment too)
+        auto prefetch_mask = [&](int64_t tt) {
+          if (tt >= total) return;
+          const int64_t r = tile_m0(tt) + q * 32 + lane;
+          const int64_t nn = tile_n0(tt);
+          if (r >= g.M) return;
+          const float *mp = g.mask + r * g.ldm + nn;
+          const int64_t cols = std::min<int64_t>(BN, g.N - nn);
+          const uintptr_t lo = reinterpret_cast<uintptr_t>(mp) & ~uintptr_t(15);
+          const uintptr_t hi = (reinterpret_cast<uintptr_t>(mp + cols) + 15) & ~uintptr_t(15);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo),
+                       "r"(static_cast<uint32_t>(hi - lo))
+                       : "memory");
+        };
+        if (t == cid) prefetch_mask(t);
+        prefetch_mask(t + ncl);
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      float *crow;
-      bool direct = g.splits == 1;
-      if (direct) crow = g.C + row * g.ldc;
-      else crow = g.C + (s * g.M + row) * g.N;
-      const bool vec_ok = ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
+      const bool direct = g.splits == 1;
+      const bool vec_ok = ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0) &&
                           (direct ? (g.ldc % 4 == 0) : (g.N % 4 == 0));
       const bool mask_vec = g.mask != nullptr && (reinterpret_cast<uintptr_t>(g.mask) & 15) == 0 &&
                             g.ldm % 4 == 0;
+      // 32-column chunks: tcgen05.ld gives each lane one row; the chunk goes
+      // through this warp's shared buffer (16-byte chunks XOR-swizzled by
+      // row, conflict-free both ways) so that every global access below is
+      // four full 128-byte row segments per instruction (coalesced C / mask
+      // reads and stores).
+      const uint32_t xb = su32(epi_buf) + static_cast<uint32_t>(q) * (32 * 32 * 4);
+      const int rsub = lane >> 3, j4 = lane & 7;  // read-back role: row rsub + 4 i, chunk j4
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        float v[16], vc[16];
-        const uint32_t ta = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                            static_cast<uint32_t>(acc * C::NACC * BN + c);
-        tmem_ld16(ta, v);
-        if (!ONE) {
-          tmem_ld16(ta + BN, vc);
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        {
+          uint32_t rh[32], rc[32];
+          const uint32_t ta = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                              static_cast<uint32_t>(acc * C::NACC * BN + c);
+          tmem_ld32_nowait(ta, rh);
+          if (!ONE) tmem_ld32_nowait(ta + BN, rc);
+          tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], vc[i]);
+          for (int i = 0; i < 32; ++i)
+            v[i] = ONE ? __uint_as_float(rh[i])
+                       : __fadd_rn(__uint_as_float(rh[i]), __uint_as_float(rc[i]));
         }
-        if (row < g.M) {
-          const int64_t nb = n0 + c;
-          if (direct) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              float o = g.alpha * v[i];
-              if (g.beta != 0.0f && nb + i < g.N) o = fmaf(g.beta, crow[nb + i], o);
-              if (g.relu) o = fmaxf(o, 0.0f);
-              v[i] = o;
-            }
-            if (g.mask != nullptr) {  // ReLU backward of the layer below
-              const float *mrow = g.mask + row * g.ldm + nb;
-              if (mask_vec && nb + 16 <= g.N) {
+        for (int j = 0; j < 8; ++j)
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                           xb + lane * 128 + ((j ^ (lane & 7)) * 16)),
+                       "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                       : "memory");
+        __syncwarp();
+        const int64_t col = n0 + c + 4 * j4;
+        const bool col4 = col + 4 <= g.N;
+        const bool colok = col < g.N;
+        // all eight row passes' operands first, so their loads are in flight together
+        float4 o[8];
 #pragma unroll
-                for (int i = 0; i < 16; i += 4) {
-                  const float4 mk = __ldg(reinterpret_cast<const float4 *>(mrow + i));
-                  v[i] = mk.x > 0.0f ? v[i] : 0.0f;
-                  v[i + 1] = mk.y > 0.0f ? v[i + 1] : 0.0f;
-                  v[i + 2] = mk.z > 0.0f ? v[i + 2] : 0.0f;
-                  v[i + 3] = mk.w > 0.0f ? v[i + 3] : 0.0f;
-                }
+        for (int i = 0; i < 8; ++i) {
+          const int rr = 4 * i + rsub;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(o[i].x), "=f"(o[i].y), "=f"(o[i].z), "=f"(o[i].w)
+                       : "r"(xb + rr * 128 + ((j4 ^ (rr & 7)) * 16))
+                       : "memory");
+        }
+        __syncwarp();  // the buffer is rewritten by the next chunk
+        const int64_t grow0 = m0 + q * 32 + rsub;
+        if (direct && (g.mask != nullptr || g.beta != 0.0f)) {
+          float4 mk[8], cv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int64_t grow = grow0 + 4 * i;
+            const bool in = grow < g.M && colok;
+            mk[i] = make_float4(1.f, 1.f, 1.f, 1.f);
+            cv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (in && g.mask != nullptr && !(g.exp & 8)) {
+              const float *mp = g.mask + grow * g.ldm + col;
+              if (mask_vec && col4) {
+                mk[i] = __ldg(reinterpret_cast<const float4 *>(mp));
               } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                  if (nb + i < g.N && !(mrow[i] > 0.0f)) v[i] = 0.0f;
+                mk[i].x = mp[0];
+                if (col + 1 < g.N) mk[i].y = mp[1];
+                if (col + 2 < g.N) mk[i].z = mp[2];
+                if (col + 3 < g.N) mk[i].w = mp[3];
+              }
+            }
+            if (in && g.beta != 0.0f) {
+              const float *cp = g.C + grow * g.ldc + col;
+              if (vec_ok && col4) {
+                cv[i] = *reinterpret_cast<const float4 *>(cp);
+              } else {
+                cv[i].x = cp[0];
+                if (col + 1 < g.N) cv[i].y = cp[1];
+                if (col + 2 < g.N) cv[i].z = cp[2];
+                if (col + 3 < g.N) cv[i].w = cp[3];
               }
             }
           }
-          if (g.exp & 4) {
-          } else if (vec_ok && nb + 16 <= g.N) {
 #pragma unroll
-            for (int i = 0; i < 16; i += 4)
-              *reinterpret_cast<float4 *>(crow + nb + i) =
-                  make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          } else {
+          for (int i = 0; i < 8; ++i) {
+            float *ov = &o[i].x;
+            const float *m4 = &mk[i].x, *c4 = &cv[i].x;
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (nb + i < g.N) crow[nb + i] = v[i];
+            for (int e = 0; e < 4; ++e) {
+              float r = g.alpha * ov[e];
+              if (g.beta != 0.0f) r = fmaf(g.beta, c4[e], r);
+              if (g.relu) r = fmaxf(r, 0.0f);
+              if (g.mask != nullptr && !(m4[e] > 0.0f)) r = 0.0f;
+              ov[e] = r;
+            }
+          }
+        } else if (direct) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float *ov = &o[i].x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float r = g.alpha * ov[e];
+              if (g.relu) r = fmaxf(r, 0.0f);
+              ov[e] = r;
+            }
           }
         }
+        if (!(g.exp & 4)) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int64_t grow = grow0 + 4 * i;
+            if (grow >= g.M || !colok) continue;
+            float *cp = direct ? g.C + grow * g.ldc + col : g.C + (s * g.M + grow) * g.N + col;
+            if (vec_ok && col4) {
+              *reinterpret_cast<float4 *>(cp) = o[i];
+            } else {
+              cp[0] = o[i].x;
+              if (col + 1 < g.N) cp[1] = o[i].y;
+              if (col + 2 < g.N) cp[2] = o[i].z;
+              if (col + 3 < g.N) cp[3] = o[i].w;
+            }
+          }
+        }
+
       }
       tc_fence_before();
       __syncwarp();

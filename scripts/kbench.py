@@ -59,9 +59,43 @@ def main():
             torch.cuda.synchronize()
             continue
         ki, ke = (ag.KernelKind(k) for k in args.pair.split(","))
+        if args.only == "gemm_dh48":
+            q48 = torch.randn((V, 48), device="cuda")
+            w48 = torch.randn((256, 48), device="cuda")
+            mk = torch.randn((V, 256), device="cuda")
+            K.gemm(q48, w48, trans_b=True, relu_mask=mk)
+            torch.cuda.synchronize()
+            continue
         if args.only == "fused_pair":
             K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM, kernel_intra=ki, kernel_inter=ke)
             torch.cuda.synchronize()
+            continue
+        if args.suite == "gemm":
+            if F != args.feat[0]:
+                continue
+            g256 = torch.randn((V, 256), device="cuda")
+            h256 = torch.randn((V, 256), device="cuda")
+            x100 = torch.randn((V, 100), device="cuda")
+            q48 = torch.randn((V, 48), device="cuda")
+            w100 = torch.randn((100, 256), device="cuda")
+            w256 = torch.randn((256, 256), device="cuda")
+            w48 = torch.randn((256, 48), device="cuda")
+            shapes = {
+                "fwd_100x256": lambda: K.gemm(x100, w100),
+                "fwd_256x256": lambda: K.gemm(h256, w256),
+                "fwd_256x48": lambda: K.gemm(h256, w48),
+                "dW_256x48": lambda: K.gemm(h256, q48, trans_a=True),
+                "dH_48x256_mask": lambda: K.gemm(q48, w48, trans_b=True, relu_mask=h256),
+                "dW_256x256": lambda: K.gemm(h256, g256, trans_a=True),
+                "dH_256x256": lambda: K.gemm(g256, w256, trans_b=True),
+                "dW_100x256": lambda: K.gemm(x100, g256, trans_a=True),
+            }
+            res = {k: timeit(fn) for k, fn in shapes.items()}
+            ref = h256[:4096].double() @ w256.double()
+            got = K.gemm(h256, w256)[:4096].double()
+            out["gemm_relerr"] = float(((got - ref).abs() / ref.abs().clamp(min=1.0)).max())
+            out["gemm_ms"] = {k: round(v, 4) for k, v in res.items()}
+            out["gemm_total_ms"] = round(sum(res.values()), 3)
             continue
         if args.suite == "agg":
             ba = bench.bytes_alg(V, E, F, rg.weights is not None)
