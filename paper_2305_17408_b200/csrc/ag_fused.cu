@@ -65,6 +65,7 @@ constexpr int kSlots = 41;   // X ring capacity in blocks (window H <= (kSlots -
 constexpr int kFarSlots = 4; // far ring: staged out-of-window sources of the next blocks
 constexpr int kFarMax = 20;  // staged far sources per block (more: read from global)
 constexpr int kReluSlots = 4;  // ReLU-mask operand tiles staged ahead (backward epilogue)
+constexpr int kRG = 1;       // consecutive rows a consumer warp takes at a time (divides kRB)
 constexpr int kISlots = 4;   // dense-intra mode: per-block intra results (16 rows x tile)
 constexpr int kReady = 16;   // per-block "ready" barriers (X window + far rows staged)
 constexpr int kDone = 32;    // per-block "done" barriers (every consumer left the block)
@@ -1121,10 +1122,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int32_t ed = inf.x + h * 32 + lane;
           return ed < inf.z ? __ldg(a.cv + ed) : make_int2(0, 0);
         };
-        uint32_t rr = r0 + warp;
+        // rows go to warps in groups of kRG consecutive rows (one block
+        // change per group instead of per row); a warp's next row:
+        auto next_row = [&](uint32_t r) -> uint32_t {
+          return (r % kRG != kRG - 1) ? r + 1 : r + (NC - 1) * kRG + 1;
+        };
+        uint32_t rr = r0 + warp * kRG;
         int4 info = info_at(rr);
         int2 q0 = pairs_at(info, 0), q1 = pairs_at(info, 1);
-        int4 info1 = info_at(rr + NC);
+        uint32_t rn = next_row(rr);
+        int4 info1 = info_at(rn);
         uint32_t kcur = kb0;
         // entering block k: its X window and far rows (ready), and in
         // dense-intra mode its intra partials
@@ -1132,15 +1139,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(bs.rdy(k), bs.rdy_phase(k));
           if (DENSE) mbar_wait(ivalid + ((k - kb0) % kISlots) * 8, ((k - kb0) / kISlots) & 1u);
         };
-        enter(kb0);
+        bool entered = false;
 #pragma unroll 1
-        for (; rr < r1; rr += NC) {
+        for (; rr < r1; rr = rn, rn = next_row(rn)) {
           const uint32_t k = rr / kRB;
-          while (kcur != k) {  // leave block kcur, enter the next
+          if (kcur != k || !entered) {  // leave the blocks before k (rows or not), enter k
             __syncwarp();
-            if (lane == 0) mbar_arrive(done + ((kcur - kb0) % kDone) * 8);
-            ++kcur;
-            enter(kcur);
+            for (; kcur != k; ++kcur)
+              if (lane == 0) mbar_arrive(done + ((kcur - kb0) % kDone) * 8);
+            enter(k);
+            entered = true;
           }
           const int32_t s = info.x, e = info.z;
           const int32_t m =
@@ -1151,7 +1159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           else w.template install<false>(s, q0, q1);
           // next row's pairs and the row after next's bounds
           const int2 n0 = pairs_at(info1, 0), n1 = pairs_at(info1, 1);
-          const int4 info2 = info_at(rr + 2 * NC);
+          const int4 info2 = info_at(next_row(rn));
           float *yrow;  // ylane + rr * ld as one IMAD.WIDE.U32
           asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(yrow) : "r"(rr), "r"(ld * 4u), "l"(ylane));
           const uint32_t relu_s = ring + G::kReluOff + ((k - kb0) % kReluSlots) * G::kSlotBytes +
@@ -1164,12 +1172,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           q0 = n0;
           q1 = n1;
         }
-        while (true) {
-          __syncwarp();
+        __syncwarp();
+        for (; kcur < kb1; ++kcur)  // leave the rest of the range
           if (lane == 0) mbar_arrive(done + ((kcur - kb0) % kDone) * 8);
-          if (++kcur >= kb1) break;
-          enter(kcur);
-        }
       }
     }
     __syncthreads();
