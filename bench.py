@@ -175,8 +175,9 @@ class HostFeeder:
 
 def ncu_traffic():
     """DRAM bytes of one F=256 aggregation launch from the committed ncu
-    capture (profiles/r01_ncu_slab_gemm.json), or (None, reason)."""
-    p = ROOT / "profiles" / "r01_ncu_slab_gemm.json"
+    capture of the pair the autotune runs (profiles/r01_ncu_dense_pair.json),
+    or (None, reason)."""
+    p = ROOT / "profiles" / "r01_ncu_dense_pair.json"
     if not p.exists():
         return None, "no ncu capture committed"
     d = json.loads(p.read_text())
@@ -412,7 +413,9 @@ def run_ours(args, cfg):
             "traffic_per": "one F=256 aggregation launch (dram read + write bytes)",
             "traffic_source": traffic_src,
             "per_width": widths,
-            "kernel": "slab_kernel (ag_fused_spmm: both roles + fused combine, bitwise reduceat order)",
+            "kernel": "slab_kernel (ag_fused_spmm: the autotuned selector pair of each width in one "
+                      "pass -- intra role (dense 16x16 block product or bitwise CSR) + bitwise "
+                      "csr_inter role + fused combine / epilogues; pairs in config.kernels)",
             "aggregations_per_step": n_agg // args.steps,
             "agg_ms_per_step": round(agg_ms / args.steps, 4),
             "algorithmic_bytes_per_step": agg_bytes // args.steps,
