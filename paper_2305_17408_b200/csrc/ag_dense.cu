@@ -210,39 +210,49 @@ constexpr int kXentLd = 64;
 __global__ void __launch_bounds__(kXentThreads) xent_rows_kernel(
     int64_t rows, int64_t C, int64_t ld, const float *logits, const int32_t *labels,
     const uint8_t *mask, float inv_n, double *partial, float *dlogits) {
-  extern __shared__ float zs[];  // kXentThreads * ld
+  extern __shared__ float zs[];  // kXentThreads * (ld + 1)
   __shared__ double tsum[kXentThreads];
   const int t = threadIdx.x;
   double acc = 0.0;
   for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * kXentThreads; r0 < rows;
        r0 += static_cast<int64_t>(gridDim.x) * kXentThreads) {
     const int64_t nr = rows - r0 < kXentThreads ? rows - r0 : static_cast<int64_t>(kXentThreads);
-    const int64_t n = nr * ld;  // multiple of 4 (ld % 4 == 0)
-    const float4 *src = reinterpret_cast<const float4 *>(logits + r0 * ld);
-    for (int64_t i = t; i < n / 4; i += kXentThreads) reinterpret_cast<float4 *>(zs)[i] = src[i];
+    const int64_t n = nr * ld;
+    const int64_t lp = ld + 1;  // odd row stride in shared memory: conflict-free per-thread rows
+    const float *src = logits + r0 * ld;
+    const int ni = static_cast<int>(n), li = static_cast<int>(ld), lpi = li + 1;
+    for (int i = t; i < ni; i += kXentThreads) zs[(i / li) * lpi + i % li] = src[i];
     __syncthreads();
     if (t < nr) {
-      float *z = zs + static_cast<int64_t>(t) * ld;
+      float *z = zs + static_cast<int64_t>(t) * lp;
       const int64_t r = r0 + t;
       if (mask && mask[r] == 0) {
         for (int64_t c = 0; c < C; ++c) z[c] = 0.0f;
       } else {
-        float mx = -INFINITY;
-        for (int64_t c = 0; c < C; ++c) mx = fmaxf(mx, z[c]);
+        const int ci = static_cast<int>(C);
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        int c = 0;
+        for (; c + 4 <= ci; c += 4)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) m4[j] = fmaxf(m4[j], z[c + j]);
+        for (; c < ci; ++c) m4[0] = fmaxf(m4[0], z[c]);
+        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
         float se = 0.0f;
-        for (int64_t c = 0; c < C; ++c) se += expf(z[c] - mx);
+#pragma unroll 8
+        for (int cc = 0; cc < ci; ++cc) se += expf(z[cc] - mx);
         const int32_t y = labels[r];
         acc += static_cast<double>(mx + logf(se) - z[y]);
         const float inv_se = 1.0f / se;
-        for (int64_t c = 0; c < C; ++c) {
-          const float pr = expf(z[c] - mx) * inv_se;
-          z[c] = (pr - (c == y ? 1.0f : 0.0f)) * inv_n;
+#pragma unroll 8
+        for (int cc = 0; cc < ci; ++cc) {
+          const float pr = expf(z[cc] - mx) * inv_se;
+          z[cc] = (pr - (cc == y ? 1.0f : 0.0f)) * inv_n;
         }
       }
     }
     __syncthreads();
-    float4 *dst = reinterpret_cast<float4 *>(dlogits + r0 * ld);
-    for (int64_t i = t; i < n / 4; i += kXentThreads) dst[i] = reinterpret_cast<float4 *>(zs)[i];
+    float *dst = dlogits + r0 * ld;
+    for (int i = t; i < ni; i += kXentThreads) dst[i] = zs[(i / li) * lpi + i % li];
     __syncthreads();
   }
   tsum[t] = acc;
@@ -325,19 +335,17 @@ extern "C" int ag_softmax_xent(int64_t rows, int64_t C, int64_t ld, const float 
   if (rows < 0 || C < 1 || ld < C) return fail(AG_ERR_VALUE, "bad loss sizes");
   cudaStream_t st = as_stream(stream);
   const float inv_n = num_masked > 0 ? 1.0f / static_cast<float>(num_masked) : 0.0f;
-  const bool narrow = ld <= kXentLd && ld % 4 == 0 &&
-                      (reinterpret_cast<uintptr_t>(logits) & 15) == 0 &&
-                      (reinterpret_cast<uintptr_t>(dlogits) & 15) == 0;
+  const bool narrow = ld <= kXentLd;
   int64_t ctas;
   Scratch part;
   if (narrow) {
     // rows per CTA chunk = kXentThreads; ~2 chunks per CTA in flight per SM slot
-    const size_t smem = static_cast<size_t>(kXentThreads) * ld * sizeof(float);
+    const size_t smem = static_cast<size_t>(kXentThreads) * (ld + 1) * sizeof(float);
     ctas = std::max<int64_t>(1, std::min<int64_t>((rows + kXentThreads - 1) / kXentThreads,
                                                   static_cast<int64_t>(sm_count()) * 4));
     AG_CUDA(part.alloc(ctas * sizeof(double), st));
     AG_CUDA(cudaFuncSetAttribute(xent_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(kXentThreads * kXentLd * sizeof(float))));
+                                 static_cast<int>(kXentThreads * (kXentLd + 1) * sizeof(float))));
     xent_rows_kernel<<<static_cast<unsigned>(ctas), kXentThreads, smem, st>>>(
         rows, C, ld, logits, labels, mask, inv_n, part.as<double>(), dlogits);
     AG_LAUNCH_CHECK("xent_rows_kernel");

@@ -27,6 +27,7 @@
 //                 K=8 step), tcgen05.commit frees ring slots / publishes tiles
 //   warps 6-9     epilogue: tcgen05.ld 32x32b -> alpha/beta/ReLU -> global,
 //                 double-buffered TMEM accumulators so it overlaps the next tile
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -49,7 +50,10 @@ constexpr int kKRow = BK * 4;                       // bytes per K-major row
 constexpr uint64_t kKLayout = BK == 32 ? 2ull : 4ull;  // SWIZZLE_128B / SWIZZLE_64B
 constexpr uint32_t kKSbo = 8 * kKRow;               // 8-row swizzle atom
 constexpr uint32_t kMnBox = 128 * BK;               // MN-major TMA box {32 mn, BK k} bytes
-constexpr int kThreads = 320;
+// warps: 0 TMA, 1 MMA, 2-5 splitters, 6-13 epilogue (two per TMEM lane quarter, each
+// taking half of the tile's columns: the epilogue bounds short-K products)
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = (6 + kEpiWarps) * 32;
 constexpr int kConvWarp0 = 2, kEpiWarp0 = 6;
 
 struct TcArgs {
@@ -66,7 +70,17 @@ struct TcArgs {
   const float *mask;  // ReLU-backward mask operand (NULL: none): out = mask > 0 ? out : 0
   int64_t ldm;
   int64_t k_per_split;  // multiple of BK
+  long long *trace;     // AG_TC_TRACE: per-tile clock stamps of CTA 0 (development only)
 };
+constexpr int kTraceTiles = 48;
+// CTA 0 stamps (globaltimer, ns): [tile][0] MMA tempty-wait start, [1] its end, [2] MMA's
+// last k-block issued, [3] epilogue tfull-wait start, [4] its end, [5] epilogue done;
+// [6..] the MMA warp's conv waits of the tile's first two k-blocks (start, end)
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // ------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ uint32_t su32(const void *p) {
@@ -218,8 +232,8 @@ struct Cfg {
   static constexpr int COLS = ACC_BUFS * NACC * BN;
   static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128
                                  : COLS <= 256 ? 256 : 512;
-  // epilogue transpose buffers: 4 warps x (32 rows x 32 fp32)
-  static constexpr int EPI = 4 * 32 * 32 * 4;
+  // epilogue transpose buffers: kEpiWarps x (32 rows x 32 fp32)
+  static constexpr int EPI = kEpiWarps * 32 * 32 * 4;
   static constexpr int SMEM = STAGES * STAGE + 1024 /* align */ + 256 /* barriers */ + EPI;
 };
 
@@ -299,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -343,6 +357,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           unsigned char *st = smem + stage * C::STAGE;
           unsigned char *sa = st, *sb = st + 2 * C::A_BYTES;
+          if (g.exp & 32) {  // experiment: no operand traffic, handoffs only
+            mbar_expect_tx(&full[stage], 0);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           mbar_expect_tx(&full[stage], C::A_BYTES + (g.b_presplit ? 2 : 1) * C::B_BYTES);
           const int kk = static_cast<int>(k0 + static_cast<int64_t>(kb) * BK);
           if (A_MN) {  // boxes {32 (m), 32 (k)}: 4 KB each, LBO apart
@@ -384,14 +403,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int64_t t = cid; t < total; t += ncl) {
       int64_t k0;
       const int nkb = tile_kblocks(t, k0);
+      const int ti = static_cast<int>((t - cid) / ncl);
+      const bool tr = g.trace != nullptr && blockIdx.x == 0 && lane == 0 && ti < kTraceTiles;
+      if (tr) g.trace[ti * 10 + 0] = gtime();
       mbar_wait(&tempty[acc], acc_phase ^ 1);
+      if (tr) g.trace[ti * 10 + 1] = gtime();
       tc_fence_after();
       const uint32_t d = tmem_base + static_cast<uint32_t>(acc * C::NACC * BN);  // hi*hi
       const uint32_t dc = ONE ? d : d + BN;                                     // correction
       for (int kb = 0; kb < nkb; ++kb) {
+        if (tr && kb < 2) g.trace[ti * 10 + 6 + 2 * kb] = gtime();
         mbar_wait(&conv[stage], phase);
+        if (tr && kb < 2) g.trace[ti * 10 + 7 + 2 * kb] = gtime();
         tc_fence_after();
         if (lane == 0) {
+          if (tr && kb == nkb - 1) g.trace[ti * 10 + 2] = gtime();
           const uint32_t st = su32(smem + stage * C::STAGE);
           const uint32_t a_hi = st, a_lo = st + C::A_BYTES;
           const uint32_t b_hi = st + 2 * C::A_BYTES, b_lo = b_hi + C::B_BYTES;
@@ -410,11 +436,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t dbh = smem_desc(b_hi + bo, blbo, bsbo, B_MN);
             const uint64_t dbl = smem_desc(b_lo + bo, blbo, bsbo, B_MN);
             const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
-            if (!(g.exp & 2)) {
+            if (!(g.exp & 18)) {
               tc_mma_tf32(dc, dal, dbh, idesc, first);
               tc_mma_tf32(dc, dah, dbl, idesc, 1u);
             }
-            tc_mma_tf32(d, dah, dbh, idesc, ONE ? 1u : first);
+            if (!(g.exp & 16)) tc_mma_tf32(d, dah, dbh, idesc, ONE ? 1u : first);
           }
           if (CL == 1) tc_commit(&empty[stage]);
           else tc_commit_mc(&empty[stage], kAll);  // the stage is free in every CTA's view
@@ -459,6 +485,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // -------------------------------------------------------- epilogue ---
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int ehalf = (warp - kEpiWarp0) >> 2;  // which half of the tile's columns
+    constexpr int kHalfCols = BN >= 64 ? BN / 2 : BN;
+    const int c_lo = ehalf * kHalfCols, c_hi = BN >= 64 ? c_lo + kHalfCols : (ehalf ? 0 : BN);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t t = cid; t < total; t += ncl) {
@@ -466,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t m0 = tile_m0(t);
       const int64_t n0 = tile_n0(t);
       const int64_t row = m0 + q * 32 + lane;
-      if (g.mask != nullptr && g.splits == 1 && (g.ldm % 4) == 0) {
+      if (g.mask != nullptr && g.splits == 1 && (g.ldm % 4) == 0 && ehalf == 0) {
         // pull this row's mask segment of the NEXT tile into L2 (a whole tile
         // period ahead of its use; the first tile's own segment too)
         auto prefetch_mask = [&](int64_t tt) {
@@ -485,7 +514,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t == cid) prefetch_mask(t);
         prefetch_mask(t + ncl);
       }
+      const int ti = static_cast<int>((t - cid) / ncl);
+      const bool tr = g.trace != nullptr && blockIdx.x == 0 && warp == kEpiWarp0 && lane == 0 &&
+                      ti < kTraceTiles;
+      if (tr) g.trace[ti * 10 + 3] = gtime();
       mbar_wait(&tfull[acc], acc_phase);
+      if (tr) g.trace[ti * 10 + 4] = gtime();
       tc_fence_after();
       const bool direct = g.splits == 1;
       const bool vec_ok = ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0) &&
@@ -497,10 +531,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // row, conflict-free both ways) so that every global access below is
       // four full 128-byte row segments per instruction (coalesced C / mask
       // reads and stores).
-      const uint32_t xb = su32(epi_buf) + static_cast<uint32_t>(q) * (32 * 32 * 4);
+      const uint32_t xb = su32(epi_buf) + static_cast<uint32_t>(warp - kEpiWarp0) * (32 * 32 * 4);
       const int rsub = lane >> 3, j4 = lane & 7;  // read-back role: row rsub + 4 i, chunk j4
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = c_lo; c < c_hi; c += 32) {
         float v[32];
         {
           uint32_t rh[32], rc[32];
@@ -537,40 +571,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();  // the buffer is rewritten by the next chunk
         const int64_t grow0 = m0 + q * 32 + rsub;
         if (direct && (g.mask != nullptr || g.beta != 0.0f)) {
-          float4 mk[8], cv[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int hf = 0; hf < 8; hf += 4) {  // four passes' loads in flight at a time
+          float4 mk[4], cv[4];
+#pragma unroll
+          for (int i0 = 0; i0 < 4; ++i0) {
+            const int i = hf + i0;
             const int64_t grow = grow0 + 4 * i;
             const bool in = grow < g.M && colok;
-            mk[i] = make_float4(1.f, 1.f, 1.f, 1.f);
-            cv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            mk[i0] = make_float4(1.f, 1.f, 1.f, 1.f);
+            cv[i0] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (in && g.mask != nullptr && !(g.exp & 8)) {
               const float *mp = g.mask + grow * g.ldm + col;
               if (mask_vec && col4) {
-                mk[i] = __ldg(reinterpret_cast<const float4 *>(mp));
+                mk[i0] = __ldg(reinterpret_cast<const float4 *>(mp));
               } else {
-                mk[i].x = mp[0];
-                if (col + 1 < g.N) mk[i].y = mp[1];
-                if (col + 2 < g.N) mk[i].z = mp[2];
-                if (col + 3 < g.N) mk[i].w = mp[3];
+                mk[i0].x = mp[0];
+                if (col + 1 < g.N) mk[i0].y = mp[1];
+                if (col + 2 < g.N) mk[i0].z = mp[2];
+                if (col + 3 < g.N) mk[i0].w = mp[3];
               }
             }
             if (in && g.beta != 0.0f) {
               const float *cp = g.C + grow * g.ldc + col;
               if (vec_ok && col4) {
-                cv[i] = *reinterpret_cast<const float4 *>(cp);
+                cv[i0] = *reinterpret_cast<const float4 *>(cp);
               } else {
-                cv[i].x = cp[0];
-                if (col + 1 < g.N) cv[i].y = cp[1];
-                if (col + 2 < g.N) cv[i].z = cp[2];
-                if (col + 3 < g.N) cv[i].w = cp[3];
+                cv[i0].x = cp[0];
+                if (col + 1 < g.N) cv[i0].y = cp[1];
+                if (col + 2 < g.N) cv[i0].z = cp[2];
+                if (col + 3 < g.N) cv[i0].w = cp[3];
               }
             }
           }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i0 = 0; i0 < 4; ++i0) {
+            const int i = hf + i0;
             float *ov = &o[i].x;
-            const float *m4 = &mk[i].x, *c4 = &cv[i].x;
+            const float *m4 = &mk[i0].x, *c4 = &cv[i0].x;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               float r = g.alpha * ov[e];
@@ -579,6 +617,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (g.mask != nullptr && !(m4[e] > 0.0f)) r = 0.0f;
               ov[e] = r;
             }
+          }
           }
         } else if (direct) {
 #pragma unroll
@@ -612,6 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
+      if (tr) g.trace[ti * 10 + 5] = gtime();
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == C::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
     }
@@ -836,6 +876,12 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
     g.C = C;
     g.ldc = ldc;
   }
+  long long *trace = nullptr;
+  if (std::getenv("AG_TC_TRACE")) {
+    AG_CUDA(cudaMalloc(&trace, kTraceTiles * 10 * sizeof(long long)));
+    AG_CUDA(cudaMemset(trace, 0, kTraceTiles * 10 * sizeof(long long)));
+    g.trace = trace;
+  }
   switch (bn) {
     case 32: rc = launch_bn<32>(a_mn, b_mn, ma, mb, mbl, g, cl, st); break;
     case 64: rc = launch_bn<64>(a_mn, b_mn, ma, mb, mbl, g, cl, st); break;
@@ -843,6 +889,23 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
     default: rc = launch_bn<256>(a_mn, b_mn, ma, mb, mbl, g, cl, st); break;
   }
   if (rc) return rc;
+  if (trace) {
+    long long h[kTraceTiles * 10];
+    AG_CUDA(cudaStreamSynchronize(st));
+    AG_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
+    cudaFree(trace);
+    const long long t0 = h[0];
+    std::fprintf(stderr, "tc_gemm trace M=%lld N=%lld K=%lld bn=%d (us from first stamp)\n",
+                 (long long)M, (long long)N, (long long)K, bn);
+    for (int i = 0; i < kTraceTiles; ++i) {
+      if (!h[i * 10]) break;
+      std::fprintf(stderr, "tile %2d mma: tempty %.2f..%.2f conv0 %.2f..%.2f conv1 %.2f..%.2f last %.2f"
+                   " | epi: tfull %.2f..%.2f done %.2f\n", i,
+                   (h[i*10+0]-t0)/1e3, (h[i*10+1]-t0)/1e3, (h[i*10+6]-t0)/1e3, (h[i*10+7]-t0)/1e3,
+                   (h[i*10+8]-t0)/1e3, (h[i*10+9]-t0)/1e3, (h[i*10+2]-t0)/1e3,
+                   (h[i*10+3]-t0)/1e3, (h[i*10+4]-t0)/1e3, (h[i*10+5]-t0)/1e3);
+    }
+  }
   if (splits > 1) {
     splitk_sum_kernel<<<grid_for(M * N, 256), 256, 0, st>>>(M, N, splits, g.C, C, ldc, alpha,
                                                             beta, g.relu, mask, ldm);

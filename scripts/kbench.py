@@ -91,6 +91,13 @@ def main():
                 "dW_100x256": lambda: K.gemm(x100, g256, trans_a=True),
             }
             res = {k: timeit(fn) for k, fn in shapes.items()}
+            import os
+            if os.environ.get("KB_GEMM_EXP"):
+                for ex in os.environ["KB_GEMM_EXP"].split(","):
+                    os.environ["AG_TC_EXP"] = ex
+                    for k in ("dH_48x256_mask", "fwd_256x256", "fwd_100x256"):
+                        res[f"{k}[exp{ex}]"] = timeit(shapes[k])
+                os.environ.pop("AG_TC_EXP")
             ref = h256[:4096].double() @ w256.double()
             got = K.gemm(h256, w256)[:4096].double()
             out["gemm_relerr"] = float(((got - ref).abs() / ref.abs().clamp(min=1.0)).max())

@@ -35,7 +35,18 @@ obj = os.path.abspath("build/csrc/" + srcfile.split("/")[-1] + ".o")
 subprocess.run(["cuobjdump", "-xelf", "all", obj], capture_output=True, cwd="/tmp")
 cub = "/tmp/" + srcfile.split("/")[-1].replace(".cu", ".sm_100a.cubin")
 txt = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout.split("\n")
-starts = [i for i, l in enumerate(txt) if l.strip().startswith(".section") and ".text." in l and re.search(kre, l)]
+# the profiled kernel's own (mangled) name, so template instances do not mix
+mangled = ""
+rawm = subprocess.run(["ncu", "-i", rep, "--print-kernel-base", "mangled", "--page", "raw", "--csv"],
+                      capture_output=True, text=True).stdout
+rm = list(csv.reader(io.StringIO(rawm)))
+if len(rm) > 2:
+    mangled = dict(zip(rm[0], rm[2])).get("Kernel Name", "")
+starts = [i for i, l in enumerate(txt) if l.strip().startswith(".section") and ".text." in l
+          and (mangled and (".text." + mangled) in l)]
+if not starts:
+    starts = [i for i, l in enumerate(txt) if l.strip().startswith(".section") and ".text." in l
+              and re.search(kre, l)]
 m = {}
 line = None
 for l in txt[starts[0] + 1:]:
