@@ -58,8 +58,13 @@ using namespace ptx;
 constexpr int kLeafN = 128;  // numpy PW_BLOCKSIZE
 constexpr int kDepth = 40;
 constexpr int kRB = 16;      // rows per ring block
-constexpr int kCons = 14;    // consumer warps; + 2 producer warps = 16 (4 per SMSP, 128 regs)
-constexpr int kThreads = (kCons + 2) * 32;
+// consumer warps per CTA (+ 2 producer warps): 14 -> 16 warps, 4 per SMSP at 128 registers
+// for the exact-order modes; the order-free inter modes (AG_EPI_INTER_COO) need fewer
+// registers: with the intra role on the dense warps (kModeDense3Coo) the consumers run
+// 16 + 2 warps at 96 registers (measured faster; the exact-order code spills there)
+constexpr int kConsMax = 16;
+template <int MODE>
+constexpr int cons_warps();
 constexpr int kWin = 64;     // topology items per window refill (two per lane)
 constexpr int kSlots = 41;   // X ring capacity in blocks (window H <= (kSlots - 9) / 2 = 16)
 constexpr int kFarSlots = 4; // far ring: staged out-of-window sources of the next blocks
@@ -648,6 +653,8 @@ constexpr int kModeSum3Coo = 4;
 constexpr int kModeDense3Coo = 5;
 __host__ __device__ constexpr bool mode_dense(int m) { return m == kModeDense3 || m == kModeDense3Coo; }
 __host__ __device__ constexpr bool mode_coo(int m) { return m == kModeSum3Coo || m == kModeDense3Coo; }
+template <int MODE>
+constexpr int cons_warps() { return MODE == kModeDense3Coo ? kConsMax : 14; }
 __host__ __device__ constexpr bool mode_sum3(int m) {
   return m == kModeSum3 || m == kModeDense3 || mode_coo(m);
 }
@@ -730,7 +737,7 @@ struct SlabGeom {
   static constexpr uint32_t kWOff = kIOff + kISlots * kSlotBytes;  // 2 warps x 2 x 512 B weights
   static constexpr uint32_t kRingBytes = kWOff + 2 * 1024;
   static constexpr uint32_t kBarBytes = (kReady + kDone + kISlots) * 8;
-  static constexpr uint32_t kWinBytes = kCons * kWin * 8;
+  static constexpr uint32_t kWinBytes = kConsMax * kWin * 8;
   static constexpr size_t kSmem = kRingBytes + kBarBytes + kWinBytes;
 };
 
@@ -1051,7 +1058,7 @@ __device__ __forceinline__ void dense_intra(const GArgs &a, uint32_t ring, const
 }
 
 template <int VEC, int MODE, bool W>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
     slab_kernel(const __grid_constant__ CUtensorMap tmap,
                 const __grid_constant__ CUtensorMap relu_map, GArgs a) {
   using G = SlabGeom<VEC>;
@@ -1063,6 +1070,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t ivalid = done + kDone * 8;  // dense-intra mode: I slot of block k written
   const uint32_t wins = ivalid + kISlots * 8;
   constexpr bool DENSE = mode_dense(MODE);
+  constexpr int kCons = cons_warps<MODE>();
   constexpr int NC = DENSE ? kCons - kDenseWarps : kCons;  // consumer warps (dense warps last)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -1270,7 +1278,8 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
   if (a.feat % 4 == 0 && env_int("AG_SLAB_NO_TMA", 0) == 0 && encode(&map, a.x, a.x_rows) &&
       (!a.relu || encode(&relu_map, a.ep.relu_src, a.rows)))
     a.tma = 1;
-  k<<<grid, kThreads, smem, st>>>(map, relu_map, a);
+  const int threads = (mode == kModeDense3Coo ? kConsMax : 14) * 32 + 64;
+  k<<<grid, threads, smem, st>>>(map, relu_map, a);
   AG_LAUNCH_CHECK("slab_kernel");
   return AG_OK;
 }
