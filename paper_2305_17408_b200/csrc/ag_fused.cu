@@ -104,8 +104,10 @@ struct GArgs {
   int64_t x_rows;           // rows of x (>= rows: a rank's halo rows follow its own)
   int64_t xblocks;          // ceil(x_rows / 16)
   int tma;                  // 1: TMA tensor loads; 0: cp.async element copies
+  int sleep;                // producers' done waits: 1 suspend between polls, 0 spin
   int dbg;                  // development knob (AG_SLAB_DEBUG bits, values then garbage): 1 skip the
-                            // reductions, 2 far copies, 4 dense products, 8 X tiles
+                            // reductions, 2 far copies, 4 dense products, 8 X tiles, 16 Y stores,
+                            // 32 consumer topology loads
 };
 
 // ---------------------------------------------------------- packed fp32x2 --
@@ -130,13 +132,6 @@ __device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b, uint64_t one) {
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(b), "l"(one));
   return a;
 }
-__device__ __forceinline__ uint64_t add2_if(uint64_t acc, uint64_t c, uint64_t one, bool on) {
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q fma.rn.f32x2 %0, %0, %1, %2;\n\t}"
-      : "+l"(acc)
-      : "l"(one), "l"(c), "r"(static_cast<int>(on)));
-  return acc;
-}
-
 // A lane's slice of one row: VEC consecutive columns as packed fp32 pairs.
 template <int VEC>
 struct Lv {
@@ -168,18 +163,6 @@ __device__ __forceinline__ Lv<VEC> lv_add(const Lv<VEC> &a, const Lv<VEC> &b, ui
   } else {
 #pragma unroll
     for (int i = 0; i < Lv<VEC>::NP; ++i) r.p[i] = add2(a.p[i], b.p[i], one);
-  }
-  return r;
-}
-template <int VEC>
-__device__ __forceinline__ Lv<VEC> lv_add_if(const Lv<VEC> &a, const Lv<VEC> &b, uint64_t one,
-                                             bool on) {
-  Lv<VEC> r;
-  if constexpr (VEC == 1) {
-    r.s = on ? __fadd_rn(a.s, b.s) : a.s;
-  } else {
-#pragma unroll
-    for (int i = 0; i < Lv<VEC>::NP; ++i) r.p[i] = add2_if(a.p[i], b.p[i], one, on);
   }
   return r;
 }
@@ -723,7 +706,7 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
 #pragma unroll
     for (int i = 0; i < VEC; ++i) out.v[i] = h.v[i] > 0.0f ? out.v[i] : 0.0f;
   }
-  stv<VEC>(yp, out);
+  if (!(a.dbg & 16)) stv<VEC>(yp, out);
 }
 
 template <int VEC>
@@ -797,6 +780,7 @@ __device__ __forceinline__ void mbar_expect_tx_only(uint32_t b, uint32_t bytes) 
 // leaves blocks in order), so waiting on done[j] covers every block <= j.
 struct BlockSync {
   uint32_t ready, done, kb0;
+  int sleep;  // wait_done suspends between polls (1) or spins (0)
   __device__ __forceinline__ uint32_t rdy(uint32_t k) const {
     return ready + ((k - kb0) % kReady) * 8;
   }
@@ -804,7 +788,8 @@ struct BlockSync {
     return ((k - kb0) / kReady) & 1u;
   }
   __device__ __forceinline__ void wait_done(uint32_t k) const {
-    mbar_wait_sleep(done + ((k - kb0) % kDone) * 8, ((k - kb0) / kDone) & 1u);
+    if (sleep) mbar_wait_sleep(done + ((k - kb0) % kDone) * 8, ((k - kb0) / kDone) & 1u);
+    else mbar_wait(done + ((k - kb0) % kDone) * 8, ((k - kb0) / kDone) & 1u);
   }
 };
 
@@ -1094,7 +1079,7 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
     const uint32_t kb0 = static_cast<uint32_t>(s_kb[0]), kb1 = static_cast<uint32_t>(s_kb[1]);
     const uint32_t Llo = kb0 > H ? kb0 - H : 0u;
     const uint32_t Lhi = static_cast<uint32_t>(std::min<int64_t>(a.xblocks, int64_t(kb1) + H));
-    const BlockSync bs{ready, done, kb0};
+    const BlockSync bs{ready, done, kb0, a.sleep};
     if (kb0 < kb1) {
       if (warp == kCons) {
         produce_x<VEC>(a, &tmap, ring, bs, Llo, Lhi, kb0, kb1, H, tile, lane);
@@ -1125,10 +1110,13 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
         // the current row's reduction and only moved after it, so each load
         // has a full row of work to land.
         const int4 zero4 = make_int4(0, 0, 0, 0);
-        auto info_at = [&](uint32_t rr) -> int4 { return rr < r1 ? __ldg(a.rowinfo + rr) : zero4; };
+        const bool notopo = (a.dbg & 32) != 0;  // experiment: rows without topology loads
+        auto info_at = [&](uint32_t rr) -> int4 {
+          return (rr < r1 && !notopo) ? __ldg(a.rowinfo + rr) : zero4;
+        };
         auto pairs_at = [&](const int4 &inf, int h) -> int2 {
           const int32_t ed = inf.x + h * 32 + lane;
-          return ed < inf.z ? __ldg(a.cv + ed) : make_int2(0, 0);
+          return (ed < inf.z && !notopo) ? __ldg(a.cv + ed) : make_int2(0, 0);
         };
         // rows go to warps in groups of kRG consecutive rows (one block
         // change per group instead of per row); a warp's next row:
@@ -1243,6 +1231,7 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
                : (wt ? slab_kernel<VEC, kModeAny, true> : slab_kernel<VEC, kModeAny, false>);
   a.H = window;
   a.dbg = env_int("AG_SLAB_DEBUG", 0);
+  a.sleep = env_int("AG_SLAB_SLEEP", 1);
   a.nblocks = (a.rows + kRB - 1) / kRB;
   a.xblocks = (a.x_rows + kRB - 1) / kRB;
   a.ntiles = static_cast<int>((a.feat + G::T - 1) / G::T);

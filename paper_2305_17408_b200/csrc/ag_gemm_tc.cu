@@ -169,20 +169,6 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, ui
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-      "%11, %12, %13, %14, %15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
 // 32 consecutive fp32 columns of this lane's TMEM row, no wait (the caller
 // issues tmem_wait_ld() once for several loads)
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
@@ -494,7 +480,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t s = t / tiles_mn;
       const int64_t m0 = tile_m0(t);
       const int64_t n0 = tile_n0(t);
-      const int64_t row = m0 + q * 32 + lane;
       if (g.mask != nullptr && g.splits == 1 && (g.ldm % 4) == 0 && ehalf == 0) {
         // pull this row's mask segment of the NEXT tile into L2 (a whole tile
         // period ahead of its use; the first tile's own segment too)
