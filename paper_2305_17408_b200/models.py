@@ -429,8 +429,9 @@ class GraphedTrainStep:
     buffer set k and returns its loss tensor (valid after the stream reaches
     it).  Graphs share one memory pool and must replay in capture order
     modulo len(inputs), which a ring of buffers does.  Capturing runs
-    `warmup` eager steps per buffer set first (they update the weights like
-    any training step).
+    `warmup` eager steps per buffer set first and replays each graph once
+    after capture (the first launch uploads it); these update the weights
+    like any training step.
     """
 
     def __init__(self, net: GNN, inputs, num_masked: int, lr: float = 0.01, warmup: int = 1):
@@ -453,6 +454,10 @@ class GraphedTrainStep:
                 loss, _ = net.train_step(x, labels, mask, num_masked, lr)
             self.graphs.append(g)
             self.losses.append(loss)
+        # the first launch of an instantiated graph uploads it to the device;
+        # do that here (one replay each) instead of inside the caller's loop
+        for g in self.graphs:
+            g.replay()
         torch.cuda.synchronize()
 
     def step(self, k: int = 0) -> torch.Tensor:

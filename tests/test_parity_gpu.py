@@ -348,7 +348,7 @@ def test_graphed_train_step_matches_eager(model, rng):
     n = int(mask.sum().item())
     eager = ag.GNN.build(model, dims, dec, seed=3)
     graphed_net = ag.GNN.build(model, dims, dec, seed=3)
-    for _ in range(3):  # 1 warm-up + 2 replays below
+    for _ in range(4):  # 1 warm-up + the upload replay + 2 replays below
         loss_e, _ = eager.train_step(x, labels, mask, n, lr=0.05)
     step = ag.GraphedTrainStep(graphed_net, [(x, labels, mask)], n, lr=0.05, warmup=1)
     step.step(0)
