@@ -330,6 +330,41 @@ def test_prepare_matches_manual_pipeline(rng):
         ag.prepare(ag.RunConfig(reorder="metis"), g)
 
 
+@pytest.mark.parametrize("pair", [("dense_block", "coo_atomic"), ("csr_intra_blocked", "coo_atomic"),
+                                  ("dense_block", "csr_inter")])
+@pytest.mark.parametrize("model", ["gcn", "gin"])
+def test_training_step_fused_pairs_vs_composed_oracle(model, pair, rng):
+    """The training step on each fused selector pair the autotune may lock (the
+    C5 bench runs dense_block + coo_atomic at every width): loss and dW within
+    1e-5 of the composed numpy oracle, as for the bitwise CSR pair."""
+    from conftest import random_graph_arrays
+    V, d, s, _ = random_graph_arrays(rng, num_vertices=500, density=0.03)
+    g = ag.Graph.from_edges(V, d, s)
+    if model == "gcn":
+        g = ag.gcn_normalize(g)
+    rg = ag.apply_reorder(g, ag.cluster_bfs(g, 16))
+    dec = ag.decompose(rg, 16)
+    dims = [24, 32, 16, 5]
+    net = ag.GNN.build(model, dims, dec, seed=3, gin_eps=0.1)
+    net.default_pair = tuple(ag.KernelKind(k) for k in pair)
+    x = rng.standard_normal((V, dims[0])).astype(np.float32)
+    labels = rng.integers(0, dims[-1], V).astype(np.int32)
+    mask = rng.random(V) < 0.5
+    ws = [to_np(w).copy() for w in net.weights]
+    loss, grads = net.train_step(torch.from_numpy(x).cuda(), torch.from_numpy(labels).cuda(),
+                                 torch.from_numpy(mask).cuda(), int(mask.sum()), lr=0.0)
+    rd, rs, rw = to_np(rg.dst), to_np(rg.src), to_np(rg.weights) if rg.weights is not None else None
+    fwd_csr = R.to_csr(V, rd, rs, rw)
+    td, ts, tw = R.canonical(V, rs, rd, rw)
+    bwd_csr = R.to_csr(V, td, ts, tw)
+    adj_f = lambda h: R.csr_aggregate(V, *fwd_csr, h, "sum")[0]  # noqa: E731
+    adj_b = lambda h: R.csr_aggregate(V, *bwd_csr, h, "sum")[0]  # noqa: E731
+    oloss, ograds, _ = R.gnn_step(model, adj_f, adj_b, x, ws, labels, mask, gin_eps=0.1)
+    assert abs(float(loss.item()) - oloss) <= 1e-5 * max(1.0, abs(oloss))
+    for l, (gw, ow) in enumerate(zip(grads, ograds)):
+        assert rel_error(to_np(gw), ow) < 1e-5, l
+
+
 @pytest.mark.parametrize("model", ["gcn", "gin"])
 def test_graphed_train_step_matches_eager(model, rng):
     """GraphedTrainStep (the step as one CUDA graph per input buffer) computes
