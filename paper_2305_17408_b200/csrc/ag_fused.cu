@@ -18,26 +18,29 @@
 //    community's own 16-row block (intra) and, for the inter edges, a band of
 //    neighbouring blocks.  One CTA per SM owns a column tile of T = 32*VEC
 //    floats of one contiguous, nnz-balanced range of 16-row blocks and sweeps
-//    it front to back.
-//  * A producer warp streams the X tile of block b (16 rows x T floats) into
-//    an S-slot ring in shared memory with one TMA tensor load per block
-//    (cp.async.bulk.tensor.2d, mbarrier complete_tx), S blocks ahead of the
-//    slowest consumer.  X crosses HBM -> L2 -> SM once per tile.
-//  * 16 consumer warps: warp w owns row w of every block.  At block k the ring
-//    holds blocks [k-H, k+H] (H = window radius, picked per graph from the
-//    edge-distance histogram, ag_slab_window); a source inside it is read
-//    from shared memory (one 128/256-byte row per warp, conflict free),
-//    anything farther with a direct global load.  The per-row reduction is
-//    the exact numpy order above, one lane per VEC columns.
-//  * Ring slots are recycled through per-slot full/empty mbarriers: a warp
-//    finishing block k releases block k-H; the producer refills a slot once
-//    all 16 warps released it.  Warps drift freely up to S-2H-1 blocks apart,
-//    which absorbs the row-length imbalance without CTA-wide barriers.
-//  * Column indices and weights of the current row are staged in a per-warp
-//    32-entry window (one coalesced load per 32 edges) already translated to
-//    ring byte offsets, so the inner loop is LDS(window) + LDS(x) + math.
-//  * Products / sums are packed FMUL2 / FADD2 (fp32x2, round-to-nearest, no
-//    FMA contraction), so results stay bitwise equal to the reference.
+//    it front to back (about two such units per CTA).
+//  * X producer warp: streams the X tile of block b (16 rows x T floats) into
+//    a kSlots-slot ring in shared memory, one TMA tensor load per block
+//    (cp.async.bulk.tensor.2d, mbarrier complete_tx), and pulls the topology
+//    ahead into L2.  X crosses HBM -> L2 -> SM once per tile.
+//  * Far producer warp: bulk-copies each block's <= kFarMax distinct sources
+//    outside the ring window into a kFarSlots-deep far ring (and, for the
+//    ReLU-backward epilogue, the block's mask tile by TMA).
+//  * Consumer warps (14; 16 in the dense + coo mode) take the range's rows
+//    round-robin.  At block k the ring holds blocks [k-H, k+H] (H picked per
+//    graph, ag_slab_window); a staged source is one conflict-free 256-byte
+//    shared load per warp, anything else a direct global load.  A row's
+//    (code, weight) pairs are prefetched in registers one row ahead and
+//    installed into a per-warp window, so the inner loop is LDS(window) +
+//    LDS(x) + math.
+//  * Per-block mbarriers: ready[k] (producers' arrivals + the copies' bytes),
+//    done[k] (every consumer left block k); a slot is refilled only after done
+//    of the last block that reads it, so warps drift freely by a few blocks.
+//  * Modes (the selector pair being run): both roles bitwise (numpy order,
+//    FMUL2 / FFMA2-with-a-runtime-one so nothing contracts); dense_block intra
+//    on two extra "dense" warps (16 x 16 block weights x the block's X rows,
+//    register-blocked, into an I-slot the consumers add); coo_atomic inter
+//    (AG_EPI_INTER_COO) with fused multiply-adds in any order.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
