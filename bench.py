@@ -530,8 +530,11 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
-                    help="e2e arm: launch the training step eagerly instead of as a CUDA graph")
+                    help="launch the training step eagerly instead of as a CUDA graph")
+    ap.add_argument("--comm-size", type=int, default=COMM_SIZE,
+                    help="decomposition block size B (SURVEY 8d: also report 64/128/256 for C4)")
     args = ap.parse_args()
+    globals()["COMM_SIZE"] = args.comm_size
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

@@ -59,6 +59,11 @@ def main():
             torch.cuda.synchronize()
             continue
         ki, ke = (ag.KernelKind(k) for k in args.pair.split(","))
+        if args.only == "gemm_dw":
+            g256 = torch.randn((V, 256), device="cuda")
+            K.gemm(x, g256, trans_a=True)
+            torch.cuda.synchronize()
+            continue
         if args.only == "gemm_dh48":
             q48 = torch.randn((V, 48), device="cuda")
             w48 = torch.randn((256, 48), device="cuda")
