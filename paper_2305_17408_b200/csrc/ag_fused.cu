@@ -649,7 +649,9 @@ __host__ __device__ constexpr bool mode_sum3(int m) {
 template <int VEC, int MODE, bool W>
 __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64_t r, int32_t s,
                                        int32_t e, int32_t m, float *yrow, bool act, bool fast,
-                                       uint32_t relu_s, uint32_t intra_s) {
+                                       uint32_t relu_s, uint32_t intra_s,
+                                       uint32_t iv_bar = 0, uint32_t iv_phase = 0,
+                                       bool *iv_pending = nullptr) {
   constexpr bool IS_MAX = MODE == kModeMax;
   constexpr bool SUM3 = mode_sum3(MODE);
   constexpr bool DENSE = mode_dense(MODE);
@@ -675,6 +677,12 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
   float *yp = yrow;
   Vf<VEC> out;
   if constexpr (DENSE) {
+    // the block's intra partials: waited for here, after this row's inter
+    // reduction, so the dense warps' block product overlaps it
+    if (iv_pending && *iv_pending) {
+      mbar_wait(iv_bar, iv_phase);
+      *iv_pending = false;
+    }
     out = vadd<VEC>(lv_out<VEC>(lv_lds<VEC>(intra_s)), O);
   } else if constexpr (SUM3) {
     out = vadd<VEC>(I, O);
@@ -1134,9 +1142,13 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
         uint32_t kcur = kb0;
         // entering block k: its X window and far rows (ready), and in
         // dense-intra mode its intra partials
+        bool iv_pending = false;  // dense-intra: the current block's ivalid not yet waited for
         auto enter = [&](uint32_t k) {
           mbar_wait(bs.rdy(k), bs.rdy_phase(k));
-          if (DENSE) mbar_wait(ivalid + ((k - kb0) % kISlots) * 8, ((k - kb0) / kISlots) & 1u);
+          // dense + coo: waited for at the first epilogue in the block (measured
+          // faster); dense + csr: here (the deferred wait costs it registers)
+          if (MODE == kModeDense3Coo) iv_pending = true;
+          else if (DENSE) mbar_wait(ivalid + ((k - kb0) % kISlots) * 8, ((k - kb0) / kISlots) & 1u);
         };
         bool entered = false;
 #pragma unroll 1
@@ -1165,7 +1177,12 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
                                   (rr % kRB) * G::kRowBytes + lane * VEC * 4;
           const uint32_t intra_s = ring + G::kIOff + ((k - kb0) % kISlots) * G::kSlotBytes +
                                    (rr % kRB) * G::kRowBytes + lane * VEC * 4;
-          do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, relu_s, intra_s);
+          if constexpr (MODE == kModeDense3Coo)
+            do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, relu_s, intra_s,
+                                 ivalid + ((k - kb0) % kISlots) * 8, ((k - kb0) / kISlots) & 1u,
+                                 &iv_pending);
+          else
+            do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, relu_s, intra_s);
           info = info1;
           info1 = info2;
           q0 = n0;
