@@ -46,6 +46,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -108,6 +109,7 @@ struct GArgs {
   int64_t xblocks;          // ceil(x_rows / 16)
   int tma;                  // 1: TMA tensor loads; 0: cp.async element copies
   int sleep;                // producers' done waits: 1 suspend between polls, 0 spin
+  long long *trace;         // AG_SLAB_TRACE: per-block globaltimer stamps of CTA 0 (development)
   int dbg;                  // development knob (AG_SLAB_DEBUG bits, values then garbage): 1 skip the
                             // reductions, 2 far copies, 4 dense products, 8 X tiles, 16 Y stores,
                             // 32 consumer topology loads
@@ -782,6 +784,20 @@ __device__ __forceinline__ void mbar_expect_tx_only(uint32_t b, uint32_t bytes) 
                : "memory");
 }
 
+// Development trace (build with -DAG_SLAB_TRACE_BUILD, run with AG_SLAB_TRACE=1): per-block
+// globaltimer stamps of CTA 0's producers / consumer warps, printed by the host.  Compiled
+// out by default.
+constexpr int kTraceBlocks = 64;
+__device__ __forceinline__ void tstamp(const GArgs &a, uint32_t fi, int slot) {
+#ifdef AG_SLAB_TRACE_BUILD
+  if (a.trace != nullptr && blockIdx.x == 0 && fi < kTraceBlocks) {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    a.trace[fi * 8 + slot] = t;
+  }
+#endif
+}
+
 // Per-block synchronisation, relative to the range's first block kb0:
 //   ready[(k - kb0) % kReady]  completes when consumer block k can run: every
 //       X block of its window is in the X ring and its far rows are staged
@@ -838,7 +854,10 @@ __device__ __forceinline__ void produce_x(const GArgs &a, const CUtensorMap *map
       if (lane == 0) {
         if (need >= 0) bs.wait_done(static_cast<uint32_t>(need));
         const uint32_t xb = (a.dbg & 8) ? 0u : G::kSlotBytes;
-        if (last) mbar_expect_tx(bs.rdy(kt), xb);
+        if (last) {
+          tstamp(a, kt - kb0, 2);
+          mbar_expect_tx(bs.rdy(kt), xb);
+        }
         else if (xb) mbar_expect_tx_only(bs.rdy(kt), xb);
         if (xb) tma_load_2d(dst, map, bs.rdy(kt), static_cast<int>(c0), static_cast<int>(t * kRB));
       }
@@ -919,7 +938,9 @@ __device__ __forceinline__ void produce_far(const GArgs &a, const CUtensorMap *r
       const uint32_t relu_dst = ring + G::kReluOff + (fi % kReluSlots) * G::kSlotBytes;
       if (a.tma) {
         if (lane == 0) {
+          tstamp(a, fi, 0);
           if (need >= int64_t(kb0)) bs.wait_done(static_cast<uint32_t>(need));
+          tstamp(a, fi, 1);
           mbar_expect_tx(bs.rdy(f), (a.dbg & 2) ? 0u
                                                 : static_cast<uint32_t>(cnt) * tile_bytes +
                                                       (a.relu ? G::kSlotBytes : 0u));
@@ -1046,6 +1067,7 @@ __device__ __forceinline__ void dense_intra(const GArgs &a, uint32_t ring, const
     }
     __syncwarp();
     if (lane == 0) {
+      if (half == 0) tstamp(a, fi, 6);
       mbar_arrive(ivalid + (fi % kISlots) * 8);
       mbar_arrive(bs.done + (fi % kDone) * 8);
     }
@@ -1144,7 +1166,9 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
         // dense-intra mode its intra partials
         bool iv_pending = false;  // dense-intra: the current block's ivalid not yet waited for
         auto enter = [&](uint32_t k) {
+          if (warp == 0 && lane == 0) tstamp(a, k - kb0, 3);
           mbar_wait(bs.rdy(k), bs.rdy_phase(k));
+          if (warp == 0 && lane == 0) tstamp(a, k - kb0, 4);
           // dense + coo: waited for at the first epilogue in the block (measured
           // faster); dense + csr: here (the deferred wait costs it registers)
           if (MODE == kModeDense3Coo) iv_pending = true;
@@ -1157,7 +1181,11 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
           if (kcur != k || !entered) {  // leave the blocks before k (rows or not), enter k
             __syncwarp();
             for (; kcur != k; ++kcur)
-              if (lane == 0) mbar_arrive(done + ((kcur - kb0) % kDone) * 8);
+              if (lane == 0) {
+                if (warp == 0) tstamp(a, kcur - kb0, 5);
+                if (warp == NC - 1) tstamp(a, kcur - kb0, 7);
+                mbar_arrive(done + ((kcur - kb0) % kDone) * 8);
+              }
             enter(k);
             entered = true;
           }
@@ -1288,8 +1316,29 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
       (!a.relu || encode(&relu_map, a.ep.relu_src, a.rows)))
     a.tma = 1;
   const int threads = (mode == kModeDense3Coo ? kConsMax : 14) * 32 + 64;
+  long long *trace = nullptr;
+  if (std::getenv("AG_SLAB_TRACE")) {
+    AG_CUDA(cudaMalloc(&trace, kTraceBlocks * 8 * sizeof(long long)));
+    AG_CUDA(cudaMemset(trace, 0, kTraceBlocks * 8 * sizeof(long long)));
+    a.trace = trace;
+  }
   k<<<grid, threads, smem, st>>>(map, relu_map, a);
   AG_LAUNCH_CHECK("slab_kernel");
+  if (trace) {
+    long long h[kTraceBlocks * 8];
+    AG_CUDA(cudaStreamSynchronize(st));
+    AG_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
+    cudaFree(trace);
+    const long long t0 = h[0] ? h[0] : h[3];
+    std::fprintf(stderr, "slab trace mode=%d feat=%d H=%d (us; far: done-wait start..end | X last | "
+                         "cons0 ready-wait start..end | cons0 leave | dense ivalid | last-cons leave)\n",
+                 mode, a.feat, a.H);
+    for (int i = 0; i < kTraceBlocks; ++i) {
+      auto f = [&](int j) { return h[i * 8 + j] ? (h[i * 8 + j] - t0) / 1e3 : -1.0; };
+      std::fprintf(stderr, "blk %2d far %7.2f..%7.2f | X %7.2f | c0 %7.2f..%7.2f leave %7.2f | dense %7.2f | "
+                           "clast leave %7.2f\n", i, f(0), f(1), f(2), f(3), f(4), f(5), f(6), f(7));
+    }
+  }
   return AG_OK;
 }
 
