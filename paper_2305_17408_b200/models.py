@@ -298,8 +298,11 @@ class GNN:
                                   for ke in (KernelKind.CSR_INTER, KernelKind.COO_ATOMIC)]
                 best, best_t = pair, None
                 for cand in dict.fromkeys(cands):
+                    # 7 repetitions: the fused pairs are within a few percent of
+                    # each other, so a 3-sample median mis-picks between runs
                     t = _time_ms(lambda: aggregate_decomposed(
-                        subj, x, AggregateOp.SUM, kernel_intra=cand[0], kernel_inter=cand[1]))
+                        subj, x, AggregateOp.SUM, kernel_intra=cand[0], kernel_inter=cand[1]),
+                        reps=7)
                     if best_t is None or t < best_t:
                         best, best_t = cand, t
                 pair = best
