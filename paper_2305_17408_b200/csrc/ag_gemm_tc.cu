@@ -480,24 +480,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t s = t / tiles_mn;
       const int64_t m0 = tile_m0(t);
       const int64_t n0 = tile_n0(t);
-      if (g.mask != nullptr && g.splits == 1 && (g.ldm % 4) == 0 && ehalf == 0) {
-        // pull this row's mask segment of the NEXT tile into L2 (a whole tile
-        // period ahead of its use; the first tile's own segment too)
-        auto prefetch_mask = [&](int64_t tt) {
+      if (g.mask != nullptr && g.splits == 1 && warp == kEpiWarp0 && lane == 0) {
+        // pull the NEXT tile's mask rows into L2 a tile period ahead: one bulk
+        // prefetch of the whole contiguous row block (per-row prefetches from
+        // every lane stalled the epilogue warps)
+        auto prefetch_rows = [&](int64_t tt) {
           if (tt >= total) return;
-          const int64_t r = tile_m0(tt) + q * 32 + lane;
-          const int64_t nn = tile_n0(tt);
-          if (r >= g.M) return;
-          const float *mp = g.mask + r * g.ldm + nn;
-          const int64_t cols = std::min<int64_t>(BN, g.N - nn);
-          const uintptr_t lo = reinterpret_cast<uintptr_t>(mp) & ~uintptr_t(15);
-          const uintptr_t hi = (reinterpret_cast<uintptr_t>(mp + cols) + 15) & ~uintptr_t(15);
+          const int64_t r0 = tile_m0(tt);
+          const int64_t r1 = std::min<int64_t>(r0 + BM, g.M);
+          if (r1 <= r0) return;
+          const uintptr_t lo = reinterpret_cast<uintptr_t>(g.mask + r0 * g.ldm) & ~uintptr_t(15);
+          const uintptr_t hi =
+              (reinterpret_cast<uintptr_t>(g.mask + (r1 - 1) * g.ldm + g.N) + 15) & ~uintptr_t(15);
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo),
                        "r"(static_cast<uint32_t>(hi - lo))
                        : "memory");
         };
-        if (t == cid) prefetch_mask(t);
-        prefetch_mask(t + ncl);
+        if (t == cid) prefetch_rows(t);
+        prefetch_rows(t + ncl);
       }
       const int ti = static_cast<int>((t - cid) / ncl);
       const bool tr = g.trace != nullptr && blockIdx.x == 0 && warp == kEpiWarp0 && lane == 0 &&
