@@ -237,17 +237,19 @@ __global__ void __launch_bounds__(kXentThreads) xent_rows_kernel(
           for (int j = 0; j < 4; ++j) m4[j] = fmaxf(m4[j], z[c + j]);
         for (; c < ci; ++c) m4[0] = fmaxf(m4[0], z[c]);
         const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        const int32_t y = labels[r];
+        const float zy = z[y];
         float se = 0.0f;
 #pragma unroll 8
-        for (int cc = 0; cc < ci; ++cc) se += expf(z[cc] - mx);
-        const int32_t y = labels[r];
-        acc += static_cast<double>(mx + logf(se) - z[y]);
+        for (int cc = 0; cc < ci; ++cc) {  // exp once, kept in place for the gradient
+          const float ex = expf(z[cc] - mx);
+          z[cc] = ex;
+          se += ex;
+        }
+        acc += static_cast<double>(mx + logf(se) - zy);
         const float inv_se = 1.0f / se;
 #pragma unroll 8
-        for (int cc = 0; cc < ci; ++cc) {
-          const float pr = expf(z[cc] - mx) * inv_se;
-          z[cc] = (pr - (cc == y ? 1.0f : 0.0f)) * inv_n;
-        }
+        for (int cc = 0; cc < ci; ++cc) z[cc] = (z[cc] * inv_se - (cc == y ? 1.0f : 0.0f)) * inv_n;
       }
     }
     __syncthreads();
