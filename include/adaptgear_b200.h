@@ -316,13 +316,14 @@ int ag_tf32_split_lo(int64_t n, const float *src, float *lo, void *stream);
 
 /* Mean softmax cross-entropy over rows with mask[r] != 0 (mask may be NULL =
  * all rows).  logits / dlogits are [num_rows] x [num_classes] with row stride
- * ld >= num_classes.  Writes the loss (fp32 scalar, device; per-CTA fp64
- * partials summed in a fixed order) and dlogits = (softmax - onehot) /
- * n_masked (0 for unmasked rows; columns >= num_classes untouched). */
+ * ld >= num_classes; dlogits has its own row stride ld_dlogits >= num_classes.
+ * Writes the loss (fp32 scalar, device; per-CTA fp64 partials summed in a
+ * fixed order) and dlogits = (softmax - onehot) / n_masked (0 for unmasked
+ * rows; columns [num_classes, ld_dlogits) are written as 0). */
 int ag_softmax_xent(int64_t num_rows, int64_t num_classes, int64_t ld,
                     const float *logits, const int32_t *labels,
                     const uint8_t *mask, int64_t num_masked, float *loss_out,
-                    float *dlogits, void *stream);
+                    float *dlogits, int64_t ld_dlogits, void *stream);
 /* g = g * (h > 0) in place (ReLU backward). */
 int ag_relu_backward(int64_t n, const float *h, float *g, void *stream);
 /* w -= lr * dw. */

@@ -65,7 +65,7 @@ SIGNATURES: dict[str, list] = {
     "ag_gemm_tf32x3": [I64, I64, I64, P, I64, I32, P, I64, I32, P, P, I64, F32, F32, I32, P,
                        I64, P],
     "ag_tf32_split_lo": [I64, P, P, P],
-    "ag_softmax_xent": [I64, I64, I64, P, P, P, I64, P, P, P],
+    "ag_softmax_xent": [I64, I64, I64, P, P, P, I64, P, P, I64, P],
     "ag_relu_backward": [I64, P, P, P],
     "ag_sgd_step": [I64, P, P, F32, P],
     "ag_cluster_bfs": [I64, I64, P, P, I64, P, P],

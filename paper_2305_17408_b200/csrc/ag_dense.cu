@@ -160,7 +160,8 @@ constexpr int kXentThreads = 256;
 
 __global__ void __launch_bounds__(kXentThreads) xent_kernel(
     int64_t rows, int64_t C, int64_t ld, const float *logits, const int32_t *labels,
-    const uint8_t *mask, float inv_n, int64_t rows_per_cta, double *partial, float *dlogits) {
+    const uint8_t *mask, float inv_n, int64_t rows_per_cta, double *partial, float *dlogits,
+    int64_t ldd) {
   __shared__ double warp_sum[kXentThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t r0 = blockIdx.x * rows_per_cta;
@@ -168,7 +169,8 @@ __global__ void __launch_bounds__(kXentThreads) xent_kernel(
   double acc = 0.0;
   for (int64_t r = r0 + warp; r < r1; r += kXentThreads / 32) {
     const float *z = logits + r * ld;
-    float *dz = dlogits + r * ld;
+    float *dz = dlogits + r * ldd;
+    for (int64_t c = C + lane; c < ldd; c += 32) dz[c] = 0.0f;  // pad columns stay 0
     const bool on = mask ? mask[r] != 0 : true;
     if (!on) {
       for (int64_t c = lane; c < C; c += 32) dz[c] = 0.0f;
@@ -209,7 +211,7 @@ constexpr int kXentLd = 64;
 
 __global__ void __launch_bounds__(kXentThreads) xent_rows_kernel(
     int64_t rows, int64_t C, int64_t ld, const float *logits, const int32_t *labels,
-    const uint8_t *mask, float inv_n, double *partial, float *dlogits) {
+    const uint8_t *mask, float inv_n, double *partial, float *dlogits, int64_t ldd) {
   extern __shared__ float zs[];  // kXentThreads * (ld + 1)
   __shared__ double tsum[kXentThreads];
   const int t = threadIdx.x;
@@ -253,8 +255,13 @@ __global__ void __launch_bounds__(kXentThreads) xent_rows_kernel(
       }
     }
     __syncthreads();
-    float *dst = dlogits + r0 * ld;
-    for (int i = t; i < ni; i += kXentThreads) dst[i] = zs[(i / li) * lpi + i % li];
+    // rows of dlogits have their own stride ldd; columns >= C (the pad) are 0
+    const int ldi = static_cast<int>(ldd), nd = static_cast<int>(nr * ldd);
+    float *dst = dlogits + r0 * ldd;
+    for (int i = t; i < nd; i += kXentThreads) {
+      const int c = i % ldi;
+      dst[i] = c < C ? zs[(i / ldi) * lpi + c] : 0.0f;
+    }
     __syncthreads();
   }
   tsum[t] = acc;
@@ -333,8 +340,9 @@ extern "C" int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int6
 
 extern "C" int ag_softmax_xent(int64_t rows, int64_t C, int64_t ld, const float *logits,
                                const int32_t *labels, const uint8_t *mask, int64_t num_masked,
-                               float *loss_out, float *dlogits, void *stream) {
-  if (rows < 0 || C < 1 || ld < C) return fail(AG_ERR_VALUE, "bad loss sizes");
+                               float *loss_out, float *dlogits, int64_t ld_dlogits,
+                               void *stream) {
+  if (rows < 0 || C < 1 || ld < C || ld_dlogits < C) return fail(AG_ERR_VALUE, "bad loss sizes");
   cudaStream_t st = as_stream(stream);
   const float inv_n = num_masked > 0 ? 1.0f / static_cast<float>(num_masked) : 0.0f;
   const bool narrow = ld <= kXentLd;
@@ -349,7 +357,7 @@ extern "C" int ag_softmax_xent(int64_t rows, int64_t C, int64_t ld, const float 
     AG_CUDA(cudaFuncSetAttribute(xent_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kXentThreads * (kXentLd + 1) * sizeof(float))));
     xent_rows_kernel<<<static_cast<unsigned>(ctas), kXentThreads, smem, st>>>(
-        rows, C, ld, logits, labels, mask, inv_n, part.as<double>(), dlogits);
+        rows, C, ld, logits, labels, mask, inv_n, part.as<double>(), dlogits, ld_dlogits);
     AG_LAUNCH_CHECK("xent_rows_kernel");
   } else {
     ctas = std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64,
@@ -358,7 +366,7 @@ extern "C" int ag_softmax_xent(int64_t rows, int64_t C, int64_t ld, const float 
     AG_CUDA(part.alloc(ctas * sizeof(double), st));
     xent_kernel<<<static_cast<unsigned>(ctas), kXentThreads, 0, st>>>(
         rows, C, ld, logits, labels, mask, inv_n, std::max<int64_t>(per, 1), part.as<double>(),
-        dlogits);
+        dlogits, ld_dlogits);
     AG_LAUNCH_CHECK("xent_kernel");
   }
   loss_final_kernel<<<1, 32, 0, st>>>(static_cast<int>(ctas), part.as<double>(),

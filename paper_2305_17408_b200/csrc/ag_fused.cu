@@ -1090,6 +1090,10 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
   constexpr bool DENSE = mode_dense(MODE);
   constexpr int kCons = cons_warps<MODE>();
   constexpr int NC = DENSE ? kCons - kDenseWarps : kCons;  // consumer warps (dense warps last)
+  // kModeDense3Coo defers a block's ivalid wait to the warp's first epilogue in
+  // it: every consumer warp must own a row of every block, or a warp skipping
+  // kISlots blocks could pass a stale-parity wait
+  static_assert((NC - 1) * kRG < kRB, "every consumer warp needs a row in every block");
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t H = static_cast<uint32_t>(a.H);

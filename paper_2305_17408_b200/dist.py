@@ -329,7 +329,7 @@ class DistGNN:
         g = models._padded_empty(n, logits.shape[1], logits.device)
         _lib.call("ag_softmax_xent", n, logits.shape[1], logits.stride(0), _lib.ptr(logits),
                   _lib.ptr(labels), _lib.ptr(mask), int(num_masked), _lib.ptr(loss),
-                  _lib.ptr(g), _lib.stream())
+                  _lib.ptr(g), g.stride(0), _lib.stream())
         for l in range(L - 1, -1, -1):
             agg, _ = saved[l]
             gemm(agg, g, self.grads[l], trans_a=True)

@@ -385,8 +385,15 @@ class GNN:
                 d_in = gemm(g, self.weights[l], trans_b=True)          # d(A H) = g W^T
                 g = self._aggregate(self.subject_t, d_in, "bwd", relu_src=h_prev)
             else:
-                # q = A_hat^T g (+ (1+eps) g), at the layer's (narrow) output width
-                q = self._aggregate(self.subject_t, _base(g), "bwd")[:, :self.dims[l + 1]]
+                # q = A_hat^T g (+ (1+eps) g), at the layer's (narrow) output width,
+                # aggregated over the zero-padded width autotune tuned for
+                gb = _base(g)
+                if gb.shape[1] != _pad4(self.dims[l + 1]):  # g from an agg-first layer above
+                    gp = torch.zeros((g.shape[0], _pad4(self.dims[l + 1])), dtype=torch.float32,
+                                     device=g.device)
+                    gp[:, :g.shape[1]] = g
+                    gb = gp
+                q = self._aggregate(self.subject_t, gb, "bwd")[:, :self.dims[l + 1]]
                 gemm(operand, q, grads[l], trans_a=True)                 # dW = H^T q
                 if l == 0:
                     break
@@ -401,7 +408,7 @@ class GNN:
                                device=logits.device)[:, :logits.shape[1]]
         _lib.call("ag_softmax_xent", logits.shape[0], logits.shape[1], logits.stride(0),
                   _lib.ptr(logits), _lib.ptr(labels), _lib.ptr(mask), int(num_masked),
-                  _lib.ptr(loss), _lib.ptr(d_logits), _lib.stream())
+                  _lib.ptr(loss), _lib.ptr(d_logits), d_logits.stride(0), _lib.stream())
         return loss, d_logits
 
     def sgd(self, grads, lr: float) -> None:
