@@ -210,6 +210,7 @@ def run_ours(args, cfg):
     n_mask = int(mask_np.sum())  # global count (the loss is a mean over all ranks' rows)
     lr = 0.01
     t_tune = time.perf_counter()
+    cache_info = None
     if world > 1:
         # row partition: each rank owns a B-aligned, nnz-balanced row range
         from paper_2305_17408_b200 import dist as D
@@ -236,7 +237,10 @@ def run_ours(args, cfg):
     else:
         labels = torch.from_numpy(labels_np).cuda()
         mask = torch.from_numpy(mask_np).cuda()
-        choices = net.autotune()
+        cache = ag.ChoiceCache(args.choice_cache) if args.choice_cache else None
+        choices = net.autotune(cache=cache)
+        cache_info = None if cache is None else {"path": str(args.choice_cache),
+                                                  "hits": cache.hits, "misses": cache.misses}
 
         def step():
             return net.train_step(x, labels, mask, n_mask, lr)
@@ -408,6 +412,7 @@ def run_ours(args, cfg):
             "l2": "inputs and activations (>= 0.98 GB per aggregation) exceed the 126 MB L2",
             "preprocess_s": round(prep_s, 2),
             "autotune_s": round(tune_s, 2),
+            "choice_cache": cache_info,
             "launch": "each timed step replays the training step as one CUDA graph "
                       "(GraphedTrainStep); per-aggregation timings from an eager pass"
                       if use_graph else "eager launches, per-aggregation CUDA events in-step",
@@ -446,75 +451,100 @@ def run_ours(args, cfg):
         "clocks": clocks.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(rg, dims, rows=args.cpu_rows)
+        line["cpu_baseline"] = cpu_baseline(rg, cfg)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def host_csr(graph):
-    from paper_2305_17408_b200 import to_csr
-    a = to_csr(graph)
-    rp = a.row_ptr.cpu().numpy()
-    col = a.col_idx.cpu().numpy()
-    val = None if a.kernel_val is None else a.kernel_val.cpu().numpy()
-    return rp, col, val
+def _host_graph(rg):
+    """Canonical reordered graph as host arrays (the GPU arm's own graph)."""
+    w = None if rg.weights is None else rg.weights.cpu().numpy()
+    return rg.dst.cpu().numpy(), rg.src.cpu().numpy(), w
 
 
-def cpu_baseline(rg, dims, rows):
+def _numpy_graph(cfg):
+    """The same workload built with the numpy oracle only (oracle/synth.py twin
+    of the device generator, gcn_normalize, load_partition, apply_reorder):
+    the reference arm never loads this repo's CUDA library."""
+    from oracle import ref_numpy as R
+    from oracle import synth as osynth
+    gen = dict(GEN)
+    gen["block_gen"] = cfg.get("block_gen", GEN["block_gen"])
+    (d, s), comm = osynth.community_graph(cfg["V"], cfg["E"], **gen)
+    V = cfg["V"]
+    if cfg["model"] == "gcn":
+        d, s, w = R.gcn_normalize(V, d, s)
+    else:
+        w = None
+    _, perm = R.partition_from_ids(comm, COMM_SIZE)
+    return R.apply_reorder(V, d, s, w, perm)
+
+
+def _cpu_plan(cfg):
+    """(fraction of rows, timed reps): every row for C1-C3; a uniform sample of
+    16-row blocks sized to ~15 s of host work for the large configs."""
+    V = cfg["V"]
+    if V <= 200_000:
+        return 1.0, (3 if V <= 20_000 else 1)
+    return 0.015, 1
+
+
+def cpu_baseline(rg, cfg):
     from oracle import baseline
-    V = rg.num_vertices
-    fwd = host_csr(rg)
-    bwd = host_csr(rg.reverse())
-    ms, sample = baseline.epoch_sample(V, fwd, bwd, dims, rows)
-    return {"value": round(ms, 1), "unit": "ms/epoch", "cores": os.cpu_count(), "kind": "port",
-            "sample": sample}
+    d, s, w = _host_graph(rg)
+    frac, reps = _cpu_plan(cfg)
+    r = baseline.time_epochs(cfg["V"], d, s, w, COMM_SIZE, cfg["dims"], cfg["model"], frac,
+                             reps=reps, warmup=1)
+    return _baseline_obj(r, frac, reps)
+
+
+def _baseline_obj(r, frac, reps):
+    if frac >= 1.0:
+        sample = (f"full epoch, every row (median of {r['reps']}), the reference's kernels: "
+                  f"intra {r['intra_choice']} (selector argmin on this host) + csr_inter, "
+                  f"combine, BLAS agg@W, backward_sum; GPU association")
+    else:
+        sample = (f"uniform random {r['frac_rows']:.2%} of the 16-row blocks ({r['sample_rows']} rows, "
+                  f"{r['sample_edges']} edges, every aggregation / GEMM / loss op of the epoch on "
+                  f"them, median of {r['reps']}), wall {r['sample_wall_s']:.1f} s scaled by "
+                  f"V/rows; reference kernels: intra {r['intra_choice']} + csr_inter, combine, "
+                  f"BLAS agg@W, backward_sum; full-size validation: profiles/cpu_fullscale_c5.json")
+    return {"value": round(r["epoch_ms"], 1), "unit": "ms/epoch", "cores": r["threads"],
+            "kind": "port", "sample": sample, "parts_ms": r["parts_ms"],
+            "note": "numpy's reduceat holds the GIL: the reference's thread pool runs at ~1 core"}
 
 
 def run_reference(args, cfg):
-    """--impl reference: the reference's CPU algorithm (oracle port; the reference
-    is pure Python/numpy and cannot travel) on the host cores, bounded sample."""
+    """--impl reference: the reference's CPU kernels (oracle port of the pure
+    numpy reference, oracle/baseline.py) on the host cores, on the same
+    workload built by the numpy oracle (no CUDA library); each step is one
+    sampled epoch (all rows for C1-C3)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch
-    torch.cuda.set_device(0) if torch.cuda.is_available() else None
-    from oracle import baseline, ref_numpy as R
-    from oracle import synth as osynth
-    if torch.cuda.is_available():
-        _, rg, _, _, _ = build_workload(cfg)
-        V = rg.num_vertices
-        fwd, bwd = host_csr(rg), host_csr(rg.reverse())
-    else:  # reference arm without a GPU: build the same graph with the numpy oracle
-        gen = dict(GEN)
-        gen["block_gen"] = cfg.get("block_gen", GEN["block_gen"])
-        (d, s), comm = osynth.community_graph(cfg["V"], cfg["E"], **gen)
-        V = cfg["V"]
-        if cfg["model"] == "gcn":
-            d, s, w = R.gcn_normalize(V, d, s)
-        else:
-            w = None
-        _, perm = R.partition_from_ids(comm, COMM_SIZE)
-        d, s, w = R.apply_reorder(V, d, s, w, perm)
-        fwd = R.to_csr(V, d, s, w)
-        td, ts, tw = R.canonical(V, s, d, w)
-        bwd = R.to_csr(V, td, ts, tw)
-    vals = []
-    sample = ""
-    for _ in range(args.warmup + args.steps):
-        ms, sample = baseline.epoch_sample(V, fwd, bwd, cfg["dims"], args.cpu_rows)
-        vals.append(ms)
-    vals = vals[args.warmup:] or vals
-    ms = statistics.median(vals)
+    from oracle import baseline
+    t0 = time.perf_counter()
+    d, s, w = _numpy_graph(cfg)
+    build_s = time.perf_counter() - t0
+    frac, _ = _cpu_plan(cfg)
+    if frac < 1.0:
+        frac = 0.005  # ~5 s per step, so K + W steps fit in a few minutes
+    r = baseline.time_epochs(cfg["V"], d, s, w, COMM_SIZE, cfg["dims"], cfg["model"], frac,
+                             reps=max(1, args.steps), warmup=max(1, args.warmup), budget_s=240.0)
+    ms = r["epoch_ms"]
+    cb = _baseline_obj(r, frac, r["reps"])
     line = {"impl": "reference", "metric": METRIC, "value": round(ms, 1), "unit": "ms/epoch",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": r["reps"], "warmup": max(1, args.warmup),
             "ms_per_step": round(ms, 1), "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config} {cfg['name']}", "dims": cfg["dims"]},
-            "cpu_baseline": {"value": round(ms, 1), "unit": "ms/epoch", "cores": os.cpu_count(),
-                             "kind": "port", "sample": sample},
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (the same seeded generator, built with numpy)",
+            "config": {"workload": f"{args.config} {cfg['name']}", "dims": cfg["dims"],
+                       "graph_build_s": round(build_s, 1),
+                       "steps_requested": args.steps},
+            "cpu_baseline": cb,
             "e2e": {"value": round(ms, 1), "unit": "ms/epoch", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -527,8 +557,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-rows", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--choice-cache", default=str(ROOT / ".choice_cache.json"),
+                    help="ChoiceCache file (selector + autotuned pairs per graph/width/direction); "
+                         "'' disables it")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the training step eagerly instead of as a CUDA graph")
     ap.add_argument("--comm-size", type=int, default=COMM_SIZE,

@@ -55,14 +55,23 @@ extern "C" {
 #define AG_EPI_COMBINE 1
 #define AG_EPI_GIN 2
 #define AG_EPI_EMPTY_OTHER 4
+/* Bit-packed ReLU masks ("relu bits"): for a [rows][feat] activation h, row r
+ * is ldw >= ceil(feat / 32) uint32 words and bit (c % 32) of word c / 32 is
+ * (h[r][c] > 0).  The forward epilogues that apply a ReLU can write them
+ * (ag_gemm_* mask_out, ag_fused_spmm relu_out with AG_EPI_RELU), the backward
+ * epilogues read them -- 1/32 of the bytes of re-reading h to test its sign.
+ * ag_relu_bits builds them from an fp32 activation. */
+int ag_relu_bits(int64_t num_rows, int64_t feat, const float *h, int64_t ld,
+                 uint32_t *bits, int64_t ldw, void *stream);
 /* AG_EPI_RELU_MASK (ag_fused_spmm only): after everything else,
- * y = relu_src > 0 ? y : 0 -- the ReLU backward of the layer below, fused
- * into the transposed aggregation (relu_src = that layer's output, same
- * shape and row stride as y). */
+ * y = bit ? y : 0 from relu_bits (row stride ceil(feat / 32) words) -- the
+ * ReLU backward of the layer below (its output's mask), fused into the
+ * transposed aggregation. */
 #define AG_EPI_RELU_MASK 8
 /* AG_EPI_RELU (ag_fused_spmm only): y = max(y, 0) after everything else --
  * the hidden layers' activation when the update GEMM runs before the
- * aggregation (A (H W) for a narrowing layer). */
+ * aggregation (A (H W) for a narrowing layer); with relu_out non-NULL the
+ * kernel also writes y's relu bits (row stride ceil(feat / 32) words). */
 #define AG_EPI_RELU 16
 /* AG_EPI_INTER_COO (ag_fused_spmm, role_mask 3, op sum only): the inter role
  * is the selector's coo_atomic kernel (kernels.py:192-225), whose summation
@@ -235,8 +244,8 @@ int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                   int32_t weighted, const float *blk_w, int64_t num_edges,
                   const float *x, float *y,
                   int32_t op, int32_t epi_flags, const uint8_t *other_touched,
-                  const int64_t *deg, float gin_scale, const float *relu_src,
-                  int64_t x_rows, int32_t window, void *stream);
+                  const int64_t *deg, float gin_scale, const uint32_t *relu_bits,
+                  uint32_t *relu_out, int64_t x_rows, int32_t window, void *stream);
 
 /* Window radius (in 16-row blocks) for ag_fused_spmm over this CSR: the
  * smallest radius whose ring covers `coverage` (e.g. 0.995) of the edges the
@@ -284,14 +293,15 @@ int ag_combine(int64_t num_rows, int64_t feat, const float *a,
 /* C = alpha * op(A) @ op(B) + beta * C, fp32 row-major, optional ReLU on
  * the result (epilogue 1).  op(A) is [M,K], op(B) is [K,N]. */
 #define AG_GEMM_RELU 1
-/* mask (may be NULL): after the epilogue, C[m][n] = mask[m * ldm + n] > 0 ?
- * C[m][n] : 0 -- the ReLU backward of the layer below, fused into dH = G W^T
- * (mask = that layer's output, never aliasing C). */
+/* mask (relu bits, may be NULL; ldm in words): after the epilogue,
+ * C[m][n] = bit(m, n) ? C[m][n] : 0 -- the ReLU backward of the layer below
+ * (its output's mask), fused into dH = G W^T.  mask_out (may be NULL; ldmo in
+ * words): the relu bits of the final C (the forward ReLU's mask). */
 int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                 int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
                 float *C, int64_t ldc, float alpha, float beta,
-                int32_t epilogue, const float *mask, int64_t ldm,
-                void *stream);
+                int32_t epilogue, const uint32_t *mask, int64_t ldm,
+                uint32_t *mask_out, int64_t ldmo, void *stream);
 
 /* The same GEMM on the tensor cores: tcgen05.mma kind::tf32 with TMA-fed,
  * 128-byte-swizzled shared-memory operands, TMEM accumulators and 3xTF32
@@ -303,8 +313,8 @@ int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
 int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                    int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
                    const float *B_lo, float *C, int64_t ldc, float alpha, float beta,
-                   int32_t epilogue, const float *mask, int64_t ldm,
-                   void *stream);
+                   int32_t epilogue, const uint32_t *mask, int64_t ldm,
+                   uint32_t *mask_out, int64_t ldmo, void *stream);
 
 /* lo[i] = src[i] - tf32_truncate(src[i]) (exact): the low half of the 3xTF32
  * split, precomputed for a small B operand that every output tile re-reads

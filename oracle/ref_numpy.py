@@ -23,8 +23,10 @@ def canonical(V, dst, src, w=None):
     uniq, inv = np.unique(key, return_inverse=True)
     wo = None
     if w is not None:
-        acc = np.zeros(uniq.size, dtype=np.float64)
-        np.add.at(acc, inv, np.asarray(w, dtype=F32).astype(np.float64))
+        # fp64 sum of duplicates in input order: np.bincount accumulates
+        # sequentially like np.add.at (the reference's merge), bit for bit
+        acc = np.bincount(inv.ravel(), weights=np.asarray(w, dtype=F32).astype(np.float64),
+                          minlength=uniq.size)
         wo = acc.astype(F32)
     base = max(V, 1)
     return (uniq // base).astype(np.int32), (uniq % base).astype(np.int32), wo

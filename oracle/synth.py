@@ -72,10 +72,33 @@ def vertex_permutation(V, seed):
     return perm
 
 
+def _candidates_threaded(V, Bg, p_intra, p_global, window, skew, seed, n, threads=None):
+    """candidates(..., 0, n) computed in index chunks on a thread pool (numpy
+    releases the GIL in its ufuncs); candidate i depends on i alone, so the
+    result is identical to one call."""
+    import concurrent.futures as cf
+    import os
+    threads = threads or os.cpu_count() or 1
+    if n < (1 << 20) or threads == 1:
+        return candidates(V, Bg, p_intra, p_global, window, skew, seed, 0, n)
+    step = (n + threads - 1) // threads
+    parts = [(a, min(n, a + step)) for a in range(0, n, step)]
+    d = np.empty(n, np.int64)
+    s = np.empty(n, np.int64)
+
+    def work(ab):
+        a, b = ab
+        d[a:b], s[a:b] = candidates(V, Bg, p_intra, p_global, window, skew, seed, a, b - a)
+
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(work, parts))
+    return d, s
+
+
 def community_graph(V, E, block_gen=16, p_intra=0.5, p_global=0.1, window=4, skew=1, seed=0):
     n = E + E // 16 + 1024
     while True:
-        d, s = candidates(V, block_gen, p_intra, p_global, window, skew, seed, 0, n)
+        d, s = _candidates_threaded(V, block_gen, p_intra, p_global, window, skew, seed, n)
         ok = s >= 0
         keys = d[ok] * V + s[ok]
         idx = np.arange(n, dtype=np.int64)[ok]

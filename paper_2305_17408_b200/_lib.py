@@ -55,15 +55,17 @@ SIGNATURES: dict[str, list] = {
     "ag_dense_block_spmm": [I64, I64, I64, P, P, P, P, P, I32, I32, P, P, F32, P],
     "ag_role_csr_build": [I64, P, P, P, I64, P, P, P, P],
     "ag_fused_spmm": [I64, I64, I32, P, P, P, P, P, P, I32, P, I64, P, P, I32, I32, P, P, F32,
-                      P, I64, I32, P],
+                      P, P, I64, I32, P],
+    "ag_relu_bits": [I64, I64, P, I64, P, I64, P],
     "ag_slab_window": [I64, P, P, F64, P, P],
     "ag_slab_codes": [I64, P, P, P, P, I32, P, P, P, P, P],
     "ag_slab_far_capacity": [],
     "ag_slab_dense_blocks": [I64, P, P, P, P, P, P],
     "ag_combine": [I64, I64, P, P, P, P, P, I32, P, P],
-    "ag_gemm_f32": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, F32, F32, I32, P, I64, P],
+    "ag_gemm_f32": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, F32, F32, I32, P, I64, P,
+                    I64, P],
     "ag_gemm_tf32x3": [I64, I64, I64, P, I64, I32, P, I64, I32, P, P, I64, F32, F32, I32, P,
-                       I64, P],
+                       I64, P, I64, P],
     "ag_tf32_split_lo": [I64, P, P, P],
     "ag_softmax_xent": [I64, I64, I64, P, P, P, I64, P, P, I64, P],
     "ag_relu_backward": [I64, P, P, P],

@@ -78,4 +78,13 @@ inline int grid_for(int64_t n, int block, int64_t cap = 148LL * 64) {
 int sm_count();
 void count_launch();
 
+// Bit-packed ReLU masks (AG_RELU_BITS layout, include/adaptgear_b200.h): row r
+// of a [rows][feat] activation is ldw = ceil(feat / 32) uint32 words; bit
+// (c % 32) of word c / 32 is (h[r][c] > 0).  1/32 of the fp32 bytes.
+__host__ __device__ inline int64_t relu_words(int64_t feat) { return (feat + 31) / 32; }
+__device__ __forceinline__ bool relu_bit(const uint32_t *bits, int64_t ldw, int64_t r,
+                                         int64_t c) {
+  return (__ldg(bits + r * ldw + (c >> 5)) >> (c & 31)) & 1u;
+}
+
 }  // namespace ag

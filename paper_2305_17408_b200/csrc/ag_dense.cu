@@ -31,8 +31,8 @@ struct GemmArgs {
   float alpha, beta;
   int epi;
   int64_t k_per_split;
-  const float *mask;  // ReLU-backward mask operand (NULL: none): out = mask > 0 ? out : 0
-  int64_t ldm;
+  const uint32_t *mask;  // ReLU-backward bit mask (NULL: none): out = bit ? out : 0
+  int64_t ldm;           // words per mask row
 };
 
 // A(m, k) of op(A) and B(k, n) of op(B)
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(NT, 2) sgemm_kernel(GemmArgs g, int partial) {
         float v = g.alpha * acc[i][j];
         if (g.beta != 0.0f) v = fmaf(g.beta, g.C[m * g.ldc + n], v);
         if (g.epi & AG_GEMM_RELU) v = fmaxf(v, 0.0f);
-        if (g.mask && !(g.mask[m * g.ldm + n] > 0.0f)) v = 0.0f;
+        if (g.mask && !relu_bit(g.mask, g.ldm, m, n)) v = 0.0f;
         g.C[m * g.ldc + n] = v;
       }
     }
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(NT, 2) sgemm_kernel(GemmArgs g, int partial) {
 
 __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const float *part, float *C,
                                      int64_t ldc, float alpha, float beta, int epi,
-                                     const float *mask, int64_t ldm) {
+                                     const uint32_t *mask, int64_t ldm) {
   const int64_t n = M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -146,7 +146,7 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const flo
     float v = alpha * s;
     if (beta != 0.0f) v = fmaf(beta, C[m * ldc + c], v);
     if (epi & AG_GEMM_RELU) v = fmaxf(v, 0.0f);
-    if (mask && !(mask[m * ldm + c] > 0.0f)) v = 0.0f;
+    if (mask && !relu_bit(mask, ldm, m, c)) v = 0.0f;
     C[m * ldc + c] = v;
   }
 }
@@ -281,6 +281,23 @@ __global__ void loss_final_kernel(int n, const double *partial, double inv_n, fl
   }
 }
 
+// bits[r][w] of a [rows][feat] (row stride ld) activation: a warp per
+// (row, 32-column word), one ballot per word.
+__global__ void relu_bits_kernel(int64_t rows, int64_t feat, const float *h, int64_t ld,
+                                 uint32_t *bits, int64_t ldw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = relu_words(feat);
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+       t < rows * nw; t += warps) {
+    const int64_t r = t / nw, w = t % nw;
+    const int64_t c = w * 32 + lane;
+    const bool on = c < feat && h[r * ld + c] > 0.0f;
+    const uint32_t b = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) bits[r * ldw + w] = b;
+  }
+}
+
 __global__ void relu_bwd_kernel(int64_t n, const float *h, float *g) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -301,9 +318,12 @@ using namespace ag;
 extern "C" int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                            int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
                            float *C, int64_t ldc, float alpha, float beta, int32_t epilogue,
-                           const float *mask, int64_t ldm, void *stream) {
+                           const uint32_t *mask, int64_t ldm, uint32_t *mask_out,
+                           int64_t ldmo, void *stream) {
   if (M < 0 || N < 0 || K < 0) return fail(AG_ERR_VALUE, "negative GEMM sizes");
   if (M == 0 || N == 0) return AG_OK;
+  if ((mask && ldm < relu_words(N)) || (mask_out && ldmo < relu_words(N)))
+    return fail(AG_ERR_VALUE, "relu-bit row strides must be >= ceil(N / 32) words");
   cudaStream_t st = as_stream(stream);
   const int64_t tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
   if (tiles_m > 65535) return fail(AG_ERR_VALUE, "GEMM M too large (%lld)", (long long)M);
@@ -324,7 +344,7 @@ extern "C" int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int6
   if (splits == 1) {
     sgemm_kernel<<<grid, NT, 0, st>>>(g, 0);
     AG_LAUNCH_CHECK("sgemm_kernel");
-    return AG_OK;
+    return mask_out ? ag_relu_bits(M, N, C, ldc, mask_out, ldmo, stream) : AG_OK;
   }
   Scratch part;
   AG_CUDA(part.alloc(static_cast<size_t>(splits) * M * N * sizeof(float), st));
@@ -335,7 +355,7 @@ extern "C" int ag_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int6
                                                             ldc, alpha, beta, epilogue, mask,
                                                             ldm);
   AG_LAUNCH_CHECK("splitk_reduce_kernel");
-  return AG_OK;
+  return mask_out ? ag_relu_bits(M, N, C, ldc, mask_out, ldmo, stream) : AG_OK;
 }
 
 extern "C" int ag_softmax_xent(int64_t rows, int64_t C, int64_t ld, const float *logits,
@@ -372,6 +392,18 @@ extern "C" int ag_softmax_xent(int64_t rows, int64_t C, int64_t ld, const float 
   loss_final_kernel<<<1, 32, 0, st>>>(static_cast<int>(ctas), part.as<double>(),
                                       num_masked > 0 ? 1.0 / num_masked : 0.0, loss_out);
   AG_LAUNCH_CHECK("loss_final_kernel");
+  return AG_OK;
+}
+
+extern "C" int ag_relu_bits(int64_t rows, int64_t feat, const float *h, int64_t ld,
+                            uint32_t *bits, int64_t ldw, void *stream) {
+  if (rows < 0 || feat < 0 || ld < feat || ldw < relu_words(feat))
+    return fail(AG_ERR_VALUE, "bad relu_bits sizes");
+  if (rows == 0 || feat == 0) return AG_OK;
+  const int64_t warps = rows * relu_words(feat);
+  relu_bits_kernel<<<grid_for(warps * 32, 256), 256, 0, as_stream(stream)>>>(rows, feat, h, ld,
+                                                                          bits, ldw);
+  AG_LAUNCH_CHECK("relu_bits_kernel");
   return AG_OK;
 }
 

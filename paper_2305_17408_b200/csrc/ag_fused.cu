@@ -24,8 +24,7 @@
 //    (cp.async.bulk.tensor.2d, mbarrier complete_tx), and pulls the topology
 //    ahead into L2.  X crosses HBM -> L2 -> SM once per tile.
 //  * Far producer warp: bulk-copies each block's <= kFarMax distinct sources
-//    outside the ring window into a kFarSlots-deep far ring (and, for the
-//    ReLU-backward epilogue, the block's mask tile by TMA).
+//    outside the ring window into a kFarSlots-deep far ring.
 //  * Consumer warps (14; 16 in the dense + coo mode) take the range's rows
 //    round-robin.  At block k the ring holds blocks [k-H, k+H] (H picked per
 //    graph, ag_slab_window); a staged source is one conflict-free 256-byte
@@ -70,10 +69,9 @@ constexpr int kConsMax = 16;
 template <int MODE>
 constexpr int cons_warps();
 constexpr int kWin = 64;     // topology items per window refill (two per lane)
-constexpr int kSlots = 41;   // X ring capacity in blocks (window H <= (kSlots - 9) / 2 = 16)
+constexpr int kSlots = 45;   // X ring capacity in blocks (window H <= (kSlots - 9) / 2 = 18)
 constexpr int kFarSlots = 4; // far ring: staged out-of-window sources of the next blocks
 constexpr int kFarMax = 20;  // staged far sources per block (more: read from global)
-constexpr int kReluSlots = 4;  // ReLU-mask operand tiles staged ahead (backward epilogue)
 constexpr int kRG = 1;       // consecutive rows a consumer warp takes at a time (divides kRB)
 constexpr int kISlots = 4;   // dense-intra mode: per-block intra results (16 rows x tile)
 constexpr int kReady = 16;   // per-block "ready" barriers (X window + far rows staged)
@@ -94,7 +92,9 @@ struct GArgs {
   const int32_t *far_src;   // [nblocks * kFarMax] their source rows
   int weighted;             // 0: every weight is 1.0 (multiplies skipped: exact)
   int has_mid;              // rowinfo.y is the intra-run end (role-ordered layout)
-  int relu;                 // AG_EPI_RELU_MASK: relu_src tiles are staged by the far producer
+  int relu;                 // AG_EPI_RELU_MASK: y *= the relu_bits mask (ep.relu_bits)
+  uint32_t *relu_out;       // AG_EPI_RELU: write y's relu bits here (or NULL)
+  int64_t ldw;              // words per relu-bit row: ceil(feat / 32)
   const float *blk_w;       // dense-intra mode: [nblocks][16][16] intra weights (dst, src)
   const float *x;
   float *y;
@@ -109,6 +109,7 @@ struct GArgs {
   int64_t xblocks;          // ceil(x_rows / 16)
   int tma;                  // 1: TMA tensor loads; 0: cp.async element copies
   int sleep;                // producers' done waits: 1 suspend between polls, 0 spin
+  uint32_t csleep;          // consumer / dense-warp waits: suspend hint (ns) per poll, 0 spin
   long long *trace;         // AG_SLAB_TRACE: per-block globaltimer stamps of CTA 0 (development)
   int dbg;                  // development knob (AG_SLAB_DEBUG bits, values then garbage): 1 skip the
                             // reductions, 2 far copies, 4 dense products, 8 X tiles, 16 Y stores,
@@ -648,10 +649,19 @@ __host__ __device__ constexpr bool mode_sum3(int m) {
 }
 
 // One destination row (both roles, epilogue) for this lane's columns.
+// spread the 16 low bits of x to the even bit positions
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+  x &= 0xFFFFu;
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  return (x | (x << 1)) & 0x55555555u;
+}
+
 template <int VEC, int MODE, bool W>
 __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64_t r, int32_t s,
                                        int32_t e, int32_t m, float *yrow, bool act, bool fast,
-                                       uint32_t relu_s, uint32_t intra_s,
+                                       int64_t fcol, uint32_t intra_s,
                                        uint32_t iv_bar = 0, uint32_t iv_phase = 0,
                                        bool *iv_pending = nullptr) {
   constexpr bool IS_MAX = MODE == kModeMax;
@@ -661,9 +671,11 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
   // dense-intra mode: the intra role comes from the dense warp's block product
   const int32_t ni = DENSE ? 0 : (SUM3 || (a.mask & 1)) ? m - s : 0;
   const int32_t no = (SUM3 || (a.mask & 2)) ? e - m : 0;
-  // the ReLU-mask operand is loaded before the reduction so its latency hides
+  // the ReLU-mask word is loaded before the reduction so its latency hides
   // behind it
   const bool relu = a.relu && act;
+  const uint32_t rbits = relu ? (__ldg(a.ep.relu_bits + r * a.ldw + (fcol >> 5)) >> (fcol & 31))
+                              : 0u;
   Vf<VEC> I, O;
   if (a.dbg & 1) {
     I = splat<VEC>(0.0f);
@@ -675,14 +687,15 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
     I = lv_out<VEC>(w.template role<IS_MAX>(s, ni));
     O = lv_out<VEC>(COO ? w.role_coo(m, no) : w.template role<IS_MAX>(m, no));
   }
-  if (!act) return;
+  // inactive lanes (columns past F) run the epilogue too -- the relu-bit
+  // ballots need the whole warp -- but store nothing
   float *yp = yrow;
   Vf<VEC> out;
   if constexpr (DENSE) {
     // the block's intra partials: waited for here, after this row's inter
     // reduction, so the dense warps' block product overlaps it
     if (iv_pending && *iv_pending) {
-      mbar_wait(iv_bar, iv_phase);
+      mbar_wait_hint(iv_bar, iv_phase, a.csleep);
       *iv_pending = false;
     }
     out = vadd<VEC>(lv_out<VEC>(lv_lds<VEC>(intra_s)), O);
@@ -715,11 +728,25 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
     for (int i = 0; i < VEC; ++i) out.v[i] = fmaxf(out.v[i], 0.0f);
   }
   if (relu) {
-    const Vf<VEC> h = lv_out<VEC>(lv_lds<VEC>(relu_s));  // staged by the far producer
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) out.v[i] = h.v[i] > 0.0f ? out.v[i] : 0.0f;
+    for (int i = 0; i < VEC; ++i) out.v[i] = (rbits >> i) & 1u ? out.v[i] : 0.0f;
   }
-  if (!(a.dbg & 16)) stv<VEC>(yp, out);
+  if (a.relu_out != nullptr) {
+    // y's relu bits: lane l holds columns fcol .. fcol + VEC - 1 of the tile
+    uint32_t *rw = a.relu_out + r * a.ldw;
+    const int64_t c0 = fcol - static_cast<int64_t>(w.lane) * VEC;  // the tile's first column
+    if constexpr (VEC == 1) {
+      const uint32_t b = __ballot_sync(0xffffffffu, act && out.v[0] > 0.0f);
+      if (w.lane == 0) rw[c0 >> 5] = b;
+    } else {
+      const uint32_t b0 = __ballot_sync(0xffffffffu, act && out.v[0] > 0.0f);
+      const uint32_t b1 = __ballot_sync(0xffffffffu, act && out.v[1] > 0.0f);
+      const uint32_t wd = w.lane == 0 ? spread16(b0) | (spread16(b1) << 1)
+                                      : spread16(b0 >> 16) | (spread16(b1 >> 16) << 1);
+      if (w.lane < 2 && c0 + 32 * w.lane < a.feat) rw[(c0 >> 5) + w.lane] = wd;
+    }
+  }
+  if (act && !(a.dbg & 16)) stv<VEC>(yp, out);
 }
 
 template <int VEC>
@@ -728,8 +755,7 @@ struct SlabGeom {
   static constexpr uint32_t kRowBytes = T * 4;
   static constexpr uint32_t kSlotBytes = kRB * kRowBytes;
   static constexpr uint32_t kFarSlotBytes = kFarMax * kRowBytes;
-  static constexpr uint32_t kReluOff = kSlots * kSlotBytes + kFarSlots * kFarSlotBytes;
-  static constexpr uint32_t kIOff = kReluOff + kReluSlots * kSlotBytes;
+  static constexpr uint32_t kIOff = kSlots * kSlotBytes + kFarSlots * kFarSlotBytes;
   static constexpr uint32_t kWOff = kIOff + kISlots * kSlotBytes;  // 2 warps x 2 x 512 B weights
   static constexpr uint32_t kRingBytes = kWOff + 2 * 1024;
   static constexpr uint32_t kBarBytes = (kReady + kDone + kISlots) * 8;
@@ -900,9 +926,8 @@ __device__ __forceinline__ void produce_x(const GArgs &a, const CUtensorMap *map
 // completing on ready[f].  Look-ahead loads are consumed in place (the loop
 // is unrolled by D): rotating them through moves would wait on each load.
 template <int VEC>
-__device__ __forceinline__ void produce_far(const GArgs &a, const CUtensorMap *relu_map,
-                                            uint32_t ring, const BlockSync &bs, uint32_t kb0,
-                                            uint32_t kb1, int tile, int lane) {
+__device__ __forceinline__ void produce_far(const GArgs &a, uint32_t ring, const BlockSync &bs,
+                                            uint32_t kb0, uint32_t kb1, int tile, int lane) {
   using G = SlabGeom<VEC>;
   constexpr int D = 4;
   const uint32_t far_ring = ring + kSlots * G::kSlotBytes;
@@ -933,20 +958,14 @@ __device__ __forceinline__ void produce_far(const GArgs &a, const CUtensorMap *r
       }
       const uint32_t slot_base = far_ring + fslot * G::kFarSlotBytes;
       if (++fslot == kFarSlots) fslot = 0;
-      // far slot reuse: done[f - kFarSlots]; ReLU tile slot reuse: done[f - kReluSlots]
-      const int64_t need = a.relu ? int64_t(f) - kReluSlots : int64_t(f) - kFarSlots;
-      const uint32_t relu_dst = ring + G::kReluOff + (fi % kReluSlots) * G::kSlotBytes;
+      // far slot reuse: done[f - kFarSlots]
+      const int64_t need = int64_t(f) - kFarSlots;
       if (a.tma) {
         if (lane == 0) {
           tstamp(a, fi, 0);
           if (need >= int64_t(kb0)) bs.wait_done(static_cast<uint32_t>(need));
           tstamp(a, fi, 1);
-          mbar_expect_tx(bs.rdy(f), (a.dbg & 2) ? 0u
-                                                : static_cast<uint32_t>(cnt) * tile_bytes +
-                                                      (a.relu ? G::kSlotBytes : 0u));
-          if (a.relu && !(a.dbg & 2))
-            tma_load_2d(relu_dst, relu_map, bs.rdy(f), static_cast<int>(c0),
-                        static_cast<int>(f * kRB));
+          mbar_expect_tx(bs.rdy(f), (a.dbg & 2) ? 0u : static_cast<uint32_t>(cnt) * tile_bytes);
         }
         __syncwarp();
         if (lane < cnt && !(a.dbg & 2))
@@ -954,18 +973,6 @@ __device__ __forceinline__ void produce_far(const GArgs &a, const CUtensorMap *r
                    tile_bytes, bs.rdy(f));
       } else {
         if (need >= int64_t(kb0)) bs.wait_done(static_cast<uint32_t>(need));
-        if (a.relu) {
-          for (int rr = 0; rr < kRB; ++rr) {
-            const int64_t row = static_cast<int64_t>(f) * kRB + rr;
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) {
-              const int64_t c = c0 + lane * VEC + v;
-              const bool ok = row < a.rows && c < a.feat;
-              cp_async4(relu_dst + (rr * G::T + lane * VEC + v) * 4,
-                        ok ? a.ep.relu_src + row * a.feat + c : a.ep.relu_src, ok ? 4 : 0);
-            }
-          }
-        }
         for (int j = 0; j < cnt; ++j) {
           const int32_t sj = __shfl_sync(0xffffffffu, src, j);
 #pragma unroll
@@ -1021,7 +1028,7 @@ __device__ __forceinline__ void dense_intra(const GArgs &a, uint32_t ring, const
     fetch_w(f + 1, buf ^ 1);
     cp_async_wait<1>();  // this block's weights have landed
     __syncwarp();
-    mbar_wait(bs.rdy(f), bs.rdy_phase(f));  // X block f is in the ring
+    mbar_wait_hint(bs.rdy(f), bs.rdy_phase(f), a.csleep);  // X block f is in the ring
     if (fi >= kISlots) bs.wait_done(f - kISlots);  // the I slot's previous block is consumed
     if (a.dbg & 4) {
       __syncwarp();
@@ -1077,8 +1084,7 @@ __device__ __forceinline__ void dense_intra(const GArgs &a, uint32_t ring, const
 
 template <int VEC, int MODE, bool W>
 __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
-    slab_kernel(const __grid_constant__ CUtensorMap tmap,
-                const __grid_constant__ CUtensorMap relu_map, GArgs a) {
+    slab_kernel(const __grid_constant__ CUtensorMap tmap, GArgs a) {
   using G = SlabGeom<VEC>;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ int64_t s_kb[2];
@@ -1121,7 +1127,7 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
       if (warp == kCons) {
         produce_x<VEC>(a, &tmap, ring, bs, Llo, Lhi, kb0, kb1, H, tile, lane);
       } else if (warp == kCons + 1) {
-        produce_far<VEC>(a, &relu_map, ring, bs, kb0, kb1, tile, lane);
+        produce_far<VEC>(a, ring, bs, kb0, kb1, tile, lane);
       } else if (DENSE && warp >= kCons - kDenseWarps) {
         dense_intra<VEC>(a, ring, bs, ivalid, kb0, kb1, lane, warp - (kCons - kDenseWarps));
       } else {
@@ -1171,12 +1177,13 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
         bool iv_pending = false;  // dense-intra: the current block's ivalid not yet waited for
         auto enter = [&](uint32_t k) {
           if (warp == 0 && lane == 0) tstamp(a, k - kb0, 3);
-          mbar_wait(bs.rdy(k), bs.rdy_phase(k));
+          mbar_wait_hint(bs.rdy(k), bs.rdy_phase(k), a.csleep);
           if (warp == 0 && lane == 0) tstamp(a, k - kb0, 4);
           // dense + coo: waited for at the first epilogue in the block (measured
           // faster); dense + csr: here (the deferred wait costs it registers)
           if (MODE == kModeDense3Coo) iv_pending = true;
-          else if (DENSE) mbar_wait(ivalid + ((k - kb0) % kISlots) * 8, ((k - kb0) / kISlots) & 1u);
+          else if (DENSE)
+            mbar_wait_hint(ivalid + ((k - kb0) % kISlots) * 8, ((k - kb0) / kISlots) & 1u, a.csleep);
         };
         bool entered = false;
 #pragma unroll 1
@@ -1205,16 +1212,14 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
           const int4 info2 = info_at(next_row(rn));
           float *yrow;  // ylane + rr * ld as one IMAD.WIDE.U32
           asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(yrow) : "r"(rr), "r"(ld * 4u), "l"(ylane));
-          const uint32_t relu_s = ring + G::kReluOff + ((k - kb0) % kReluSlots) * G::kSlotBytes +
-                                  (rr % kRB) * G::kRowBytes + lane * VEC * 4;
           const uint32_t intra_s = ring + G::kIOff + ((k - kb0) % kISlots) * G::kSlotBytes +
                                    (rr % kRB) * G::kRowBytes + lane * VEC * 4;
           if constexpr (MODE == kModeDense3Coo)
-            do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, relu_s, intra_s,
+            do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, fcol, intra_s,
                                  ivalid + ((k - kb0) % kISlots) * 8, ((k - kb0) / kISlots) & 1u,
                                  &iv_pending);
           else
-            do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, relu_s, intra_s);
+            do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, fcol, intra_s);
           info = info1;
           info1 = info2;
           q0 = n0;
@@ -1284,6 +1289,7 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
   a.H = window;
   a.dbg = env_int("AG_SLAB_DEBUG", 0);
   a.sleep = env_int("AG_SLAB_SLEEP", 1);
+  a.csleep = static_cast<uint32_t>(env_int("AG_SLAB_CSLEEP", 0));
   a.nblocks = (a.rows + kRB - 1) / kRB;
   a.xblocks = (a.x_rows + kRB - 1) / kRB;
   a.ntiles = static_cast<int>((a.feat + G::T - 1) / G::T);
@@ -1298,11 +1304,11 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
   const int64_t units = ranges * a.ntiles;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, sms)));
 
-  CUtensorMap map, relu_map;
+  CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
-  std::memset(&relu_map, 0, sizeof(relu_map));
   a.tma = 0;
   a.relu = (a.ep.flags & AG_EPI_RELU_MASK) ? 1 : 0;
+  a.ldw = relu_words(a.feat);
   // 2-D fp32 tensor map over [rows, feat] with row stride feat, box 16 x T
   auto encode = [&](CUtensorMap *m, const float *base, int64_t rows) -> bool {
     TmaEncodeFn enc = tma_encode_fn();
@@ -1316,8 +1322,7 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
-  if (a.feat % 4 == 0 && env_int("AG_SLAB_NO_TMA", 0) == 0 && encode(&map, a.x, a.x_rows) &&
-      (!a.relu || encode(&relu_map, a.ep.relu_src, a.rows)))
+  if (a.feat % 4 == 0 && env_int("AG_SLAB_NO_TMA", 0) == 0 && encode(&map, a.x, a.x_rows))
     a.tma = 1;
   const int threads = (mode == kModeDense3Coo ? kConsMax : 14) * 32 + 64;
   long long *trace = nullptr;
@@ -1326,7 +1331,7 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
     AG_CUDA(cudaMemset(trace, 0, kTraceBlocks * 8 * sizeof(long long)));
     a.trace = trace;
   }
-  k<<<grid, threads, smem, st>>>(map, relu_map, a);
+  k<<<grid, threads, smem, st>>>(map, a);
   AG_LAUNCH_CHECK("slab_kernel");
   if (trace) {
     long long h[kTraceBlocks * 8];
@@ -1525,8 +1530,8 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                              const float *blk_w, int64_t num_edges,
                              const float *x, float *y, int32_t op, int32_t epi_flags,
                              const uint8_t *other_touched, const int64_t *deg, float gin_scale,
-                             const float *relu_src, int64_t x_rows, int32_t window,
-                             void *stream) {
+                             const uint32_t *relu_bits, uint32_t *relu_out, int64_t x_rows,
+                             int32_t window, void *stream) {
   if (num_rows < 0 || feat < 0 || num_edges < 0) return fail(AG_ERR_VALUE, "negative sizes");
   if (op < AG_OP_SUM || op > AG_OP_MAX) return fail(AG_ERR_KERNEL, "unknown op %d", op);
   if (role_mask < 1 || role_mask > 3) return fail(AG_ERR_VALUE, "role_mask must be 1, 2 or 3");
@@ -1534,8 +1539,10 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
     return fail(AG_ERR_VALUE, "role_mask 3 needs the role-ordered CSR (role_mid)");
   if (op == AG_OP_MEAN && deg == nullptr && (role_mask == 3 || (epi_flags & AG_EPI_COMBINE)))
     return fail(AG_ERR_KERNEL, "mean combine requires the full-graph degree vector");
-  if ((epi_flags & AG_EPI_RELU_MASK) && relu_src == nullptr)
-    return fail(AG_ERR_VALUE, "AG_EPI_RELU_MASK needs relu_src");
+  if ((epi_flags & AG_EPI_RELU_MASK) && relu_bits == nullptr)
+    return fail(AG_ERR_VALUE, "AG_EPI_RELU_MASK needs relu_bits");
+  if (relu_out != nullptr && !(epi_flags & AG_EPI_RELU))
+    return fail(AG_ERR_VALUE, "relu_out is written with AG_EPI_RELU only");
   if (window < 0 || window > kMaxWindow)
     return fail(AG_ERR_VALUE, "window must be in [0, %d]", kMaxWindow);
   if (x_rows < num_rows) return fail(AG_ERR_VALUE, "x_rows must be >= num_rows");
@@ -1571,13 +1578,13 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
     return fail(AG_ERR_VALUE, "AG_EPI_INTER_COO needs role_mask 3, op sum and role_mid");
   a.x = x;
   a.y = y;
-  a.ep = Epi{op, epi_flags, other_touched, deg, x, feat, gin_scale, relu_src};
+  a.ep = Epi{op, epi_flags, other_touched, deg, x, feat, gin_scale, relu_bits};
+  a.relu_out = relu_out;
   a.cost_total = num_edges + kRowCost * num_rows;
   a.one = 1.0f;
   const bool is_max = op == AG_OP_MAX;
   const bool v2 = feat % 2 == 0 && feat > 32 && (reinterpret_cast<uintptr_t>(x) % 8) == 0 &&
                   (reinterpret_cast<uintptr_t>(y) % 8) == 0 &&
-                  (relu_src == nullptr || (reinterpret_cast<uintptr_t>(relu_src) % 8) == 0) &&
                   env_int("AG_SLAB_VEC", 2) == 2;
   const int mode = blk_w != nullptr ? (coo ? kModeDense3Coo : kModeDense3)
                  : coo ? kModeSum3Coo

@@ -55,6 +55,10 @@ constexpr uint32_t kMnBox = 128 * BK;               // MN-major TMA box {32 mn, 
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = (6 + kEpiWarps) * 32;
 constexpr int kConvWarp0 = 2, kEpiWarp0 = 6;
+// chunked split-K (TcArgs::split_mode 2): k-blocks per tensor-core accumulation
+// 64 k-blocks = 2048 rows: error below numpy's fp32 BLAS at K = 2.45M
+// (scripts/gemm_kerr.py), the per-chunk epilogue amortised
+constexpr int kChunkKb = 64;
 
 struct TcArgs {
   int64_t M, N, K;
@@ -67,9 +71,17 @@ struct TcArgs {
   int b_presplit;  // 1: B's lo half comes from global (ag_tf32_split_lo), only A is split
   int exp;         // timing experiments (AG_TC_EXP bits; results invalid): 1 no split,
                    // 2 one MMA per k-step, 4 no epilogue stores
-  const float *mask;  // ReLU-backward mask operand (NULL: none): out = mask > 0 ? out : 0
-  int64_t ldm;
+  const uint32_t *mask;  // ReLU-backward bit mask (NULL: none): out = bit ? out : 0
+  int64_t ldm;           // words per mask row
+  uint32_t *mask_out;    // (splits == 1) bits of out > 0 (the forward ReLU's mask), or NULL
+  int64_t ldmo;
   int64_t k_per_split;  // multiple of BK
+  // split-K products: 1 = the partial of split s goes to workspace slot s; 2 =
+  // "chunked": every CTA adds each of its (short) K splits into its own slot
+  // [blockIdx.x][M][N] in IEEE fp32, so no tensor-core accumulation runs over
+  // more than k_per_split rows (its fp32 accumulation truncates: the error of
+  // one long accumulation grows with K, measured 20x numpy's at K = 2.45M)
+  int split_mode;
   long long *trace;     // AG_TC_TRACE: per-tile clock stamps of CTA 0 (development only)
 };
 constexpr int kTraceTiles = 48;
@@ -490,8 +502,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int64_t r1 = std::min<int64_t>(r0 + BM, g.M);
           if (r1 <= r0) return;
           const uintptr_t lo = reinterpret_cast<uintptr_t>(g.mask + r0 * g.ldm) & ~uintptr_t(15);
-          const uintptr_t hi =
-              (reinterpret_cast<uintptr_t>(g.mask + (r1 - 1) * g.ldm + g.N) + 15) & ~uintptr_t(15);
+          const uintptr_t hi = (reinterpret_cast<uintptr_t>(g.mask + (r1 - 1) * g.ldm +
+                                                            relu_words(g.N)) + 15) & ~uintptr_t(15);
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo),
                        "r"(static_cast<uint32_t>(hi - lo))
                        : "memory");
@@ -509,8 +521,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool direct = g.splits == 1;
       const bool vec_ok = ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0) &&
                           (direct ? (g.ldc % 4 == 0) : (g.N % 4 == 0));
-      const bool mask_vec = g.mask != nullptr && (reinterpret_cast<uintptr_t>(g.mask) & 15) == 0 &&
-                            g.ldm % 4 == 0;
       // 32-column chunks: tcgen05.ld gives each lane one row; the chunk goes
       // through this warp's shared buffer (16-byte chunks XOR-swizzled by
       // row, conflict-free both ways) so that every global access below is
@@ -567,15 +577,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mk[i0] = make_float4(1.f, 1.f, 1.f, 1.f);
             cv[i0] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (in && g.mask != nullptr && !(g.exp & 8)) {
-              const float *mp = g.mask + grow * g.ldm + col;
-              if (mask_vec && col4) {
-                mk[i0] = __ldg(reinterpret_cast<const float4 *>(mp));
-              } else {
-                mk[i0].x = mp[0];
-                if (col + 1 < g.N) mk[i0].y = mp[1];
-                if (col + 2 < g.N) mk[i0].z = mp[2];
-                if (col + 3 < g.N) mk[i0].w = mp[3];
-              }
+              // the 4 columns' bits of the row's mask word (col % 4 == 0)
+              const uint32_t nib = (__ldg(g.mask + grow * g.ldm + (col >> 5)) >> (col & 31)) & 15u;
+              mk[i0] = make_float4(nib & 1u ? 1.f : 0.f, nib & 2u ? 1.f : 0.f,
+                                   nib & 4u ? 1.f : 0.f, nib & 8u ? 1.f : 0.f);
             }
             if (in && g.beta != 0.0f) {
               const float *cp = g.C + grow * g.ldc + col;
@@ -616,12 +621,42 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+        if (direct && g.mask_out != nullptr) {
+          // forward ReLU mask: the 8 lanes of a row pass hold its 32 columns
+          // [n0 + c, n0 + c + 32) = one mask word (n0, c multiples of 32)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float *ov = &o[i].x;
+            uint32_t nib = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (col + e < g.N && ov[e] > 0.0f) nib |= 1u << e;
+            uint32_t wd = nib << (4 * j4);
+            wd |= __shfl_xor_sync(0xffffffffu, wd, 1);
+            wd |= __shfl_xor_sync(0xffffffffu, wd, 2);
+            wd |= __shfl_xor_sync(0xffffffffu, wd, 4);
+            const int64_t grow = grow0 + 4 * i;
+            if (j4 == 0 && grow < g.M && colok) g.mask_out[grow * g.ldmo + (col >> 5)] = wd;
+          }
+        }
         if (!(g.exp & 4)) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int64_t grow = grow0 + 4 * i;
             if (grow >= g.M || !colok) continue;
-            float *cp = direct ? g.C + grow * g.ldc + col : g.C + (s * g.M + grow) * g.N + col;
+            const int64_t slot = g.split_mode == 2 ? static_cast<int64_t>(blockIdx.x) : s;
+            float *cp = direct ? g.C + grow * g.ldc + col : g.C + (slot * g.M + grow) * g.N + col;
+            if (g.split_mode == 2) {  // this CTA's running sum (slot zeroed by the host)
+              if (vec_ok && col4) {
+                const float4 p = *reinterpret_cast<const float4 *>(cp);
+                o[i].x += p.x; o[i].y += p.y; o[i].z += p.z; o[i].w += p.w;
+              } else {
+                o[i].x += cp[0];
+                if (col + 1 < g.N) o[i].y += cp[1];
+                if (col + 2 < g.N) o[i].z += cp[2];
+                if (col + 3 < g.N) o[i].w += cp[3];
+              }
+            }
             if (vec_ok && col4) {
               *reinterpret_cast<float4 *>(cp) = o[i];
             } else {
@@ -655,17 +690,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 __global__ void splitk_sum_kernel(int64_t M, int64_t N, int splits, const float *part, float *C,
                                   int64_t ldc, float alpha, float beta, int relu,
-                                  const float *mask, int64_t ldm) {
+                                  const uint32_t *mask, int64_t ldm) {
   const int64_t n = M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.0f;
+    double s = 0.0;
     for (int p = 0; p < splits; ++p) s += part[p * n + i];  // fixed order: deterministic
     const int64_t m = i / N, c = i % N;
-    float v = alpha * s;
+    float v = alpha * static_cast<float>(s);
     if (beta != 0.0f) v = fmaf(beta, C[m * ldc + c], v);
     if (relu) v = fmaxf(v, 0.0f);
-    if (mask && !(mask[m * ldm + c] > 0.0f)) v = 0.0f;
+    if (mask && !relu_bit(mask, ldm, m, c)) v = 0.0f;
     C[m * ldc + c] = v;
   }
 }
@@ -788,7 +823,8 @@ extern "C" int ag_tf32_split_lo(int64_t n, const float *src, float *lo, void *st
 extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                               int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
                               const float *B_lo, float *C, int64_t ldc, float alpha, float beta,
-                              int32_t epilogue, const float *mask, int64_t ldm, void *stream) {
+                              int32_t epilogue, const uint32_t *mask, int64_t ldm,
+                              uint32_t *mask_out, int64_t ldmo, void *stream) {
   if (M < 0 || N < 0 || K < 0) return fail(AG_ERR_VALUE, "negative GEMM sizes");
   if (M == 0 || N == 0) return AG_OK;
   const bool a_mn = trans_a != 0;  // A stored [K][M]
@@ -814,6 +850,12 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   g.alpha = alpha; g.beta = beta; g.relu = (epilogue & AG_GEMM_RELU) ? 1 : 0;
   g.mask = mask;
   g.ldm = ldm;
+  g.mask_out = mask_out;
+  g.ldmo = ldmo;
+  if (mask_out != nullptr && ldmo < relu_words(N))
+    return fail(AG_ERR_VALUE, "mask_out row stride must be >= ceil(N / 32) words");
+  if (mask != nullptr && ldm < relu_words(N))
+    return fail(AG_ERR_VALUE, "mask row stride must be >= ceil(N / 32) words");
   g.b_presplit = B_lo != nullptr;
   if (const char *e = std::getenv("AG_TC_EXP")) g.exp = std::atoi(e);
   {
@@ -829,7 +871,24 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   if (tiles < sms / 2 && kblocks >= 16) {  // skinny-output product (dW): split K
     splits = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, sms / tiles), kblocks / 8));
   }
-  const int64_t kb_per = (kblocks + splits - 1) / splits;
+  int64_t kb_per = (kblocks + splits - 1) / splits;
+  g.split_mode = splits > 1 ? 1 : 0;
+  if (splits > 1 && kb_per > kChunkKb) {
+    // long K per split: chunk it (split_mode 2)
+    if (const char *e = std::getenv("AG_TC_CHUNK_BN")) {  // development: narrower tiles
+      bn = std::min(bn, std::max(32, std::atoi(e)));
+      g.n_tiles = static_cast<int>((N + bn - 1) / bn);
+    }
+    int64_t chunk = kChunkKb;
+    if (const char *e = std::getenv("AG_TC_CHUNK_KB")) chunk = std::max(8, std::atoi(e));
+    // as many chunks as needed, rounded up to a multiple of the CTAs per
+    // output tile so every persistent CTA gets the same number of chunks
+    const int64_t per_tile = std::max<int64_t>(1, sms / (static_cast<int64_t>(g.m_tiles) * g.n_tiles));
+    int64_t nsp = (kblocks + chunk - 1) / chunk;
+    nsp = (nsp + per_tile - 1) / per_tile * per_tile;
+    kb_per = (kblocks + nsp - 1) / nsp;
+    g.split_mode = 2;
+  }
   g.k_per_split = kb_per * BK;
   splits = static_cast<int>((kblocks + kb_per - 1) / kb_per);
   g.splits = splits;
@@ -853,7 +912,17 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
     if (rc) return rc;
   }
   Scratch ws;
-  if (splits > 1) {
+  int nparts = splits;
+  if (g.split_mode == 2) {
+    // one zeroed slot per CTA of the persistent grid (launch_tc's grid)
+    const int64_t msup = (g.m_tiles + cl - 1) / cl;
+    const int64_t total = msup * g.n_tiles * static_cast<int64_t>(splits);
+    nparts = static_cast<int>(std::min<int64_t>(total, sms / cl)) * cl;
+    AG_CUDA(ws.alloc(static_cast<size_t>(nparts) * M * N * sizeof(float), st));
+    AG_CUDA(cudaMemsetAsync(ws.ptr, 0, static_cast<size_t>(nparts) * M * N * sizeof(float), st));
+    g.C = ws.as<float>();
+    g.ldc = N;
+  } else if (splits > 1) {
     AG_CUDA(ws.alloc(static_cast<size_t>(splits) * M * N * sizeof(float), st));
     g.C = ws.as<float>();
     g.ldc = N;
@@ -892,9 +961,13 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
     }
   }
   if (splits > 1) {
-    splitk_sum_kernel<<<grid_for(M * N, 256), 256, 0, st>>>(M, N, splits, g.C, C, ldc, alpha,
+    splitk_sum_kernel<<<grid_for(M * N, 256), 256, 0, st>>>(M, N, nparts, g.C, C, ldc, alpha,
                                                             beta, g.relu, mask, ldm);
     AG_LAUNCH_CHECK("splitk_sum_kernel");
+    if (mask_out != nullptr) {
+      rc = ag_relu_bits(M, N, C, ldc, mask_out, ldmo, stream);
+      if (rc) return rc;
+    }
   }
   return AG_OK;
 }

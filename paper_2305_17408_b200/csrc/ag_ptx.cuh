@@ -41,6 +41,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t b, uint32_t parity) {
     if (++spins > (1u << 22)) __trap();
   }
 }
+// Wait with a suspend-time hint of `ns` nanoseconds per poll (0: plain
+// try_wait).  A consumer warp that would otherwise spin gives its issue slots
+// to the warps that have work; it wakes as soon as the phase completes.
+__device__ __forceinline__ void mbar_wait_hint(uint32_t b, uint32_t parity, uint32_t ns) {
+  uint32_t done = 0;
+  uint32_t spins = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(b), "r"(parity), "r"(ns)
+        : "memory");
+    if (done) return;
+    if (++spins > (1u << 22)) __trap();
+  }
+}
 // Same, for a warp that has nothing else to do (the ring producer): each
 // poll suspends the thread in hardware for up to ~1 us, waking as soon as
 // the phase completes, so waiting costs neither issue slots nor latency.

@@ -98,7 +98,7 @@ struct Epi {
   const float *x;  // for the GIN term
   int64_t ld;      // row stride of x and y
   float gin_scale;
-  const float *relu_src = nullptr;  // AG_EPI_RELU_MASK: zero where relu_src <= 0
+  const uint32_t *relu_bits = nullptr;  // AG_EPI_RELU_MASK: zero where the mask bit is 0
 };
 
 // combine() of kernels.py:253-276 fused into the producing kernel, plus the

@@ -281,6 +281,10 @@ class DistGNN:
         gs = self.gin_scale()
         flags = (_lib.AG_EPI_GIN if gs is not None else 0) | \
             (_lib.AG_EPI_RELU_MASK if relu_src is not None else 0)
+        rbits = None
+        if relu_src is not None:  # the kernel reads the layer's bit-packed ReLU mask
+            from .kernels import relu_bits
+            rbits = relu_bits(relu_src)
         e0 = e1 = None
         if self.events is not None:
             e0 = torch.cuda.Event(enable_timing=True)
@@ -290,8 +294,8 @@ class DistGNN:
                   _lib.ptr(op.row_ptr), _lib.ptr(op.mid), *map(_lib.ptr, op.codes()),
                   int(op.val is not None), None,
                   op.num_edges, _lib.ptr(x_ext), _lib.ptr(out), _lib.AG_OP["sum"], flags, None,
-                  _lib.ptr(op.deg), 0.0 if gs is None else gs, _lib.ptr(relu_src), x_ext.shape[0], op.window(),
-                  _lib.stream())
+                  _lib.ptr(op.deg), 0.0 if gs is None else gs, _lib.ptr(rbits), None,
+                  x_ext.shape[0], op.window(), _lib.stream())
         if e0 is not None:
             e1.record()
             self.events.append((e0, e1, F, op))

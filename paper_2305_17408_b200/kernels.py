@@ -92,24 +92,65 @@ def launch_csr(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp, 
               _lib.stream())
 
 
+def relu_words(feat: int) -> int:
+    """uint32 words per row of a bit-packed ReLU mask (include/adaptgear_b200.h)."""
+    return (feat + 31) // 32
+
+
+def relu_bits_empty(rows: int, feat: int, dev) -> torch.Tensor:
+    """Uninitialised [rows, ceil(feat / 32)] int32 relu-bit mask (bit c % 32 of
+    word c // 32 = activation > 0)."""
+    return torch.empty((rows, relu_words(feat)), dtype=torch.int32, device=dev)
+
+
+def relu_bits(h: torch.Tensor) -> torch.Tensor:
+    """The relu-bit mask of an fp32 activation (ag_relu_bits)."""
+    out = relu_bits_empty(h.shape[0], h.shape[1], h.device)
+    _lib.call("ag_relu_bits", h.shape[0], h.shape[1], _lib.ptr(h), h.stride(0), _lib.ptr(out),
+              out.stride(0), _lib.stream())
+    return out
+
+
+def _bits_for(relu_src, relu_bits_in, rows: int, feat: int):
+    """A relu-bit mask for the kernels: given bits (checked) or built from an
+    fp32 relu_src."""
+    if relu_bits_in is not None:
+        if relu_bits_in.dtype != torch.int32 or tuple(relu_bits_in.shape) != (rows, relu_words(feat)) \
+                or not relu_bits_in.is_contiguous():
+            raise ValueError(f"relu bits must be a contiguous int32 [{rows}, {relu_words(feat)}] mask")
+        return relu_bits_in
+    if relu_src is None:
+        return None
+    if tuple(relu_src.shape) != (rows, feat):
+        raise ValueError(f"relu_src must have shape [{rows}, {feat}]")
+    return relu_bits(relu_src)
+
+
 def launch_fused(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp,
                  block: int = 0, mask: int = 2, flags: int = 0,
                  other_touched: torch.Tensor | None = None, deg: torch.Tensor | None = None,
                  gin_scale: float = 0.0, relu_src: torch.Tensor | None = None,
-                 dense_intra: bool = False) -> None:
+                 dense_intra: bool = False, relu_bits_in: torch.Tensor | None = None,
+                 relu_out: torch.Tensor | None = None) -> None:
     """ag_fused_spmm: slab (smem X ring) row gather, reduceat-order reduction (+ role split).
 
     block > 0 splits every row into its intra run and inter edges (role-ordered
     copy of the CSR, built once); block == 0 treats the row as one role.
+    relu_src (fp32) / relu_bits_in (bit mask) apply the ReLU backward of the
+    layer below in the epilogue; relu_out receives y's relu bits (with
+    AG_EPI_RELU in flags).
     """
+    rb = _bits_for(relu_src, relu_bits_in, a.num_vertices, x.shape[1])
+    if relu_out is not None:
+        _bits_for(None, relu_out, a.num_vertices, x.shape[1])
     mid, cv, rowinfo, far_cnt, far_src, weighted = a.slab_layout(block)
     _lib.call("ag_fused_spmm", a.num_vertices, x.shape[1], int(mask), _lib.ptr(a.row_ptr),
               _lib.ptr(mid), _lib.ptr(cv), _lib.ptr(rowinfo), _lib.ptr(far_cnt),
               _lib.ptr(far_src), weighted,
               _lib.ptr(a.dense_blocks16() if dense_intra else None), a.num_edges, _lib.ptr(x), _lib.ptr(y),
-              _opcode(op), flags | (_lib.AG_EPI_RELU_MASK if relu_src is not None else 0),
-              _lib.ptr(other_touched), _lib.ptr(deg), float(gin_scale), _lib.ptr(relu_src),
-              x.shape[0], a.window(), _lib.stream())
+              _opcode(op), flags | (_lib.AG_EPI_RELU_MASK if rb is not None else 0),
+              _lib.ptr(other_touched), _lib.ptr(deg), float(gin_scale), _lib.ptr(rb),
+              _lib.ptr(relu_out), x.shape[0], a.window(), _lib.stream())
 
 
 def _check_block_local(a: CsrMatrix, block_size: int) -> None:
@@ -256,14 +297,16 @@ def _tc_ok(t: torch.Tensor) -> bool:
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
          trans_a: bool = False, trans_b: bool = False, alpha: float = 1.0, beta: float = 0.0,
          relu: bool = False, relu_mask: torch.Tensor | None = None,
-         engine: str = "auto") -> torch.Tensor:
+         engine: str = "auto", relu_mask_bits: torch.Tensor | None = None,
+         mask_out: torch.Tensor | None = None) -> torch.Tensor:
     """out = alpha * op(a) @ op(b) + beta * out (the layers' update GEMM).
 
     engine "auto" runs the tcgen05 3xTF32 tensor-core kernel (ag_gemm_tf32x3)
     whenever the operands are 16-byte aligned with row strides that are
     multiples of 4 floats, else the fp32 SIMT kernel (ag_gemm_f32); "tc" /
     "simt" force one of them.  relu_mask fuses the ReLU backward of the layer
-    below: out = relu_mask > 0 ? out : 0 (same shape as out).
+    below: out = relu_mask > 0 ? out : 0 (same shape as out); relu_mask_bits
+    is the same as a bit-packed mask.  mask_out receives out's relu bits.
     """
     M = a.shape[1] if trans_a else a.shape[0]
     K = a.shape[0] if trans_a else a.shape[1]
@@ -275,7 +318,11 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
         out = torch.empty((M, N), dtype=torch.float32, device=a.device)
     tc = engine == "tc" or (engine == "auto" and K > 0 and _tc_ok(a) and _tc_ok(b))
     epi = _lib.AG_GEMM_RELU if relu else 0
-    mask_ld = 0 if relu_mask is None else relu_mask.stride(0)
+    mbits = _bits_for(relu_mask, relu_mask_bits, M, N)
+    mask_ld = 0 if mbits is None else mbits.stride(0)
+    if mask_out is not None:
+        _bits_for(None, mask_out, M, N)
+    mo_ld = 0 if mask_out is None else mask_out.stride(0)
     if tc:
         b_lo = None
         if b.shape[0] * b.stride(0) <= PRESPLIT_MAX_ELEMS:
@@ -287,11 +334,13 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
                       _lib.stream())
         _lib.call("ag_gemm_tf32x3", M, N, K, _lib.ptr(a), a.stride(0), int(trans_a), _lib.ptr(b),
                   b.stride(0), int(trans_b), _lib.ptr(b_lo), _lib.ptr(out), out.stride(0),
-                  float(alpha), float(beta), epi, _lib.ptr(relu_mask), mask_ld, _lib.stream())
+                  float(alpha), float(beta), epi, _lib.ptr(mbits), mask_ld, _lib.ptr(mask_out),
+                  mo_ld, _lib.stream())
     else:
         _lib.call("ag_gemm_f32", M, N, K, _lib.ptr(a), a.stride(0), int(trans_a), _lib.ptr(b),
                   b.stride(0), int(trans_b), _lib.ptr(out), out.stride(0), float(alpha),
-                  float(beta), epi, _lib.ptr(relu_mask), mask_ld, _lib.stream())
+                  float(beta), epi, _lib.ptr(mbits), mask_ld, _lib.ptr(mask_out), mo_ld,
+                  _lib.stream())
     return out
 
 
@@ -435,10 +484,14 @@ def run_fused_pair(d: DecomposedGraph, x: torch.Tensor, y: torch.Tensor, op: Agg
                    gin_scale: float | None = None, relu_src: torch.Tensor | None = None,
                    relu: bool = False, dense_intra: bool = False,
                    kernel_intra: KernelKind | None = None,
-                   kernel_inter: KernelKind = KernelKind.CSR_INTER) -> None:
+                   kernel_inter: KernelKind = KernelKind.CSR_INTER,
+                   relu_bits_in: torch.Tensor | None = None,
+                   relu_out: torch.Tensor | None = None) -> None:
     """y = combine(intra, inter) [+ gin] [relu] [* (relu_src > 0)] in one pass
     over the full reordered CSR for the selector pair (kernel_intra,
-    kernel_inter); `dense_intra` is shorthand for kernel_intra=dense_block."""
+    kernel_inter); `dense_intra` is shorthand for kernel_intra=dense_block.
+    The ReLU-backward mask is relu_src (fp32) or relu_bits_in (bit mask);
+    with relu=True, relu_out receives y's relu bits."""
     if kernel_intra is None:
         kernel_intra = KernelKind.DENSE_BLOCK if dense_intra else KernelKind.CSR_INTRA_BLOCKED
     if not fused_ok(kernel_intra, kernel_inter, d.block_size, op):
@@ -450,7 +503,8 @@ def run_fused_pair(d: DecomposedGraph, x: torch.Tensor, y: torch.Tensor, op: Agg
              | (_lib.AG_EPI_INTER_COO if kernel_inter is KernelKind.COO_ATOMIC else 0))
     launch_fused(to_csr(full), x, y, op, block=d.block_size, mask=3, flags=flags,
                  deg=d.full_in_degree, gin_scale=0.0 if gin_scale is None else gin_scale,
-                 relu_src=relu_src, dense_intra=kernel_intra is KernelKind.DENSE_BLOCK)
+                 relu_src=relu_src, dense_intra=kernel_intra is KernelKind.DENSE_BLOCK,
+                 relu_bits_in=relu_bits_in, relu_out=relu_out if relu else None)
 
 
 def aggregate_full(g: Graph, x, op: AggregateOp, kernel: KernelKind = KernelKind.CSR_INTER,

@@ -34,6 +34,7 @@ from .kernels import (
     aggregate_full,
     fused_ok,
     gemm,
+    relu_bits_empty,
     run_fused_pair,
 )
 
@@ -229,6 +230,12 @@ class GNN:
     default_pair: tuple = (KernelKind.CSR_INTRA_BLOCKED, KernelKind.CSR_INTER)
     # when a list, every aggregation appends (start_event, end_event, F, subject)
     events: list | None = None
+    # update-GEMM arithmetic: "tf32x3" -- tcgen05 3xTF32 (fp32-faithful to a few
+    # ulp per product, but the tensor core's truncating fp32 accumulation biases
+    # long chains; stated tolerance: loss within 1e-4 relative of the exact
+    # composition, tests/test_config_parity_gpu.py); "fp32" -- the fp32 FMA
+    # SIMT kernel (IEEE, the reference BLAS's arithmetic; within 1e-5)
+    precision: str = "tf32x3"
 
     @classmethod
     def build(cls, model: str, dims, subject: DecomposedGraph, seed: int = 0,
@@ -260,7 +267,7 @@ class GNN:
     def gin_scale(self) -> float | None:
         return float(np.float32(1.0 + self.gin_eps)) if self.model == "gin" else None
 
-    def autotune(self, profile_iters: int = 3) -> dict:
+    def autotune(self, profile_iters: int = 3, cache=None) -> dict:
         """Run the adaptive selector once per (direction, width); cache the pairs.
 
         The selector itself is the reference's (per-role argmin of separately
@@ -271,10 +278,14 @@ class GNN:
         csr_inter or coo_atomic), the pair actually executed is the fastest
         of the selector's pair and the fused pairs, timed once more on the
         device.
+
+        `cache` (a selector.ChoiceCache) persists both pairs per (graph, op,
+        width, direction): a hit skips the profiling entirely.
         """
-        from .selector import SelectorState, run_training_loop
+        from .selector import SelectorState, graph_key, run_training_loop
         if not hasattr(self, "selector_choice"):
             self.selector_choice = {}
+        gkeys = {}
         L = self.num_layers
         fwd = [_pad4(self.dims[l + 1]) if self.gemm_first(l) else self.dims[l] for l in range(L)]
         bwd = [_pad4(self.dims[l + 1]) if self.gemm_first(l) else self.dims[l]
@@ -283,6 +294,17 @@ class GNN:
             for f in sorted(set(widths)):
                 if (direction, f) in self.kernels:
                     continue
+                ckey = None
+                if cache is not None:
+                    if direction not in gkeys:
+                        gkeys[direction] = graph_key(subj)
+                    ckey = cache.key(gkeys[direction], AggregateOp.SUM, f, direction)
+                    hit = cache.get(ckey)
+                    run = cache.get_run(ckey)
+                    if hit is not None and run is not None:
+                        self.selector_choice[(direction, f)] = (hit.choice_intra, hit.choice_inter)
+                        self.kernels[(direction, f)] = run
+                        continue
                 x = torch.randn((subj.num_vertices, f), device=_lib.device())
                 s = SelectorState.fresh(AggregateOp.SUM, profile_iters_per_candidate=profile_iters)
                 _, s, _ = run_training_loop(subj, x, AggregateOp.SUM, s.total_profiling_iters, s)
@@ -305,18 +327,29 @@ class GNN:
                         reps=7)
                     if best_t is None or t < best_t:
                         best, best_t = cand, t
-                pair = best
-                self.kernels[(direction, f)] = pair
+                self.kernels[(direction, f)] = best
+                if cache is not None:
+                    cache.put(ckey, s, run=best)
         return dict(self.kernels)
+
+    def _gemm(self, *args, **kwargs):
+        if self.precision == "fp32":
+            kwargs["engine"] = "simt"
+        elif self.precision != "tf32x3":
+            raise ValueError(f"unknown precision {self.precision!r}")
+        return gemm(*args, **kwargs)
 
     def gemm_first(self, l: int) -> bool:
         return self.reassociate and self.dims[l + 1] < self.dims[l]
 
     def _aggregate(self, subj: DecomposedGraph, h: torch.Tensor, direction: str,
-                   relu_src: torch.Tensor | None = None, relu: bool = False):
-        """Aggregation of one layer; relu_src fuses the ReLU backward of the
-        layer below into the (transposed) aggregation's epilogue, relu the
-        forward activation (gemm-first layers)."""
+                   relu_src: torch.Tensor | None = None, relu: bool = False,
+                   relu_bits_in: torch.Tensor | None = None,
+                   relu_out: torch.Tensor | None = None):
+        """Aggregation of one layer; relu_src (fp32) / relu_bits_in (its bit
+        mask, read by the fused kernel) fuse the ReLU backward of the layer
+        below into the (transposed) aggregation's epilogue, relu the forward
+        activation (gemm-first layers), whose bit mask goes to relu_out."""
         ki, ke = self.pair(direction, h.shape[1])
         if relu_src is not None and relu_src.stride(0) != relu_src.shape[1]:
             relu_src = relu_src.contiguous()  # the kernel reads it with row stride F
@@ -329,8 +362,10 @@ class GNN:
             h = _check_features(subj.num_vertices, h)
             out = torch.empty((subj.num_vertices, h.shape[1]), dtype=torch.float32,
                               device=h.device)
-            run_fused_pair(subj, h, out, AggregateOp.SUM, self.gin_scale(), relu_src=relu_src,
-                           relu=relu, kernel_intra=ki, kernel_inter=ke)
+            run_fused_pair(subj, h, out, AggregateOp.SUM, self.gin_scale(),
+                           relu_src=None if relu_bits_in is not None else relu_src,
+                           relu=relu, kernel_intra=ki, kernel_inter=ke,
+                           relu_bits_in=relu_bits_in, relu_out=relu_out)
         else:
             out = aggregate_decomposed(subj, h, AggregateOp.SUM, kernel_intra=ki,
                                        kernel_inter=ke, gin_scale=self.gin_scale())
@@ -340,32 +375,41 @@ class GNN:
             if relu:  # out = out > 0 ? out : 0
                 _lib.call("ag_relu_backward", out.numel(), _lib.ptr(out), _lib.ptr(out),
                           _lib.stream())
+                if relu_out is not None:
+                    _lib.call("ag_relu_bits", out.shape[0], out.shape[1], _lib.ptr(out),
+                              out.stride(0), _lib.ptr(relu_out), relu_out.stride(0),
+                              _lib.stream())
         if e0 is not None:
             e1.record()
             self.events.append((e0, e1, h.shape[1], subj))
         return out
 
     def forward(self, x: torch.Tensor):
-        """Returns (logits, saved) with saved[l] = (kind, operand, output):
+        """Returns (logits, saved) with saved[l] = (kind, operand, output, bits):
         kind "agg" -- operand is A_hat H_l (agg first, models.py:86-112 order);
-        kind "gemm" -- operand is H_l itself (gemm first, narrowing layers)."""
+        kind "gemm" -- operand is H_l itself (gemm first, narrowing layers);
+        bits -- the hidden output's bit-packed ReLU mask (written by the
+        epilogue that applies the ReLU; None for the last layer), which the
+        backward's ReLU epilogues read instead of the fp32 output."""
         saved = []
         h = x
         for l in range(self.num_layers):
             last = l == self.num_layers - 1
+            bits = None if last else relu_bits_empty(h.shape[0], self.dims[l + 1], h.device)
             if self.gemm_first(l):
                 # P = H W over the zero-padded output width, then A_hat P (+ GIN
                 # (1+eps) P) with the activation fused into the aggregation
                 p = _padded_empty(h.shape[0], self.dims[l + 1], h.device)
-                gemm(h, self.weights[l], p)
-                out = self._aggregate(self.subject, _base(p), "fwd", relu=not last)
+                self._gemm(h, self.weights[l], p)
+                out = self._aggregate(self.subject, _base(p), "fwd", relu=not last,
+                                      relu_out=bits)
                 out = out[:, :self.dims[l + 1]]
-                saved.append(("gemm", h, out))
+                saved.append(("gemm", h, out, bits))
             else:
                 agg = self._aggregate(self.subject, h, "fwd")
                 out = _padded_empty(agg.shape[0], self.dims[l + 1], agg.device)
-                gemm(agg, self.weights[l], out, relu=not last)
-                saved.append(("agg", agg, out))
+                self._gemm(agg, self.weights[l], out, relu=not last, mask_out=bits)
+                saved.append(("agg", agg, out, bits))
             h = out
         return h, saved
 
@@ -374,16 +418,18 @@ class GNN:
         grads = [None] * self.num_layers
         g = d_logits
         for l in range(self.num_layers - 1, -1, -1):
-            kind, operand, _ = saved[l]
+            kind, operand, _, _ = saved[l]
             grads[l] = torch.zeros((self.dims[l], _pad4(self.dims[l + 1])), dtype=torch.float32,
                                    device=g.device)[:, :self.dims[l + 1]]
             h_prev = saved[l - 1][2] if l > 0 else None
+            bits_prev = saved[l - 1][3] if l > 0 else None
             if kind == "agg":
-                gemm(operand, g, grads[l], trans_a=True)                 # dW = (A H)^T g
+                self._gemm(operand, g, grads[l], trans_a=True)                 # dW = (A H)^T g
                 if l == 0:
                     break
-                d_in = gemm(g, self.weights[l], trans_b=True)          # d(A H) = g W^T
-                g = self._aggregate(self.subject_t, d_in, "bwd", relu_src=h_prev)
+                d_in = self._gemm(g, self.weights[l], trans_b=True)          # d(A H) = g W^T
+                g = self._aggregate(self.subject_t, d_in, "bwd", relu_src=h_prev,
+                                    relu_bits_in=bits_prev)
             else:
                 # q = A_hat^T g (+ (1+eps) g), at the layer's (narrow) output width,
                 # aggregated over the zero-padded width autotune tuned for
@@ -394,11 +440,11 @@ class GNN:
                     gp[:, :g.shape[1]] = g
                     gb = gp
                 q = self._aggregate(self.subject_t, gb, "bwd")[:, :self.dims[l + 1]]
-                gemm(operand, q, grads[l], trans_a=True)                 # dW = H^T q
+                self._gemm(operand, q, grads[l], trans_a=True)                 # dW = H^T q
                 if l == 0:
                     break
                 g = _padded_empty(q.shape[0], self.dims[l], q.device)
-                gemm(q, self.weights[l], g, trans_b=True, relu_mask=h_prev)  # dH, ReLU bwd
+                self._gemm(q, self.weights[l], g, trans_b=True, relu_mask_bits=bits_prev)  # dH, ReLU bwd
         return grads
 
     def loss_and_grad(self, logits, labels, mask, num_masked: int):

@@ -83,3 +83,14 @@ def test_bad_format(tmp_path):
         emit_report({"a": 1}, "csv", tmp_path / "r.csv")
     with pytest.raises(ValueError):
         parse_report(tmp_path / "r.xml", "xml")
+
+
+def test_threaded_candidates_equal_single_call():
+    """oracle/synth.py's chunked thread-pool candidate draw (used to build the
+    C5 graph for the host baseline) equals one vectorised call."""
+    from oracle import synth as osynth
+    n = (1 << 20) + 12345
+    args = (100_000, 16, 0.4, 0.05, 16, 1, 3)
+    d1, s1 = osynth.candidates(*args, 0, n)
+    d2, s2 = osynth._candidates_threaded(*args, n, threads=5)
+    assert np.array_equal(d1, d2) and np.array_equal(s1, s2)

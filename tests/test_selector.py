@@ -110,3 +110,15 @@ def test_choice_cache_roundtrip(tmp_path):
     assert (s2.choice_intra, s2.choice_inter) == (s.choice_intra, s.choice_inter)
     with pytest.raises(SelectorError):
         c.put(key, SelectorState.fresh(AggregateOp.SUM))
+
+
+def test_choice_cache_run_pair_and_counts(tmp_path):
+    s, _ = drive(SelectorState.fresh(AggregateOp.SUM), {k: [1.0] * 3 for k in KEYS})
+    c = ChoiceCache(tmp_path / "sub" / "choices.json")
+    key = ChoiceCache.key("g1", AggregateOp.SUM, 48, "bwd")
+    assert key.endswith("|bwd") and c.get(key) is None and c.misses == 1
+    run = (KernelKind.DENSE_BLOCK, KernelKind.COO_ATOMIC)
+    c.put(key, s, run=run)
+    c2 = ChoiceCache(tmp_path / "sub" / "choices.json")
+    assert c2.get_run(key) == run and c2.get(key) is not None and c2.hits == 1
+    assert c2.get_run(ChoiceCache.key("g1", AggregateOp.SUM, 48, "fwd")) is None
