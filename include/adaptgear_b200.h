@@ -199,6 +199,22 @@ int ag_dense_block_spmm(int64_t num_rows, int64_t feat, int64_t block_size,
                         const uint8_t *other_touched, const int64_t *deg,
                         float gin_scale, void *stream);
 
+/* Tensor-core dense_block (K4 on tcgen05): the DenseBlockSet as
+ * block-diagonal panels of width panel = max(block_size, 128) (block_size
+ * divides 128 -- 8 blocks of 16 share a 128 x 128 panel, zeros off their
+ * diagonal -- or is a multiple of 128), A[num_rows][lda]; then
+ *   y[r] = A[r][0:panel] @ x[(r / panel) * panel + k]  (+ beta * y[r])
+ * with kind::tf32 3xTF32 (fp32-faithful: ~1e-7 of the sum of |terms|; the
+ * reference's BLAS matmul order is unpinned anyway, kernels.py:247).  beta 1
+ * accumulates onto an inter partial already in y (combine(sum)). */
+int ag_dense_block_pack(int64_t num_rows, int64_t block_size, int64_t panel,
+                        const int32_t *comm_slot, const float *blocks, float *A,
+                        int64_t lda, void *stream);
+int ag_block_diag_gemm_tf32x3(int64_t num_rows, int64_t feat, int64_t panel,
+                              const float *A, int64_t lda, const float *x, int64_t ldx,
+                              int64_t x_rows, float *y, int64_t ldy, float beta,
+                              void *stream);
+
 /* Role-ordered CSR of the fused kernel, built once per (topology, B):
  * every row's edges re-listed as its intra run (cols in [floor(r/B)B, +B),
  * ascending) followed by its inter edges (the sorted row's prefix ++ suffix,
@@ -231,6 +247,11 @@ int ag_role_csr_build(int64_t num_rows, const int32_t *row_ptr,
  * round-robin, reducing out of shared memory.  `window` only affects speed,
  * never values (ag_slab_window picks it per graph).  Any F (TMA when
  * F % 4 == 0 and x is 16-byte aligned, cp.async otherwise).
+ * max_block_edges (0: unknown): the most edges any 16-row block holds
+ * (ag_slab_max_block_edges); when every block's pairs fit a shared-memory
+ * topology slot, the far producer bulk-copies each block's rowinfo and pairs
+ * ahead of the consumers ("staged topology") instead of the consumers
+ * loading their rows' topology from global memory.
  * blk_w (NULL: bitwise intra role): the pair (dense_block, csr_inter) of the
  * reference's selector in one pass -- the intra role of every 16-row block as
  * a dense 16 x 16 block product (ag_slab_dense_blocks; the reference's
@@ -245,7 +266,8 @@ int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                   const float *x, float *y,
                   int32_t op, int32_t epi_flags, const uint8_t *other_touched,
                   const int64_t *deg, float gin_scale, const uint32_t *relu_bits,
-                  uint32_t *relu_out, int64_t x_rows, int32_t window, void *stream);
+                  uint32_t *relu_out, int64_t x_rows, int32_t window,
+                  int64_t max_block_edges, void *stream);
 
 /* Window radius (in 16-row blocks) for ag_fused_spmm over this CSR: the
  * smallest radius whose ring covers `coverage` (e.g. 0.995) of the edges the
@@ -279,6 +301,10 @@ int ag_slab_codes(int64_t num_rows, const int32_t *row_ptr,
 int ag_slab_dense_blocks(int64_t num_rows, const int32_t *row_ptr,
                          const int32_t *role_mid, const int32_t *role_col,
                          const float *role_val, float *blk_w, void *stream);
+/* The most edges any 16-row block [16b, 16b + 16) of a CSR holds (synchronous;
+ * call once per topology and cache): ag_fused_spmm's max_block_edges. */
+int ag_slab_max_block_edges(int64_t num_rows, const int32_t *row_ptr,
+                            int64_t *max_edges, void *stream);
 /* Staged far sources per 16-row block (the far-ring capacity). */
 int ag_slab_far_capacity(void);
 

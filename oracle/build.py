@@ -19,6 +19,25 @@ def build(force: bool = False) -> pathlib.Path:
     return OUT
 
 
+REFERENCE_TESTS = pathlib.Path("/root/reference/pkg/tests")
+REF_STAGE = HERE / "_ref" / "reftests"
+STAGED = ("conftest.py", "test_kernels.py", "test_models.py", "test_selector.py")
+
+
+def stage_reference_tests() -> pathlib.Path | None:
+    """Stage the reference's own kernel / model / selector test files in
+    oracle/_ref/reftests (git-ignored; travels to the GPU box like the other
+    _ref outputs) so tests/test_dropin_gpu.py can run them unmodified against
+    the package.  Only when /root/reference is present (this container)."""
+    if not REFERENCE_TESTS.is_dir():
+        return REF_STAGE if REF_STAGE.is_dir() else None
+    import shutil
+    REF_STAGE.mkdir(parents=True, exist_ok=True)
+    for name in STAGED:
+        shutil.copyfile(REFERENCE_TESTS / name, REF_STAGE / name)
+    return REF_STAGE
+
+
 def load() -> ctypes.CDLL:
     lib = ctypes.CDLL(str(build()))
     P, I64 = ctypes.c_void_p, ctypes.c_int64
@@ -47,3 +66,4 @@ def csr_sum(row_ptr, col, val, x):
 
 if __name__ == "__main__":
     print(build(force=True))
+    print(stage_reference_tests())

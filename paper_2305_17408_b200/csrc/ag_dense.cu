@@ -298,6 +298,28 @@ __global__ void relu_bits_kernel(int64_t rows, int64_t feat, const float *h, int
   }
 }
 
+// Dense diagonal blocks -> block-diagonal panels for the tensor-core dense
+// block product: row r of A (panel width P = max(B, 128)) holds block
+// b = r / B's row r - bB at columns bB - pb .. bB - pb + B (pb = the panel's
+// first row), zeros elsewhere; a missing community (comm_slot < 0) is a zero row.
+__global__ void dense_block_pack_kernel(int64_t rows, int64_t B, int64_t P,
+                                        const int32_t *comm_slot, const float *blocks, float *A,
+                                        int64_t lda) {
+  const int64_t n = rows * P;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / P, c = i % P;
+    const int64_t b = r / B, pb = (r / P) * P;
+    const int64_t j = c - (b * B - pb);
+    float v = 0.0f;
+    if (j >= 0 && j < B) {
+      const int32_t slot = comm_slot[b];
+      if (slot >= 0) v = blocks[(static_cast<int64_t>(slot) * B + (r - b * B)) * B + j];
+    }
+    A[r * lda + c] = v;
+  }
+}
+
 __global__ void relu_bwd_kernel(int64_t n, const float *h, float *g) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -404,6 +426,21 @@ extern "C" int ag_relu_bits(int64_t rows, int64_t feat, const float *h, int64_t 
   relu_bits_kernel<<<grid_for(warps * 32, 256), 256, 0, as_stream(stream)>>>(rows, feat, h, ld,
                                                                           bits, ldw);
   AG_LAUNCH_CHECK("relu_bits_kernel");
+  return AG_OK;
+}
+
+extern "C" int ag_dense_block_pack(int64_t num_rows, int64_t block_size, int64_t panel,
+                                   const int32_t *comm_slot, const float *blocks, float *A,
+                                   int64_t lda, void *stream) {
+  if (num_rows < 0 || block_size < 1) return fail(AG_ERR_VALUE, "bad dense block sizes");
+  if (panel % 128 != 0 || (block_size <= 128 ? panel != 128 : panel != block_size) ||
+      (block_size < 128 && 128 % block_size != 0) || lda < panel)
+    return fail(AG_ERR_VALUE, "panel must be max(block_size, 128) with block_size dividing 128 "
+                              "or a multiple of 128");
+  if (num_rows == 0) return AG_OK;
+  dense_block_pack_kernel<<<grid_for(num_rows * panel, 256), 256, 0, as_stream(stream)>>>(
+      num_rows, block_size, panel, comm_slot, blocks, A, lda);
+  AG_LAUNCH_CHECK("dense_block_pack_kernel");
   return AG_OK;
 }
 

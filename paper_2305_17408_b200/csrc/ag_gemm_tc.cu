@@ -56,9 +56,12 @@ constexpr int kEpiWarps = 8;
 constexpr int kThreads = (6 + kEpiWarps) * 32;
 constexpr int kConvWarp0 = 2, kEpiWarp0 = 6;
 // chunked split-K (TcArgs::split_mode 2): k-blocks per tensor-core accumulation
-// 64 k-blocks = 2048 rows: error below numpy's fp32 BLAS at K = 2.45M
-// (scripts/gemm_kerr.py), the per-chunk epilogue amortised
-constexpr int kChunkKb = 64;
+// chunk length 1024 k-blocks = 32768 rows: products up to ~4.8M rows keep
+// one accumulation per CTA (C5 dW: 33k rows per split, 3e-7 of the sum of
+// |terms|, scripts/gemm_kerr.py); longer K is chunked so the truncation of
+// one accumulation stays bounded.  Shorter chunks measured slower (per-chunk
+// epilogue round trips and workspace): 2048 rows 2.15 ms vs 1.68 ms at C5.
+constexpr int kChunkKb = 1024;
 
 struct TcArgs {
   int64_t M, N, K;
@@ -82,6 +85,9 @@ struct TcArgs {
   // more than k_per_split rows (its fp32 accumulation truncates: the error of
   // one long accumulation grows with K, measured 20x numpy's at K = 2.45M)
   int split_mode;
+  // block-diagonal product (ag_block_diag_gemm_tf32x3): the B operand's K rows
+  // of output tile m0 start at the panel base (m0 / bdiag) * bdiag; 0 = plain GEMM
+  int64_t bdiag;
   long long *trace;     // AG_TC_TRACE: per-tile clock stamps of CTA 0 (development only)
 };
 constexpr int kTraceTiles = 48;
@@ -370,18 +376,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(sa, &tmA, &full[stage], kk, m0);
           }
           // B (and its presplit lo half): this CTA's 1/CL share, multicast
+          // block-diagonal mode: this tile's B rows start at its panel base
+          const int kb_row = kk + (g.bdiag ? static_cast<int>((m0 / g.bdiag) * g.bdiag) : 0);
           auto load_b = [&](unsigned char *dst, const CUtensorMap *map) {
             if (B_MN) {  // BN/32 boxes {32 (n), 32 (k)}: box c from CTA c % CL
 #pragma unroll
               for (int c = 0; c < BN / 32; ++c) {
-                if (CL == 1) tma_load_2d(dst + c * kMnBox, map, &full[stage], n0 + 32 * c, kk);
+                if (CL == 1) tma_load_2d(dst + c * kMnBox, map, &full[stage], n0 + 32 * c, kb_row);
                 else if (c % CL == rank)
-                  tma_load_2d_mc(dst + c * kMnBox, map, &full[stage], n0 + 32 * c, kk, kAll);
+                  tma_load_2d_mc(dst + c * kMnBox, map, &full[stage], n0 + 32 * c, kb_row, kAll);
               }
             } else {  // box {32 (k), BN / CL rows}: rows of 128 B, 8-row swizzle atoms
               constexpr int R = BN / CL;
-              if (CL == 1) tma_load_2d(dst, map, &full[stage], kk, n0);
-              else tma_load_2d_mc(dst + rank * R * kKRow, map, &full[stage], kk, n0 + rank * R,
+              if (CL == 1) tma_load_2d(dst, map, &full[stage], kb_row, n0);
+              else tma_load_2d_mc(dst + rank * R * kKRow, map, &full[stage], kb_row, n0 + rank * R,
                                   kAll);
             }
           };
@@ -820,11 +828,15 @@ extern "C" int ag_tf32_split_lo(int64_t n, const float *src, float *lo, void *st
   return AG_OK;
 }
 
-extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
-                              int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
-                              const float *B_lo, float *C, int64_t ldc, float alpha, float beta,
-                              int32_t epilogue, const uint32_t *mask, int64_t ldm,
-                              uint32_t *mask_out, int64_t ldmo, void *stream) {
+namespace ag {
+namespace {
+// bdiag > 0: block-diagonal product C[m] = A[m][0:K] @ B[(m / bdiag) * bdiag + k] with B
+// (N-major, not transposed) holding b_rows rows
+int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int32_t trans_a,
+            const float *B, int64_t ldb, int32_t trans_b, const float *B_lo, float *C,
+            int64_t ldc, float alpha, float beta, int32_t epilogue, const uint32_t *mask,
+            int64_t ldm, uint32_t *mask_out, int64_t ldmo, int64_t bdiag, int64_t b_rows,
+            void *stream) {
   if (M < 0 || N < 0 || K < 0) return fail(AG_ERR_VALUE, "negative GEMM sizes");
   if (M == 0 || N == 0) return AG_OK;
   const bool a_mn = trans_a != 0;  // A stored [K][M]
@@ -857,6 +869,7 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   if (mask != nullptr && ldm < relu_words(N))
     return fail(AG_ERR_VALUE, "mask row stride must be >= ceil(N / 32) words");
   g.b_presplit = B_lo != nullptr;
+  g.bdiag = bdiag;
   if (const char *e = std::getenv("AG_TC_EXP")) g.exp = std::atoi(e);
   {
     const char *rh = std::getenv("AG_TC_RAWHI");
@@ -868,7 +881,7 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   const int sms = sm_count();
   int splits = 1;
   const int64_t kblocks = (K + BK - 1) / BK;
-  if (tiles < sms / 2 && kblocks >= 16) {  // skinny-output product (dW): split K
+  if (tiles < sms / 2 && kblocks >= 16 && bdiag == 0) {  // skinny-output product (dW): split K
     splits = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, sms / tiles), kblocks / 8));
   }
   int64_t kb_per = (kblocks + splits - 1) / splits;
@@ -896,13 +909,14 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
   // (not for the M-major, split-K dW products: measured slower there)
   int cl = (bn >= 64 && g.m_tiles >= 2 && !a_mn) ? 2 : 1;
   if (const char *e = std::getenv("AG_TC_CL")) cl = std::atoi(e) == 2 && bn >= 64 ? 2 : 1;
+  if (bdiag) cl = 1;  // neighbouring tiles read different B panels: no multicast
   CUtensorMap ma, mb;
   int rc;
   // A: K-major [M][K] (inner K) or M-major [K][M] (inner M)
   if (a_mn) rc = make_map(&ma, A, M, K, lda, BK, true);
   else rc = make_map(&ma, A, K, M, lda, BM, false);
   if (rc) return rc;
-  if (b_mn) rc = make_map(&mb, B, N, K, ldb, BK, true);
+  if (b_mn) rc = make_map(&mb, B, N, bdiag ? b_rows : K, ldb, BK, true);
   else rc = make_map(&mb, B, K, N, ldb, bn / cl, false);
   if (rc) return rc;
   CUtensorMap mbl = mb;
@@ -970,4 +984,28 @@ extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, i
     }
   }
   return AG_OK;
+}
+}  // namespace
+}  // namespace ag
+
+extern "C" int ag_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                              int32_t trans_a, const float *B, int64_t ldb, int32_t trans_b,
+                              const float *B_lo, float *C, int64_t ldc, float alpha, float beta,
+                              int32_t epilogue, const uint32_t *mask, int64_t ldm,
+                              uint32_t *mask_out, int64_t ldmo, void *stream) {
+  return gemm_tc(M, N, K, A, lda, trans_a, B, ldb, trans_b, B_lo, C, ldc, alpha, beta, epilogue,
+                 mask, ldm, mask_out, ldmo, 0, 0, stream);
+}
+
+extern "C" int ag_block_diag_gemm_tf32x3(int64_t num_rows, int64_t feat, int64_t panel,
+                                         const float *A, int64_t lda, const float *x,
+                                         int64_t ldx, int64_t x_rows, float *y, int64_t ldy,
+                                         float beta, void *stream) {
+  if (num_rows < 0 || feat < 0 || x_rows < 0) return fail(AG_ERR_VALUE, "negative sizes");
+  if (panel < 128 || panel % 128 != 0 || panel > 4096)
+    return fail(AG_ERR_VALUE, "panel must be a multiple of 128 in [128, 4096]");
+  if (lda < panel) return fail(AG_ERR_VALUE, "lda must be >= panel");
+  if (num_rows == 0 || feat == 0) return AG_OK;
+  return gemm_tc(num_rows, feat, panel, A, lda, 0, x, ldx, 0, nullptr, y, ldy, 1.0f, beta, 0,
+                 nullptr, 0, nullptr, 0, panel, x_rows, stream);
 }

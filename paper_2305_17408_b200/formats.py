@@ -68,7 +68,7 @@ class CsrMatrix:
     """Compressed sparse rows over destination vertices."""
 
     __slots__ = ("num_vertices", "row_ptr", "col_idx", "_val", "_ones", "_rows", "_touched",
-                 "_off_block", "_long", "_window", "_codes", "_dense16")
+                 "_off_block", "_long", "_window", "_codes", "_dense16", "_max_block_edges")
 
     def __init__(self, num_vertices: int, row_ptr: torch.Tensor, col_idx: torch.Tensor,
                  val: torch.Tensor | None, rows: torch.Tensor | None = None):
@@ -81,6 +81,7 @@ class CsrMatrix:
         self._window = None
         self._codes = {}
         self._dense16 = None
+        self._max_block_edges = None
 
     @property
     def val(self) -> torch.Tensor:
@@ -108,6 +109,16 @@ class CsrMatrix:
                       _lib.ptr(self.col_idx), SLAB_COVERAGE, _lib.byref(w), _lib.stream())
             self._window = int(w.value)
         return self._window
+
+    def max_block_edges(self) -> int:
+        """Most edges of any 16-row block (ag_slab_max_block_edges), cached: the
+        slab kernel stages each block's topology in shared memory when it fits."""
+        if self._max_block_edges is None:
+            m = _lib.out_i64()
+            _lib.call("ag_slab_max_block_edges", self.num_vertices, _lib.ptr(self.row_ptr),
+                      _lib.byref(m), _lib.stream())
+            self._max_block_edges = int(m.value)
+        return self._max_block_edges
 
     def touched(self) -> torch.Tensor:
         """bool[V]: row has >= 1 edge (kernels.py:121)."""
@@ -201,7 +212,7 @@ class DenseBlockSet:
     """
 
     __slots__ = ("num_vertices", "block_size", "community_ids", "blocks", "row_touched",
-                 "comm_slot")
+                 "comm_slot", "_panels")
 
     def __init__(self, num_vertices, block_size, community_ids, blocks, row_touched, comm_slot):
         self.num_vertices = int(num_vertices)
@@ -210,6 +221,29 @@ class DenseBlockSet:
         self.blocks = blocks
         self.row_touched = row_touched
         self.comm_slot = comm_slot
+        self._panels = None
+
+    @property
+    def panel(self) -> int:
+        """Panel width of the tensor-core layout: max(B, 128)."""
+        return max(self.block_size, 128)
+
+    def tc_ok(self) -> bool:
+        """B divides 128 or is a multiple of 128 (block-diagonal panels)."""
+        B = self.block_size
+        return (B <= 128 and 128 % B == 0) or B % 128 == 0
+
+    def panels(self) -> torch.Tensor:
+        """The blocks as block-diagonal [V, panel] panels (ag_dense_block_pack),
+        cached: the A operand of the tensor-core dense_block product."""
+        if self._panels is None:
+            P = self.panel
+            a = torch.empty((self.num_vertices, P), dtype=torch.float32, device=self.blocks.device)
+            _lib.call("ag_dense_block_pack", self.num_vertices, self.block_size, P,
+                      _lib.ptr(self.comm_slot), _lib.ptr(self.blocks), _lib.ptr(a), P,
+                      _lib.stream())
+            self._panels = a
+        return self._panels
 
     def nonzero_count(self) -> int:
         return int(torch.count_nonzero(self.blocks).item())

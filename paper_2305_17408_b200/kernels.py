@@ -150,7 +150,7 @@ def launch_fused(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp
               _lib.ptr(a.dense_blocks16() if dense_intra else None), a.num_edges, _lib.ptr(x), _lib.ptr(y),
               _opcode(op), flags | (_lib.AG_EPI_RELU_MASK if rb is not None else 0),
               _lib.ptr(other_touched), _lib.ptr(deg), float(gin_scale), _lib.ptr(rb),
-              _lib.ptr(relu_out), x.shape[0], a.window(), _lib.stream())
+              _lib.ptr(relu_out), x.shape[0], a.window(), a.max_block_edges(), _lib.stream())
 
 
 def _check_block_local(a: CsrMatrix, block_size: int) -> None:
@@ -190,6 +190,36 @@ def launch_dense_block(d: DenseBlockSet, x: torch.Tensor, y: torch.Tensor, op: A
               _lib.ptr(d.comm_slot), _lib.ptr(d.blocks), _lib.ptr(d.row_touched), _lib.ptr(x),
               _lib.ptr(y), _opcode(op), flags, _lib.ptr(other_touched), _lib.ptr(deg),
               float(gin_scale), _lib.stream())
+
+
+# dense_block on the tensor cores (tcgen05 3xTF32, fp32-faithful) from this
+# block size up; below it the fp32 SIMT kernel (B = 16 blocks are HBM-bound and
+# would need 8x the operand bytes as 128-wide panels).  SURVEY §2.2 K4.
+DENSE_TC_MIN_BLOCK = 64
+
+
+def dense_block_engine(d: DenseBlockSet, x: torch.Tensor, precision: str | None) -> str:
+    """"tc" (ag_block_diag_gemm_tf32x3) or "simt" (ag_dense_block_spmm)."""
+    if precision not in (None, "fp32", "tf32x3"):
+        raise ValueError(f"unknown dense_block precision {precision!r}")
+    tc_able = d.tc_ok() and _tc_ok(x) and x.shape[0] == d.num_vertices
+    if precision == "tf32x3":
+        if not tc_able:
+            raise KernelError("tensor-core dense_block needs B dividing 128 or a multiple of 128 "
+                              "and 16-byte aligned features with a row stride multiple of 4")
+        return "tc"
+    if precision is None and tc_able and d.block_size >= DENSE_TC_MIN_BLOCK:
+        return "tc"
+    return "simt"
+
+
+def launch_dense_block_tc(d: DenseBlockSet, x: torch.Tensor, y: torch.Tensor,
+                          beta: float = 0.0) -> None:
+    """y = blockdiag(blocks) @ x (+ beta * y) on the tensor cores."""
+    A = d.panels()
+    _lib.call("ag_block_diag_gemm_tf32x3", d.num_vertices, x.shape[1], d.panel, _lib.ptr(A),
+              A.stride(0), _lib.ptr(x), x.stride(0), x.shape[0], _lib.ptr(y), y.stride(0),
+              float(beta), _lib.stream())
 
 
 def _coo_touched(a: CooMatrix) -> torch.Tensor:
@@ -250,13 +280,21 @@ def aggregate_coo_atomic(a: CooMatrix, x, op: AggregateOp) -> PartialResult:
     return PartialResult(values=y, touched=touched, op=op, note=note)
 
 
-def aggregate_dense_block(d: DenseBlockSet, x, op: AggregateOp) -> PartialResult:
-    """Batched dense products over diagonal blocks, kernels.py:228-250 (no max)."""
+def aggregate_dense_block(d: DenseBlockSet, x, op: AggregateOp,
+                          precision: str | None = None) -> PartialResult:
+    """Batched dense products over diagonal blocks, kernels.py:228-250 (no max).
+
+    precision None picks the tensor cores (3xTF32) for B >= DENSE_TC_MIN_BLOCK
+    and the fp32 SIMT kernel below; "fp32" / "tf32x3" force one.  The
+    reference's BLAS matmul leaves the order unpinned (tolerance 1e-5)."""
     if op is AggregateOp.MAX:
         raise KernelError("dense_block kernel does not support max aggregation")
     x = _check_features(d.num_vertices, x)
     y = torch.empty((d.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
-    launch_dense_block(d, x, y, op)
+    if dense_block_engine(d, x, precision) == "tc":
+        launch_dense_block_tc(d, x, y)
+    else:
+        launch_dense_block(d, x, y, op)
     return PartialResult(values=y, touched=_block_touched(d), op=op)
 
 
@@ -436,7 +474,12 @@ class SubgraphExec:
                 raise KernelError("dense_block kernel requires an intra subgraph")
             if op is AggregateOp.MAX:
                 raise KernelError("dense_block kernel does not support max aggregation")
-            launch_dense_block(self.blocks, x, y, op, flags, other_touched, deg, g)
+            if (op is AggregateOp.SUM and gin_scale is None
+                    and dense_block_engine(self.blocks, x, None) == "tc"):
+                # combine(sum): the inter partial already in y (0 where untouched)
+                launch_dense_block_tc(self.blocks, x, y, beta=1.0)
+            else:
+                launch_dense_block(self.blocks, x, y, op, flags, other_touched, deg, g)
         else:
             mine = self.run(kind, x, op, tile_budget_bytes)
             other = PartialResult(values=y, touched=other_touched, op=op)

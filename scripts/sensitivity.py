@@ -1,0 +1,109 @@
+"""Sensitivity of the aggregation kernel to the graph: the
+C5 F=256 (and F=100) aggregation on generator variants -- inter-edge window 16
+(the bench graph), 32 and 64 blocks, 20% global edges, skew 2 (hub rows) --
+and the C3 graph reordered by cluster_bfs instead of the planted partition.
+Every fused pair is timed; the best is reported with its algorithmic GB/s and
+fraction of the measured HBM peak.
+
+    python scripts/sensitivity.py > gpurun_out/sensitivity.json
+"""
+import json
+import pathlib
+import sys
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2305_17408_b200 as ag  # noqa: E402
+from paper_2305_17408_b200 import kernels as K  # noqa: E402
+from paper_2305_17408_b200 import synth  # noqa: E402
+from paper_2305_17408_b200.decompose import full_graph  # noqa: E402
+
+PAIRS = [(ag.KernelKind.CSR_INTRA_BLOCKED, ag.KernelKind.CSR_INTER),
+         (ag.KernelKind.DENSE_BLOCK, ag.KernelKind.CSR_INTER),
+         (ag.KernelKind.CSR_INTRA_BLOCKED, ag.KernelKind.COO_ATOMIC),
+         (ag.KernelKind.DENSE_BLOCK, ag.KernelKind.COO_ATOMIC)]
+
+
+def timeit(fn, reps=5):
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        e.synchronize()
+        ts.append(s.elapsed_time(e))
+    return sorted(ts)[reps // 2]
+
+
+def measure(name, dec, rg, feats, peak, extra):
+    V = dec.num_vertices
+    csr = K.to_csr(full_graph(dec))
+    lens = (csr.row_ptr[1:] - csr.row_ptr[:-1]).float()
+    row = {"variant": name, **extra, "edges": rg.num_edges,
+           "intra_fraction": round(dec.intra.num_edges / rg.num_edges, 4),
+           "deg_max": int(lens.max().item()), "rows_over_64": int((lens > 64).sum().item()),
+           "window": csr.window(), "max_block_edges": csr.max_block_edges()}
+    for F in feats:
+        x = torch.randn((V, F), device="cuda")
+        y = torch.empty_like(x)
+        ba = bench.bytes_alg(V, rg.num_edges, F, rg.weights is not None)
+        best = None
+        for ki, ke in PAIRS:
+            t = timeit(lambda: K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM, kernel_intra=ki,
+                                                kernel_inter=ke))
+            if best is None or t < best[0]:
+                best = (t, f"{ki.value}+{ke.value}")
+        gbs = ba / best[0] / 1e6
+        row[f"F{F}"] = {"ms": round(best[0], 4), "pair": best[1], "alg_GBps": round(gbs, 1),
+                        "frac": round(gbs / peak, 4)}
+        del x, y
+    print(json.dumps(row), file=sys.stderr, flush=True)
+    return row
+
+
+def main():
+    peak, _ = bench.peaks()
+    cfg = bench.CONFIGS["C5"]
+    out = {"peak_GBps": peak, "rows": []}
+    variants = [("bench (window 16, 5% global)", {}),
+                ("window 32", {"window": 32}),
+                ("window 64", {"window": 64}),
+                ("20% global edges", {"p_global": 0.2}),
+                ("skew 2 (hub rows)", {"skew": 2})]
+    for name, over in variants:
+        gen = dict(bench.GEN)
+        gen.update(over)
+        t0 = time.perf_counter()
+        g, comm = synth.community_graph(cfg["V"], cfg["E"], **gen)
+        g = ag.gcn_normalize(g)
+        rg = ag.apply_reorder(g, ag.reorder.partition_from_ids(comm, 16))
+        dec = ag.decompose(rg, 16)
+        torch.cuda.synchronize()
+        out["rows"].append(measure(name, dec, rg, (256, 100), peak,
+                                   {"generator": gen, "prep_s": round(time.perf_counter() - t0, 1)}))
+        del g, rg, dec
+        torch.cuda.empty_cache()
+    # C3 with the reference's own reorder (cluster_bfs) vs the planted partition
+    c3 = bench.CONFIGS["C3"]
+    g, comm = synth.community_graph(c3["V"], c3["E"], **bench.GEN)
+    for name, part in (("C3 planted partition", lambda: ag.reorder.partition_from_ids(comm, 16)),
+                       ("C3 cluster_bfs", lambda: ag.cluster_bfs(g, 16))):
+        t0 = time.perf_counter()
+        p = part()
+        reorder_s = time.perf_counter() - t0
+        rg = ag.apply_reorder(g, p)
+        dec = ag.decompose(rg, 16)
+        out["rows"].append(measure(name, dec, rg, (128, 64), peak, {"reorder_s": round(reorder_s, 2)}))
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
