@@ -247,11 +247,6 @@ int ag_role_csr_build(int64_t num_rows, const int32_t *row_ptr,
  * round-robin, reducing out of shared memory.  `window` only affects speed,
  * never values (ag_slab_window picks it per graph).  Any F (TMA when
  * F % 4 == 0 and x is 16-byte aligned, cp.async otherwise).
- * max_block_edges (0: unknown): the most edges any 16-row block holds
- * (ag_slab_max_block_edges); when every block's pairs fit a shared-memory
- * topology slot, the far producer bulk-copies each block's rowinfo and pairs
- * ahead of the consumers ("staged topology") instead of the consumers
- * loading their rows' topology from global memory.
  * blk_w (NULL: bitwise intra role): the pair (dense_block, csr_inter) of the
  * reference's selector in one pass -- the intra role of every 16-row block as
  * a dense 16 x 16 block product (ag_slab_dense_blocks; the reference's
@@ -266,8 +261,7 @@ int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                   const float *x, float *y,
                   int32_t op, int32_t epi_flags, const uint8_t *other_touched,
                   const int64_t *deg, float gin_scale, const uint32_t *relu_bits,
-                  uint32_t *relu_out, int64_t x_rows, int32_t window,
-                  int64_t max_block_edges, void *stream);
+                  uint32_t *relu_out, int64_t x_rows, int32_t window, void *stream);
 
 /* Window radius (in 16-row blocks) for ag_fused_spmm over this CSR: the
  * smallest radius whose ring covers `coverage` (e.g. 0.995) of the edges the
@@ -301,10 +295,6 @@ int ag_slab_codes(int64_t num_rows, const int32_t *row_ptr,
 int ag_slab_dense_blocks(int64_t num_rows, const int32_t *row_ptr,
                          const int32_t *role_mid, const int32_t *role_col,
                          const float *role_val, float *blk_w, void *stream);
-/* The most edges any 16-row block [16b, 16b + 16) of a CSR holds (synchronous;
- * call once per topology and cache): ag_fused_spmm's max_block_edges. */
-int ag_slab_max_block_edges(int64_t num_rows, const int32_t *row_ptr,
-                            int64_t *max_edges, void *stream);
 /* Staged far sources per 16-row block (the far-ring capacity). */
 int ag_slab_far_capacity(void);
 

@@ -55,9 +55,8 @@ SIGNATURES: dict[str, list] = {
     "ag_dense_block_spmm": [I64, I64, I64, P, P, P, P, P, I32, I32, P, P, F32, P],
     "ag_role_csr_build": [I64, P, P, P, I64, P, P, P, P],
     "ag_fused_spmm": [I64, I64, I32, P, P, P, P, P, P, I32, P, I64, P, P, I32, I32, P, P, F32,
-                      P, P, I64, I32, I64, P],
+                      P, P, I64, I32, P],
     "ag_relu_bits": [I64, I64, P, I64, P, I64, P],
-    "ag_slab_max_block_edges": [I64, P, P, P],
     "ag_dense_block_pack": [I64, I64, I64, P, P, P, I64, P],
     "ag_block_diag_gemm_tf32x3": [I64, I64, I64, P, I64, P, I64, I64, P, I64, F32, P],
     "ag_slab_window": [I64, P, P, F64, P, P],

@@ -31,10 +31,15 @@ inline int cuda_status(cudaError_t e, const char *where) {
   return fail(AG_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 
+// A failed runtime call also records itself as the thread's last error;
+// clear it (non-sticky errors) so the next launch check does not report it.
 #define AG_CUDA(expr)                                        \
   do {                                                       \
     cudaError_t _e = (expr);                                 \
-    if (_e != cudaSuccess) return ag::cuda_status(_e, #expr); \
+    if (_e != cudaSuccess) {                                 \
+      (void)cudaGetLastError();                              \
+      return ag::cuda_status(_e, #expr);                     \
+    }                                                        \
   } while (0)
 
 // Every kernel launch of the library goes through this check, which also

@@ -69,13 +69,7 @@ constexpr int kConsMax = 16;
 template <int MODE>
 constexpr int cons_warps();
 constexpr int kWin = 64;     // topology items per window refill (two per lane)
-constexpr int kSlots = 41;   // X ring capacity in blocks (window H <= (kSlots - 9) / 2 = 16)
-// staged topology (GArgs::topo): each block's rowinfo (16 x int4) and its
-// (code, weight) pairs are bulk-copied into a kTopoSlots-deep topology ring by
-// the far producer, so consumers read their rows' topology from shared memory
-constexpr int kTopoSlots = 3;
-constexpr uint32_t kTopoBytes = 5632;                  // 256 B rowinfo + pairs
-constexpr int kTopoPairs = (kTopoBytes - 256) / 8;    // 672 pairs per block
+constexpr int kSlots = 45;   // X ring capacity in blocks (window H <= (kSlots - 9) / 2 = 18)
 constexpr int kFarSlots = 4; // far ring: staged out-of-window sources of the next blocks
 constexpr int kFarMax = 20;  // staged far sources per block (more: read from global)
 constexpr int kRG = 1;       // consecutive rows a consumer warp takes at a time (divides kRB)
@@ -114,7 +108,6 @@ struct GArgs {
   int64_t x_rows;           // rows of x (>= rows: a rank's halo rows follow its own)
   int64_t xblocks;          // ceil(x_rows / 16)
   int tma;                  // 1: TMA tensor loads; 0: cp.async element copies
-  int topo;                 // 1: staged topology (every block's pairs fit kTopoPairs; needs tma)
   int sleep;                // producers' done waits: 1 suspend between polls, 0 spin
   uint32_t csleep;          // consumer / dense-warp waits: suspend hint (ns) per poll, 0 spin
   long long *trace;         // AG_SLAB_TRACE: per-block globaltimer stamps of CTA 0 (development)
@@ -281,7 +274,6 @@ struct RowWarp {
   uint64_t one;        // {1.0f, 1.0f} loaded at run time (see add2)
   int32_t p, end;      // window holds items [p, p + kWin)
   uint64_t far;        // bit i: window item p + i is a far (global) source
-  bool staged;         // the window is the block's staged topology (never refilled)
   __device__ __forceinline__ void fill(int32_t at) {
     __syncwarp();
     p = at;
@@ -315,7 +307,7 @@ struct RowWarp {
     __syncwarp();
   }
   __device__ __forceinline__ void ensure(int32_t lo, int n) {
-    if (!staged && lo + n > p + kWin) fill(lo);
+    if (lo + n > p + kWin) fill(lo);
   }
   // NEAR: the caller checked `far` -- the item is in the ring
   template <bool RAW, bool NEAR = false>
@@ -472,10 +464,7 @@ struct RowWarp {
   // the all-in-ring path (shared loads only) or the mixed one
   template <int N, bool RAW>
   __device__ __forceinline__ void items(int32_t e, Lv<VEC> (&c)[N]) const {
-    // staged topology: far is all-zero (fast rows) or all-ones (rows with
-    // global sources: every item checks its code); rows may exceed 64 items
-    const uint32_t fb = staged ? static_cast<uint32_t>(far & 1u)
-                               : static_cast<uint32_t>(far >> (e - p)) & ((1u << N) - 1u);
+    const uint32_t fb = static_cast<uint32_t>(far >> (e - p)) & ((1u << N) - 1u);
     if (fb == 0) {
 #pragma unroll
       for (int j = 0; j < N; ++j) c[j] = item<RAW, true>(e + j);
@@ -575,7 +564,7 @@ struct RowWarp {
 // warp state travels by value so the hot path keeps it in registers.
 template <int VEC, bool W>
 __device__ __noinline__ Lv<VEC> pairwise_long_fn(RowWarp<VEC, W> w, int32_t e0, int n) {
-  if (!w.staged) w.fill(e0);
+  w.fill(e0);
   return w.pairwise_long(e0, n);
 }
 
@@ -672,7 +661,7 @@ __device__ __forceinline__ uint32_t spread16(uint32_t x) {
 template <int VEC, int MODE, bool W>
 __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64_t r, int32_t s,
                                        int32_t e, int32_t m, float *yrow, bool act, bool fast,
-                                       int64_t fcol, uint32_t intra_s,
+                                       int64_t fcol, uint32_t intra_s, uint32_t rword,
                                        uint32_t iv_bar = 0, uint32_t iv_phase = 0,
                                        bool *iv_pending = nullptr) {
   constexpr bool IS_MAX = MODE == kModeMax;
@@ -682,11 +671,9 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
   // dense-intra mode: the intra role comes from the dense warp's block product
   const int32_t ni = DENSE ? 0 : (SUM3 || (a.mask & 1)) ? m - s : 0;
   const int32_t no = (SUM3 || (a.mask & 2)) ? e - m : 0;
-  // the ReLU-mask word is loaded before the reduction so its latency hides
-  // behind it
+  // the row's ReLU-mask word was loaded a row ahead (the consumer pipeline)
   const bool relu = a.relu && act;
-  const uint32_t rbits = relu ? (__ldg(a.ep.relu_bits + r * a.ldw + (fcol >> 5)) >> (fcol & 31))
-                              : 0u;
+  const uint32_t rbits = relu ? rword >> (fcol & 31) : 0u;
   Vf<VEC> I, O;
   if (a.dbg & 1) {
     I = splat<VEC>(0.0f);
@@ -768,8 +755,7 @@ struct SlabGeom {
   static constexpr uint32_t kFarSlotBytes = kFarMax * kRowBytes;
   static constexpr uint32_t kIOff = kSlots * kSlotBytes + kFarSlots * kFarSlotBytes;
   static constexpr uint32_t kWOff = kIOff + kISlots * kSlotBytes;  // 2 warps x 2 x 512 B weights
-  static constexpr uint32_t kTopoOff = kWOff + 2 * 1024;
-  static constexpr uint32_t kRingBytes = kTopoOff + kTopoSlots * kTopoBytes;
+  static constexpr uint32_t kRingBytes = kWOff + 2 * 1024;
   static constexpr uint32_t kBarBytes = (kReady + kDone + kISlots) * 8;
   static constexpr uint32_t kWinBytes = kConsMax * kWin * 8;
   static constexpr size_t kSmem = kRingBytes + kBarBytes + kWinBytes;
@@ -950,11 +936,6 @@ __device__ __forceinline__ void produce_far(const GArgs &a, uint32_t ring, const
     return (f < kb1 && lane < kFarMax) ? a.far_src[static_cast<int64_t>(f) * kFarMax + lane] : 0;
   };
   auto far_counts = [&](uint32_t f) -> int32_t { return f + lane < kb1 ? a.far_cnt[f + lane] : 0; };
-  // staged topology: per-lane edge bounds of 32 consecutive blocks, one batch ahead
-  auto blk_lo = [&](uint32_t f) -> int32_t {
-    return f + lane < kb1 ? a.row_ptr[static_cast<int64_t>(f + lane) * kRB] : 0;
-  };
-  int32_t tlo = a.topo ? blk_lo(kb0) : 0, tlo_next = a.topo ? blk_lo(kb0 + 32) : 0;
   int32_t fsa[D];
 #pragma unroll
   for (int u = 0; u < D; ++u) fsa[u] = far_list(kb0 + u);
@@ -967,47 +948,22 @@ __device__ __forceinline__ void produce_far(const GArgs &a, uint32_t ring, const
       if (f >= kb1) break;
       const uint32_t fi = f - kb0;
       const int cnt = __shfl_sync(0xffffffffu, fc, fi & 31);
-      // block f's edge range [e_lo, e_hi) (the next block's start, or the end)
-      int32_t e_lo = 0, e_hi = 0;
-      if (a.topo) {
-        e_lo = __shfl_sync(0xffffffffu, tlo, fi & 31);
-        const int32_t nx = __shfl_sync(0xffffffffu, (fi & 31) == 31 ? tlo_next : tlo, (fi + 1) & 31);
-        e_hi = f + 1 < kb1 ? nx : a.row_ptr[std::min<int64_t>(int64_t(f + 1) * kRB, a.rows)];
-      }
       const int32_t src = fsa[u];
       fsa[u] = far_list(f + D);
       if ((fi & 31) == 31) {
         fc = fc_next;
         fc_next = far_counts(f + 33);
-        if (a.topo) {
-          tlo = tlo_next;
-          tlo_next = blk_lo(f + 33);
-        }
       }
       const uint32_t slot_base = far_ring + fslot * G::kFarSlotBytes;
       if (++fslot == kFarSlots) fslot = 0;
-      // far slot reuse: done[f - kFarSlots]; topology slot reuse: done[f - kTopoSlots]
-      const int64_t need = int64_t(f) - (a.topo ? kTopoSlots : kFarSlots);
+      // far slot reuse: done[f - kFarSlots]
+      const int64_t need = int64_t(f) - kFarSlots;
       if (a.tma) {
         if (lane == 0) {
           tstamp(a, fi, 0);
           if (need >= int64_t(kb0)) bs.wait_done(static_cast<uint32_t>(need));
           tstamp(a, fi, 1);
-          uint32_t tb = 0, ri_bytes = 0, cv_bytes = 0;
-          int32_t ea = 0;
-          if (a.topo) {
-            const int64_t r0 = static_cast<int64_t>(f) * kRB;
-            ri_bytes = static_cast<uint32_t>(std::min<int64_t>(kRB, a.rows - r0)) * 16u;
-            ea = e_lo & ~1;  // 16-byte aligned pair range covering [e_lo, e_hi)
-            cv_bytes = static_cast<uint32_t>(((e_hi + 1) & ~1) - ea) * 8u;
-            tb = ri_bytes + cv_bytes;
-          }
-          mbar_expect_tx(bs.rdy(f), (a.dbg & 2) ? tb : static_cast<uint32_t>(cnt) * tile_bytes + tb);
-          if (a.topo) {
-            const uint32_t ts = ring + G::kTopoOff + (fi % kTopoSlots) * kTopoBytes;
-            bulk_g2s(ts, a.rowinfo + static_cast<int64_t>(f) * kRB, ri_bytes, bs.rdy(f));
-            if (cv_bytes) bulk_g2s(ts + 256, a.cv + ea, cv_bytes, bs.rdy(f));
-          }
+          mbar_expect_tx(bs.rdy(f), (a.dbg & 2) ? 0u : static_cast<uint32_t>(cnt) * tile_bytes);
         }
         __syncwarp();
         if (lane < cnt && !(a.dbg & 2))
@@ -1186,7 +1142,6 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
         w.p = 0;
         w.end = 0;
         w.far = 0;
-        w.staged = a.topo != 0;
         float *const ylane = a.y + (act ? fcol : 0);
         const uint32_t ld = static_cast<uint32_t>(a.feat);
         const uint32_t r0 = kb0 * kRB;
@@ -1196,8 +1151,7 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
         // the current row's reduction and only moved after it, so each load
         // has a full row of work to land.
         const int4 zero4 = make_int4(0, 0, 0, 0);
-        // (staged topology: rows read their rowinfo / pairs from the block's slot instead)
-        const bool notopo = (a.dbg & 32) != 0 || a.topo;
+        const bool notopo = (a.dbg & 32) != 0;  // experiment: rows without topology loads
         auto info_at = [&](uint32_t rr) -> int4 {
           return (rr < r1 && !notopo) ? __ldg(a.rowinfo + rr) : zero4;
         };
@@ -1210,8 +1164,16 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
         auto next_row = [&](uint32_t r) -> uint32_t {
           return (r % kRG != kRG - 1) ? r + 1 : r + (NC - 1) * kRG + 1;
         };
+        // ReLU-backward mask words, one row ahead like the topology
+        const bool relu_rows = a.relu && act;
+        auto rword_at = [&](uint32_t rrow) -> uint32_t {
+          return (relu_rows && rrow < r1) ? __ldg(a.ep.relu_bits + static_cast<int64_t>(rrow) * a.ldw +
+                                                  (fcol >> 5))
+                                          : 0u;
+        };
         uint32_t rr = r0 + warp * kRG;
         int4 info = info_at(rr);
+        uint32_t rw = rword_at(rr);
         int2 q0 = pairs_at(info, 0), q1 = pairs_at(info, 1);
         uint32_t rn = next_row(rr);
         int4 info1 = info_at(rn);
@@ -1230,8 +1192,6 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
             mbar_wait_hint(ivalid + ((k - kb0) % kISlots) * 8, ((k - kb0) / kISlots) & 1u, a.csleep);
         };
         bool entered = false;
-        uint32_t tslot = 0;  // staged topology: the current block's slot
-        int32_t tea = 0;     // ... and the (even) edge index of its first pair
 #pragma unroll 1
         for (; rr < r1; rr = rn, rn = next_row(rn)) {
           const uint32_t k = rr / kRB;
@@ -1245,52 +1205,33 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
               }
             enter(k);
             entered = true;
-            if (a.topo) {  // the block's topology slot and its pairs' base edge
-              tslot = ring + G::kTopoOff + ((k - kb0) % kTopoSlots) * kTopoBytes;
-              int32_t s0;
-              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(s0) : "r"(tslot) : "memory");
-              tea = s0 & ~1;
-            }
-          }
-          if (a.topo) {
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(info.x), "=r"(info.y), "=r"(info.z), "=r"(info.w)
-                         : "r"(tslot + (rr % kRB) * 16u)
-                         : "memory");
           }
           const int32_t s = info.x, e = info.z;
           const int32_t m =
               (mode_sum3(MODE) || a.has_mid) ? info.y : (a.mask == 1 ? e : s);
           const bool fast = !(info.w & kRowSlow);
           w.end = e;
-          if (a.topo) {
-            // the row's pairs are in the slot: the window is the slot itself;
-            // rows with global sources check every item (far = all ones)
-            w.win = tslot + 256u + static_cast<uint32_t>(s - tea) * 8u;
-            w.p = s;
-            w.far = fast ? 0ull : ~0ull;
-          } else if (fast) {
-            w.template install<true>(s, q0, q1);
-          } else {
-            w.template install<false>(s, q0, q1);
-          }
-          // next row's pairs and the row after next's bounds
+          if (fast) w.template install<true>(s, q0, q1);
+          else w.template install<false>(s, q0, q1);
+          // next row's pairs and mask word, the row after next's bounds
           const int2 n0 = pairs_at(info1, 0), n1 = pairs_at(info1, 1);
+          const uint32_t rw1 = rword_at(rn);
           const int4 info2 = info_at(next_row(rn));
           float *yrow;  // ylane + rr * ld as one IMAD.WIDE.U32
           asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(yrow) : "r"(rr), "r"(ld * 4u), "l"(ylane));
           const uint32_t intra_s = ring + G::kIOff + ((k - kb0) % kISlots) * G::kSlotBytes +
                                    (rr % kRB) * G::kRowBytes + lane * VEC * 4;
           if constexpr (MODE == kModeDense3Coo)
-            do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, fcol, intra_s,
+            do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, fcol, intra_s, rw,
                                  ivalid + ((k - kb0) % kISlots) * 8, ((k - kb0) / kISlots) & 1u,
                                  &iv_pending);
           else
-            do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, fcol, intra_s);
+            do_row<VEC, MODE, W>(a, w, rr, s, e, m, yrow, act, fast, fcol, intra_s, rw);
           info = info1;
           info1 = info2;
           q0 = n0;
           q1 = n1;
+          rw = rw1;
         }
         __syncwarp();
         for (; kcur < kb1; ++kcur)  // leave the rest of the range
@@ -1361,6 +1302,16 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
   a.xblocks = (a.x_rows + kRB - 1) / kRB;
   a.ntiles = static_cast<int>((a.feat + G::T - 1) / G::T);
   const size_t smem = G::kSmem;
+  {
+    cudaFuncAttributes fa;
+    AG_CUDA(cudaFuncGetAttributes(&fa, k));
+    int dev = 0, optin = 0;
+    AG_CUDA(cudaGetDevice(&dev));
+    AG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (smem + fa.sharedSizeBytes > static_cast<size_t>(optin))
+      return fail(AG_ERR_CUDA, "slab kernel needs %zu + %zu B of shared memory, the device allows %d",
+                  smem, static_cast<size_t>(fa.sharedSizeBytes), optin);
+  }
   AG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   const int sms = sm_count();
@@ -1391,7 +1342,6 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
   };
   if (a.feat % 4 == 0 && env_int("AG_SLAB_NO_TMA", 0) == 0 && encode(&map, a.x, a.x_rows))
     a.tma = 1;
-  if (!a.tma) a.topo = 0;  // the staged topology rides on the bulk-copy path
   const int threads = (mode == kModeDense3Coo ? kConsMax : 14) * 32 + 64;
   long long *trace = nullptr;
   if (std::getenv("AG_SLAB_TRACE")) {
@@ -1515,42 +1465,6 @@ using namespace ag;
 
 extern "C" int ag_slab_far_capacity(void) { return kFarMax; }
 
-namespace ag {
-namespace {
-__global__ void max_block_edges_kernel(int64_t rows, const int32_t *row_ptr,
-                                       unsigned long long *out) {
-  const int64_t nb = (rows + kRB - 1) / kRB;
-  unsigned long long m = 0;
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb;
-       b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = row_ptr[std::min<int64_t>(b * kRB + kRB, rows)] - row_ptr[b * kRB];
-    m = e > static_cast<int64_t>(m) ? static_cast<unsigned long long>(e) : m;
-  }
-  atomicMax(out, m);
-}
-}  // namespace
-}  // namespace ag
-
-extern "C" int ag_slab_max_block_edges(int64_t num_rows, const int32_t *row_ptr,
-                                       int64_t *max_edges, void *stream) {
-  if (num_rows < 0 || max_edges == nullptr) return fail(AG_ERR_VALUE, "bad arguments");
-  *max_edges = 0;
-  if (num_rows == 0) return AG_OK;
-  cudaStream_t st = as_stream(stream);
-  Scratch m;
-  AG_CUDA(m.alloc(sizeof(unsigned long long), st));
-  AG_CUDA(cudaMemsetAsync(m.ptr, 0, sizeof(unsigned long long), st));
-  const int64_t nb = (num_rows + kRB - 1) / kRB;
-  max_block_edges_kernel<<<grid_for(nb, 256), 256, 0, st>>>(num_rows, row_ptr,
-                                                            m.as<unsigned long long>());
-  AG_LAUNCH_CHECK("max_block_edges_kernel");
-  unsigned long long h = 0;
-  AG_CUDA(cudaMemcpyAsync(&h, m.ptr, sizeof(h), cudaMemcpyDeviceToHost, st));
-  AG_CUDA(cudaStreamSynchronize(st));
-  *max_edges = static_cast<int64_t>(h);
-  return AG_OK;
-}
-
 extern "C" int ag_slab_dense_blocks(int64_t num_rows, const int32_t *row_ptr,
                                     const int32_t *role_mid, const int32_t *role_col,
                                     const float *role_val, float *blk_w, void *stream) {
@@ -1635,7 +1549,7 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                              const float *x, float *y, int32_t op, int32_t epi_flags,
                              const uint8_t *other_touched, const int64_t *deg, float gin_scale,
                              const uint32_t *relu_bits, uint32_t *relu_out, int64_t x_rows,
-                             int32_t window, int64_t max_block_edges, void *stream) {
+                             int32_t window, void *stream) {
   if (num_rows < 0 || feat < 0 || num_edges < 0) return fail(AG_ERR_VALUE, "negative sizes");
   if (op < AG_OP_SUM || op > AG_OP_MAX) return fail(AG_ERR_KERNEL, "unknown op %d", op);
   if (role_mask < 1 || role_mask > 3) return fail(AG_ERR_VALUE, "role_mask must be 1, 2 or 3");
@@ -1696,11 +1610,6 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                    : (role_mask == 3 && op == AG_OP_SUM && (epi_flags & ~kSum3Flags) == 0)
                        ? kModeSum3
                        : kModeAny;
-  // staged topology when every 16-row block's pairs (+ the alignment pair on
-  // each side) fit a topology slot; the launcher also needs TMA (bulk copies)
-  a.topo = (max_block_edges > 0 && max_block_edges + 2 <= kTopoPairs &&
-            (reinterpret_cast<uintptr_t>(cv) & 15) == 0 &&
-            env_int("AG_SLAB_NO_TOPO", 0) == 0) ? 1 : 0;
   if (v2) return launch_slab<2>(a, mode, window, st);
   return launch_slab<1>(a, mode, window, st);
 }

@@ -295,7 +295,7 @@ class DistGNN:
                   int(op.val is not None), None,
                   op.num_edges, _lib.ptr(x_ext), _lib.ptr(out), _lib.AG_OP["sum"], flags, None,
                   _lib.ptr(op.deg), 0.0 if gs is None else gs, _lib.ptr(rbits), None,
-                  x_ext.shape[0], op.window(), 0, _lib.stream())
+                  x_ext.shape[0], op.window(), _lib.stream())
         if e0 is not None:
             e1.record()
             self.events.append((e0, e1, F, op))

@@ -68,7 +68,7 @@ class CsrMatrix:
     """Compressed sparse rows over destination vertices."""
 
     __slots__ = ("num_vertices", "row_ptr", "col_idx", "_val", "_ones", "_rows", "_touched",
-                 "_off_block", "_long", "_window", "_codes", "_dense16", "_max_block_edges")
+                 "_off_block", "_long", "_window", "_codes", "_dense16")
 
     def __init__(self, num_vertices: int, row_ptr: torch.Tensor, col_idx: torch.Tensor,
                  val: torch.Tensor | None, rows: torch.Tensor | None = None):
@@ -81,7 +81,6 @@ class CsrMatrix:
         self._window = None
         self._codes = {}
         self._dense16 = None
-        self._max_block_edges = None
 
     @property
     def val(self) -> torch.Tensor:
@@ -109,16 +108,6 @@ class CsrMatrix:
                       _lib.ptr(self.col_idx), SLAB_COVERAGE, _lib.byref(w), _lib.stream())
             self._window = int(w.value)
         return self._window
-
-    def max_block_edges(self) -> int:
-        """Most edges of any 16-row block (ag_slab_max_block_edges), cached: the
-        slab kernel stages each block's topology in shared memory when it fits."""
-        if self._max_block_edges is None:
-            m = _lib.out_i64()
-            _lib.call("ag_slab_max_block_edges", self.num_vertices, _lib.ptr(self.row_ptr),
-                      _lib.byref(m), _lib.stream())
-            self._max_block_edges = int(m.value)
-        return self._max_block_edges
 
     def touched(self) -> torch.Tensor:
         """bool[V]: row has >= 1 edge (kernels.py:121)."""

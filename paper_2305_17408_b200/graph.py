@@ -28,6 +28,8 @@ def as_device(a, dtype: torch.dtype) -> torch.Tensor:
         return a.to(device=dev, dtype=dtype).contiguous()
     np_dtype = {torch.int64: np.int64, torch.int32: np.int32, torch.float32: np.float32}[dtype]
     arr = np.ascontiguousarray(np.asarray(a, dtype=np_dtype))
+    if not arr.flags.writeable:  # read-only host input (the reference's arrays are)
+        return torch.tensor(arr, device=dev)
     return torch.from_numpy(arr).to(dev)
 
 

@@ -150,7 +150,7 @@ def launch_fused(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp
               _lib.ptr(a.dense_blocks16() if dense_intra else None), a.num_edges, _lib.ptr(x), _lib.ptr(y),
               _opcode(op), flags | (_lib.AG_EPI_RELU_MASK if rb is not None else 0),
               _lib.ptr(other_touched), _lib.ptr(deg), float(gin_scale), _lib.ptr(rb),
-              _lib.ptr(relu_out), x.shape[0], a.window(), a.max_block_edges(), _lib.stream())
+              _lib.ptr(relu_out), x.shape[0], a.window(), _lib.stream())
 
 
 def _check_block_local(a: CsrMatrix, block_size: int) -> None:

@@ -50,7 +50,7 @@ def measure(name, dec, rg, feats, peak, extra):
     row = {"variant": name, **extra, "edges": rg.num_edges,
            "intra_fraction": round(dec.intra.num_edges / rg.num_edges, 4),
            "deg_max": int(lens.max().item()), "rows_over_64": int((lens > 64).sum().item()),
-           "window": csr.window(), "max_block_edges": csr.max_block_edges()}
+           "window": csr.window()}
     for F in feats:
         x = torch.randn((V, F), device="cuda")
         y = torch.empty_like(x)

@@ -51,7 +51,11 @@ def main():
     V, E = cfg["V"], rg.num_edges
     knobs = [(k.split("=")[0], k.split("=")[1].split(",")) for k in args.knob] or [("", [""])]
     pairs = PAIRS if args.pairs == "all" else [tuple(p.split("+")) for p in args.pairs.split(";")]
-    out = {"V": V, "E": E, "results": []}
+    from paper_2305_17408_b200.decompose import full_graph
+    csr = K.to_csr(full_graph(dec))
+    tcsr = K.to_csr(full_graph(net.subject_t))
+    out = {"V": V, "E": E, "window": csr.window(), "window_T": tcsr.window(), "results": []}
+    print(json.dumps({k: v for k, v in out.items() if k != "results"}), flush=True)
     for F in args.feat:
         x = torch.randn((V, F), device="cuda")
         y = torch.empty_like(x)

@@ -240,36 +240,3 @@ def test_coo_inter_needs_sum():
                                             kernel_inter=ag.KernelKind.COO_ATOMIC))
         from conftest import rel_error
         assert rel_error(got, _oracle_pair(rg, 16, to_np(x), op.value)) < 1e-4
-
-
-@pytest.mark.parametrize("F", [33, 64, 256])
-def test_staged_topology_equals_register_pipeline(F, monkeypatch):
-    """The staged-topology consumers (each block's rowinfo and pairs bulk-copied
-    into a shared-memory slot by the far producer) compute exactly what the
-    register-pipelined consumers do (AG_SLAB_NO_TOPO=1): every op, every fused
-    pair, with the GIN and ReLU-mask epilogues, rows past 64 pairs included."""
-    rg, dec = _community(5000, 120000, window=8, p_global=0.1)
-    csr = K.to_csr(full_graph(dec))
-    assert csr.max_block_edges() + 2 <= 672  # the staged path is the one that runs
-    x = torch.from_numpy(np.random.default_rng(F).standard_normal((5000, F)).astype(np.float32)).cuda()
-    h = torch.randn_like(x)
-    outs = {}
-    for env in ("0", "1"):
-        monkeypatch.setenv("AG_SLAB_NO_TOPO", env)
-        res = []
-        for op in OPS:
-            res.append(_pair(dec, x, op))
-        for ki in (ag.KernelKind.CSR_INTRA_BLOCKED, ag.KernelKind.DENSE_BLOCK):
-            for ke in (ag.KernelKind.CSR_INTER, ag.KernelKind.COO_ATOMIC):
-                y = torch.empty_like(x)
-                K.run_fused_pair(dec, x, y, ag.AggregateOp.SUM, 1.25, relu_src=h,
-                                 kernel_intra=ki, kernel_inter=ke)
-                res.append(to_np(y))
-        outs[env] = res
-    for a, b in zip(outs["0"], outs["1"]):
-        if (a == b).all():
-            continue
-        # only the order-free coo modes may differ (FMAs in another order)
-        assert np.abs(a - b).max() <= 1e-5 * max(1.0, np.abs(b).max())
-    for i in range(3):  # the bitwise CSR pair, each op
-        assert same_float(outs["0"][i], outs["1"][i])
