@@ -298,6 +298,47 @@ int ag_slab_dense_blocks(int64_t num_rows, const int32_t *row_ptr,
 /* Staged far sources per 16-row block (the far-ring capacity). */
 int ag_slab_far_capacity(void);
 
+/* ---- band kernel: the order-free (dense_block, coo_atomic) pair ----------
+ * The same selector pair as ag_fused_spmm with blk_w and AG_EPI_INTER_COO
+ * (kernels.py:228-250 intra, :192-225 inter, combine :253-276), with the
+ * inter topology packed per 16-row block into a RECORD that a producer warp
+ * bulk-copies into an 8-deep shared-memory FIFO (no per-row global topology
+ * loads in the consumers):
+ *   words 0..15 : row i's end offset into the block's pairs (bits 0-19)
+ *                 | nfar << 20 (the row's leading far pairs, <= 255)
+ *                 | 1 << 30 if nfar > 255 (the row takes the general path)
+ *                 | 1 << 31 if the block has more than ag_band_capacity()
+ *                   pairs (then read from the global record, not staged)
+ *   then int32 pairs (code, weight bits) of the inter edges, each row's far
+ *   pairs first (role-ordered CSR [role_mid[r], row_ptr[r+1])), padded to
+ *   16 bytes.  code = band-ring row ((src / 16) % 42) * 16 + src % 16 within
+ *   `window` blocks, else ~src (read from global memory; far_cnt / far_src
+ *   list up to ag_slab_far_capacity() of them per block for L2 prefetch).
+ * ag_band_sizes: per-block record sizes in 16-byte units (int32[nb]) and the
+ * largest pair count (host).  The caller scans them into rec_off
+ * (int32[nb + 1], exclusive) and allocates rec (16-byte aligned,
+ * rec_off[nb] * 16 bytes) for ag_band_records.  window <= ag_band_max_window().
+ * ag_band_spmm: y = dense_intra(x) + coo_inter(x) [+ gin_scale * x] [relu]
+ * [* relu_bits] (flags as in ag_fused_spmm: GIN, RELU (+ relu_out),
+ * RELU_MASK; INTER_COO is implied); feat % 4 == 0, feat > 32, x / rec /
+ * relu_bits 16-byte aligned.  Order-free like the pair it runs (tested at
+ * 1e-5 against the reference pair).  An alternative to ag_fused_spmm's
+ * dense + coo mode, measured slower on the C5 graph. */
+int ag_band_max_window(void);
+int ag_band_capacity(void);
+int ag_band_sizes(int64_t num_rows, const int32_t *row_ptr, const int32_t *role_mid,
+                  int32_t *sizes, int64_t *max_pairs_host, void *stream);
+int ag_band_records(int64_t num_rows, const int32_t *row_ptr, const int32_t *role_col,
+                    const float *role_val, const int32_t *role_mid, int32_t window,
+                    const int32_t *rec_off, int32_t *rec, int32_t *far_cnt,
+                    int32_t *far_src, void *stream);
+int ag_band_spmm(int64_t num_rows, int64_t feat, const int32_t *row_ptr,
+                 const int32_t *rec, const int32_t *rec_off, const int32_t *far_cnt,
+                 const int32_t *far_src, const float *blk_w, int64_t num_edges,
+                 const float *x, float *y, int32_t epi_flags, float gin_scale,
+                 const uint32_t *relu_bits, uint32_t *relu_out, int64_t x_rows,
+                 int32_t window, void *stream);
+
 /* K5 combine (kernels.py:253-276) as a standalone pass. out may alias a. */
 int ag_combine(int64_t num_rows, int64_t feat, const float *a,
                const uint8_t *touched_a, const float *b,

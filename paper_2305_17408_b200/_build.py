@@ -52,7 +52,9 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
 
     def compile_one(src: pathlib.Path) -> pathlib.Path:
         obj = BUILD / (src.name + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        # AG_NVCC_EXTRA: development-only defines (e.g. -DAG_SLAB_TRACE_BUILD)
+        extra = os.environ.get("AG_NVCC_EXTRA", "").split()
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         res = subprocess.run(cmd, capture_output=True, text=True)

@@ -62,6 +62,11 @@ SIGNATURES: dict[str, list] = {
     "ag_slab_window": [I64, P, P, F64, P, P],
     "ag_slab_codes": [I64, P, P, P, P, I32, P, P, P, P, P],
     "ag_slab_far_capacity": [],
+    "ag_band_max_window": [],
+    "ag_band_capacity": [],
+    "ag_band_sizes": [I64, P, P, P, P, P],
+    "ag_band_records": [I64, P, P, P, P, I32, P, P, P, P, P],
+    "ag_band_spmm": [I64, I64, P, P, P, P, P, P, I64, P, P, I32, F32, P, P, I64, I32, P],
     "ag_slab_dense_blocks": [I64, P, P, P, P, P, P],
     "ag_combine": [I64, I64, P, P, P, P, P, I32, P, P],
     "ag_gemm_f32": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, F32, F32, I32, P, I64, P,

@@ -110,6 +110,8 @@ struct GArgs {
   int tma;                  // 1: TMA tensor loads; 0: cp.async element copies
   int sleep;                // producers' done waits: 1 suspend between polls, 0 spin
   uint32_t csleep;          // consumer / dense-warp waits: suspend hint (ns) per poll, 0 spin
+  const int4 *brec;         // band kernel: per-block topology records (ag_band_records), or NULL
+  const int32_t *brec_off;  // [nblocks + 1] record offsets in 16-byte units
   long long *trace;         // AG_SLAB_TRACE: per-block globaltimer stamps of CTA 0 (development)
   int dbg;                  // development knob (AG_SLAB_DEBUG bits, values then garbage): 1 skip the
                             // reductions, 2 far copies, 4 dense products, 8 X tiles, 16 Y stores,
@@ -747,18 +749,35 @@ __device__ __forceinline__ void do_row(const GArgs &a, RowWarp<VEC, W> &w, int64
   if (act && !(a.dbg & 16)) stv<VEC>(yp, out);
 }
 
-template <int VEC>
+// Band-kernel topology records (see band_kernel): per 16-row block, a 64-byte
+// header of row words, the block's inter (code, weight) pairs, and (staged
+// next to them) the block's ReLU-mask words.
+constexpr int kBandCap = 560;               // pairs staged per block (more: read from global)
+constexpr uint32_t kRecHdr = 64;            // 16 row words
+constexpr uint32_t kRecRelu = 512;          // 16 rows x up to 8 mask words (feat <= 256)
+constexpr uint32_t kRecSlot = kRecHdr + kBandCap * 8 + kRecRelu;
+constexpr int kTopoSlots = 8;               // band topology FIFO depth (blocks)
+
+// Shared-memory geometry of one slab-family kernel: an X ring of SLOTS blocks
+// (column tile T = 32 * VEC), the far ring, intra slots, dense-warp weights,
+// the barriers, then per-warp windows (slab) or the topology FIFO (band).
+template <int VEC_, int SLOTS = kSlots, bool BAND = false>
 struct SlabGeom {
+  static constexpr int VEC = VEC_;
+  static constexpr int kSlotsN = SLOTS;
+  static constexpr int kFarRow = SLOTS * kRB;  // first far-ring row (codes >= kFarRow)
   static constexpr int T = 32 * VEC;
   static constexpr uint32_t kRowBytes = T * 4;
   static constexpr uint32_t kSlotBytes = kRB * kRowBytes;
   static constexpr uint32_t kFarSlotBytes = kFarMax * kRowBytes;
-  static constexpr uint32_t kIOff = kSlots * kSlotBytes + kFarSlots * kFarSlotBytes;
+  static constexpr uint32_t kIOff = SLOTS * kSlotBytes + (BAND ? 0 : kFarSlots * kFarSlotBytes);
   static constexpr uint32_t kWOff = kIOff + kISlots * kSlotBytes;  // 2 warps x 2 x 512 B weights
   static constexpr uint32_t kRingBytes = kWOff + 2 * 1024;
   static constexpr uint32_t kBarBytes = (kReady + kDone + kISlots) * 8;
-  static constexpr uint32_t kWinBytes = kConsMax * kWin * 8;
-  static constexpr size_t kSmem = kRingBytes + kBarBytes + kWinBytes;
+  static constexpr uint32_t kWinBytes = BAND ? 0 : kConsMax * kWin * 8;
+  static constexpr uint32_t kTopoBytes = BAND ? kTopoSlots * kRecSlot : 0;
+  static constexpr size_t kSmem = kRingBytes + kBarBytes + kWinBytes + kTopoBytes;
+  static_assert(kBarBytes % 16 == 0 && kRecSlot % 16 == 0, "16-byte aligned topology slots");
 };
 
 // Bulk L2 prefetch of [p, p + bytes), widened to 16-byte granules.
@@ -778,6 +797,13 @@ struct TopoBounds {
 };
 __device__ __forceinline__ TopoBounds topo_bounds(const GArgs &a, uint32_t b, uint32_t kb1) {
   TopoBounds t{0, 0};
+  if (a.brec != nullptr) {  // band kernel: the block's record
+    if (b < kb1) {
+      t.e0 = a.brec_off[b];
+      t.e1 = a.brec_off[b + 1];
+    }
+    return t;
+  }
   if (b < kb1) {
     const int64_t r0 = static_cast<int64_t>(b) * kRB;
     t.e0 = a.row_ptr[r0];
@@ -786,8 +812,13 @@ __device__ __forceinline__ TopoBounds topo_bounds(const GArgs &a, uint32_t b, ui
   return t;
 }
 __device__ __forceinline__ void prefetch_topology(const GArgs &a, uint32_t b, uint32_t kb0,
-                                                  uint32_t kb1, TopoBounds tb) {
+                                                  uint32_t kb1, TopoBounds tb, int64_t c0,
+                                                  int64_t tile_bytes) {
   if (b < kb0 || b >= kb1) return;
+  if (a.brec != nullptr) {  // band: the record and the block's far rows (read by the consumers)
+    l2_prefetch(a.brec + tb.e0, static_cast<int64_t>(tb.e1 - tb.e0) * 16);
+    return;
+  }
   const int64_t r0 = static_cast<int64_t>(b) * kRB;
   const int64_t r1 = std::min<int64_t>(r0 + kRB, a.rows);
   l2_prefetch(a.rowinfo + r0, (r1 - r0) * 16);
@@ -850,12 +881,13 @@ struct BlockSync {
 // consumer block kt = max(kb0, t - H) and completes on ready[kt].  Before
 // overwriting a slot it waits until no consumer block still needs the old
 // block (done[t - kSlots + H]).  It also pulls the topology into L2 ahead.
-template <int VEC>
+template <class G>
 __device__ __forceinline__ void produce_x(const GArgs &a, const CUtensorMap *map, uint32_t ring,
                                           const BlockSync &bs, uint32_t Llo, uint32_t Lhi,
                                           uint32_t kb0, uint32_t kb1, uint32_t H, int tile,
                                           int lane) {
-  using G = SlabGeom<VEC>;
+  constexpr int VEC = G::VEC;
+  constexpr int kSlots = G::kSlotsN;
   const int64_t c0 = static_cast<int64_t>(tile) * G::T;
   uint32_t slot = Llo % kSlots;
   TopoBounds tb = topo_bounds(a, Llo + lane, kb1);
@@ -863,7 +895,7 @@ __device__ __forceinline__ void produce_x(const GArgs &a, const CUtensorMap *map
   for (uint32_t t = Llo; t < Lhi; ++t) {
     const uint32_t i = t - Llo;
     if (i % 32 == 0) {
-      prefetch_topology(a, t + lane, kb0, kb1, tb);
+      prefetch_topology(a, t + lane, kb0, kb1, tb, c0, std::min<int64_t>(G::T, a.feat - c0) * 4);
       tb = tb_next;
       tb_next = topo_bounds(a, t + 64 + lane, kb1);
     }
@@ -917,18 +949,24 @@ __device__ __forceinline__ void produce_x(const GArgs &a, const CUtensorMap *map
   __syncwarp();
 }
 
+// Band kernel: block f's ReLU-mask words (16 rows x ldw words, contiguous) are
+// staged with its record when they fit the slot and the block is whole.
+__device__ __forceinline__ bool band_relu_staged(const GArgs &a, uint32_t f) {
+  return a.relu && a.ldw * kRB * 4 <= kRecRelu && int64_t(f + 1) * kRB <= a.rows;
+}
+
 // Far producer warp: for every consumer block f in [kb0, kb1), copies the
 // tile columns of its staged far sources (far_src; one bulk copy per source,
 // lanes in parallel; cp.async elements when x is not bulk-copyable) into
 // far-ring slot f % kFarSlots once every consumer left block f - kFarSlots,
 // completing on ready[f].  Look-ahead loads are consumed in place (the loop
 // is unrolled by D): rotating them through moves would wait on each load.
-template <int VEC>
+template <class G>
 __device__ __forceinline__ void produce_far(const GArgs &a, uint32_t ring, const BlockSync &bs,
                                             uint32_t kb0, uint32_t kb1, int tile, int lane) {
-  using G = SlabGeom<VEC>;
+  constexpr int VEC = G::VEC;
   constexpr int D = 4;
-  const uint32_t far_ring = ring + kSlots * G::kSlotBytes;
+  const uint32_t far_ring = ring + G::kSlotsN * G::kSlotBytes;
   const int64_t c0 = static_cast<int64_t>(tile) * G::T;
   const uint32_t tile_bytes =
       static_cast<uint32_t>(std::min<int64_t>(G::T, a.feat - c0)) * 4u;  // partial last tile
@@ -969,6 +1007,7 @@ __device__ __forceinline__ void produce_far(const GArgs &a, uint32_t ring, const
         if (lane < cnt && !(a.dbg & 2))
           bulk_g2s(slot_base + lane * G::kRowBytes, a.x + static_cast<int64_t>(src) * a.feat + c0,
                    tile_bytes, bs.rdy(f));
+
       } else {
         if (need >= int64_t(kb0)) bs.wait_done(static_cast<uint32_t>(need));
         for (int j = 0; j < cnt; ++j) {
@@ -995,6 +1034,63 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 
+// Band topology producer: block f's record (header + pairs, or the header
+// alone when the block is unstaged) and its ReLU-mask words into topology
+// slot f % kTopoSlots once every consumer left block f - kTopoSlots,
+// completing on ready[f].  Record offsets are read 32 blocks at a time.
+template <class G>
+__device__ __forceinline__ void produce_topo(const GArgs &a, uint32_t ring, const BlockSync &bs,
+                                             uint32_t kb0, uint32_t kb1, int tile, int lane) {
+  const uint32_t topo = ring + G::kRingBytes + G::kBarBytes + G::kWinBytes;
+  auto rec_offs = [&](uint32_t f) -> int32_t {
+    return (f + lane <= a.nblocks) ? a.brec_off[f + lane] : 0;
+  };
+  int32_t ro = rec_offs(kb0), ro_next = rec_offs(kb0 + 32);
+  // far rows of block f + kFarAhead into L2 (the consumers load them), the
+  // source list loaded one block earlier
+  constexpr uint32_t kFarAhead = 12;
+  const int64_t c0 = static_cast<int64_t>(tile) * G::T;
+  const uint32_t tile_bytes = static_cast<uint32_t>(std::min<int64_t>(G::T, a.feat - c0)) * 4u;
+  const bool pf = !(a.dbg & 64);  // 64: development, no far-row prefetch
+  auto far_at = [&](uint32_t f) -> int32_t {  // -1: none
+    if (!pf || f >= kb1 || lane >= kFarMax) return -1;
+    return lane < a.far_cnt[f] ? a.far_src[static_cast<int64_t>(f) * kFarMax + lane] : -1;
+  };
+  for (uint32_t f = kb0; f < kb0 + kFarAhead; ++f) {
+    const int32_t src = far_at(f);
+    if (src >= 0) l2_prefetch(a.x + static_cast<int64_t>(src) * a.feat + c0, tile_bytes);
+  }
+  int32_t fnext = far_at(kb0 + kFarAhead);
+#pragma unroll 1
+  for (uint32_t f = kb0; f < kb1; ++f) {
+    const uint32_t fi = f - kb0;
+    if (fnext >= 0) l2_prefetch(a.x + static_cast<int64_t>(fnext) * a.feat + c0, tile_bytes);
+    fnext = far_at(f + kFarAhead + 1);
+    const int32_t o0 = __shfl_sync(0xffffffffu, ro, fi & 31);
+    const int32_t o1 = __shfl_sync(0xffffffffu, (fi & 31) == 31 ? ro_next : ro, (fi + 1) & 31);
+    if ((fi & 31) == 31) {
+      ro = ro_next;
+      ro_next = rec_offs(f + 33);
+    }
+    if (lane == 0) {
+      const uint32_t rb = static_cast<uint32_t>(o1 - o0) * 16u;
+      const uint32_t rec_bytes = rb <= kRecHdr + kBandCap * 8 ? rb : kRecHdr;  // unstaged: header
+      const uint32_t relu_bytes =
+          band_relu_staged(a, f) ? static_cast<uint32_t>(kRB * a.ldw * 4) : 0u;
+      tstamp(a, fi, 0);
+      if (fi >= kTopoSlots) bs.wait_done(f - kTopoSlots);
+      tstamp(a, fi, 1);
+      const uint32_t tslot = topo + (f % kTopoSlots) * kRecSlot;
+      mbar_expect_tx(bs.rdy(f), rec_bytes + relu_bytes);
+      bulk_g2s(tslot, a.brec + o0, rec_bytes, bs.rdy(f));
+      if (relu_bytes)
+        bulk_g2s(tslot + kRecHdr + kBandCap * 8,
+                 a.ep.relu_bits + static_cast<int64_t>(f) * kRB * a.ldw, relu_bytes, bs.rdy(f));
+    }
+    __syncwarp();
+  }
+}
+
 // Dense-intra warp (kModeDense3): for every block f in [kb0, kb1), the 16 x 16
 // intra weight block (cp.async, one block ahead) times the block's 16 X rows
 // (already in the ring) -> the 16 intra partials of this column tile, into
@@ -1002,18 +1098,18 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
 // row is read from shared memory once per block instead of once per edge.
 constexpr int kDenseWarps = 2;  // each takes 16 / kDenseWarps rows of every block (measured: 2 > 1, 4)
 
-template <int VEC>
+template <class G, int ND = kDenseWarps>
 __device__ __forceinline__ void dense_intra(const GArgs &a, uint32_t ring, const BlockSync &bs,
                                             uint32_t ivalid, uint32_t kb0, uint32_t kb1,
                                             int lane, int half) {
-  using G = SlabGeom<VEC>;
+  constexpr int VEC = G::VEC;
   // this warp's own double buffer of its kRB / kDenseWarps weight rows (the
   // warps drift apart by a block, so they must not share one)
-  constexpr int kRows = kRB / kDenseWarps;
-  constexpr uint32_t kBuf = kRows * kRB * 4;  // 512 B
+  constexpr int kRows = kRB / ND;
+  constexpr uint32_t kBuf = kRows * kRB * 4;  // 512 B for 2 warps
   const uint32_t wbuf = ring + G::kWOff + half * 2 * kBuf;
   auto fetch_w = [&](uint32_t f, int buf) {  // 16 bytes per lane
-    if (f < kb1)
+    if (f < kb1 && lane * 16u < kBuf)
       cp_async16(wbuf + buf * kBuf + lane * 16,
                  a.blk_w + static_cast<int64_t>(f) * 256 + half * kRows * kRB + lane * 4);
     cp_async_commit();
@@ -1036,7 +1132,7 @@ __device__ __forceinline__ void dense_intra(const GArgs &a, uint32_t ring, const
       }
       continue;
     }
-    const uint32_t xs = ring + (f % kSlots) * G::kSlotBytes + lane * VEC * 4;
+    const uint32_t xs = ring + (f % G::kSlotsN) * G::kSlotBytes + lane * VEC * 4;
     Lv<VEC> xr[kRB];
 #pragma unroll
     for (int j = 0; j < kRB; ++j) xr[j] = lv_lds<VEC>(xs + j * G::kRowBytes);
@@ -1123,11 +1219,11 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
     const BlockSync bs{ready, done, kb0, a.sleep};
     if (kb0 < kb1) {
       if (warp == kCons) {
-        produce_x<VEC>(a, &tmap, ring, bs, Llo, Lhi, kb0, kb1, H, tile, lane);
+        produce_x<G>(a, &tmap, ring, bs, Llo, Lhi, kb0, kb1, H, tile, lane);
       } else if (warp == kCons + 1) {
-        produce_far<VEC>(a, ring, bs, kb0, kb1, tile, lane);
+        produce_far<G>(a, ring, bs, kb0, kb1, tile, lane);
       } else if (DENSE && warp >= kCons - kDenseWarps) {
-        dense_intra<VEC>(a, ring, bs, ivalid, kb0, kb1, lane, warp - (kCons - kDenseWarps));
+        dense_intra<G>(a, ring, bs, ivalid, kb0, kb1, lane, warp - (kCons - kDenseWarps));
       } else {
         RowWarp<VEC, W> w;
         const int64_t fcol = static_cast<int64_t>(tile) * G::T + lane * VEC;
@@ -1248,6 +1344,354 @@ __global__ void __launch_bounds__((cons_warps<MODE>() + 2) * 32, 1)
   }
 }
 
+// ===================================================================== band ==
+// The band kernel: the order-free selector pair (dense_block intra, coo_atomic
+// inter; kModeDense3Coo's semantics) with a leaner consumer.  The slab
+// consumer fetches every row's rowinfo, pairs and mask word from global
+// memory, installs the pairs into a per-warp window and runs a general
+// epilogue: ~200 issue slots of control per row-tile, which bounds it.  Here
+// the far producer also bulk-copies each block's TOPOLOGY RECORD (built once
+// per graph by ag_band_records) and its ReLU-mask words into a shared-memory
+// slot next to the block's far rows, completing on the same ready barrier:
+//   record = 16 row words (end offset of the row's pairs | kRowGlobal) and the
+//            block's inter (code, weight) pairs in row order, codes as in the
+//            slab layout but for the band ring (kBandSlots blocks);
+// so a consumer warp's row is: two shared-memory loads for its bounds, the
+// pairs two at a time (one broadcast LDS.128 per two edges), one conflict-
+// free 256-byte gather and one FFMA2 per edge, then the epilogue.  The only
+// global accesses left in the consumers are the y stores.
+constexpr int kBandSlots = 42;
+constexpr int kBandMaxWindow = (kBandSlots - 9) / 2;  // 16 blocks
+#ifndef AG_BAND_CONS
+#define AG_BAND_CONS 26
+#endif
+#ifndef AG_BAND_DENSE
+#define AG_BAND_DENSE 2
+#endif
+// consumer warps (rows round-robin) and dense-intra warps (each 16 / kBandDense
+// rows of every block): many consumers starve a single-warp stage of issue
+// slots, so the dense product is split over several warps
+constexpr int kBandCons = AG_BAND_CONS;
+constexpr int kBandDense = AG_BAND_DENSE;
+constexpr uint32_t kRowEndMask = 0xFFFFFu;
+constexpr uint32_t kRowGlobal = 1u << 30;    // the row has sources in global memory
+constexpr uint32_t kBlkUnstaged = 1u << 31;  // the block has > kBandCap pairs: read them from global
+using BandGeom = SlabGeom<2, kBandSlots, true>;
+static_assert(BandGeom::kSmem + 256 <= 232448, "band kernel shared memory");
+// a consumer's consecutive rows are kBandCons apart: it skips at most
+// kBandCons / kRB blocks, fewer than the kISlots intra slots (stale-parity safe)
+static_assert(kBandCons / kRB + 1 < kISlots, "consumer row stride vs intra slots");
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void lds_pair2(uint32_t addr, int32_t &c0, float &w0, int32_t &c1,
+                                          float &w1) {
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(c0), "=f"(w0), "=r"(c1), "=f"(w1)
+               : "r"(addr));
+}
+__device__ __forceinline__ void lds_pair(uint32_t addr, int32_t &c, float &w) {
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(c), "=f"(w) : "r"(addr));
+}
+__device__ __forceinline__ uint64_t lds_x(uint32_t xl, int32_t code) {
+  uint64_t v;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(xl + static_cast<uint32_t>(code) * 256u));
+  return v;
+}
+__device__ __forceinline__ void fma2(uint64_t &acc, uint64_t x, float w) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(x), "l"(pk(w, w)));
+}
+
+// One band row: the inter pairs [s, e) of record `pairs` (shared), all in the
+// X ring or the far ring.
+__device__ __forceinline__ uint64_t ldg_x(const float *xg, uint32_t feat, int32_t code) {
+  const float *ptr;  // xg + src * feat as one IMAD.WIDE.U32
+  asm("mad.wide.u32 %0, %1, %2, %3;"
+      : "=l"(ptr)
+      : "r"(static_cast<uint32_t>(~code)), "r"(feat * 4u), "l"(xg));
+  uint64_t v;
+  asm("ld.global.nc.b64 %0, [%1];" : "=l"(v) : "l"(ptr));
+  return v;
+}
+
+// One band row: its nf leading far pairs (sources in global memory, loaded
+// first so their latency overlaps the ring part), then the ring pairs up to e.
+__device__ __forceinline__ uint64_t band_row_fast(uint32_t pairs, uint32_t xl, const float *xg,
+                                                  uint32_t feat, uint32_t s, uint32_t e,
+                                                  uint32_t nf) {
+  uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;  // +0.0f pairs
+  uint64_t fx[4];
+  float fw[4];
+  const uint32_t nq = nf < 4 ? nf : 4;
+#pragma unroll
+  for (uint32_t q = 0; q < 4; ++q) {
+    fx[q] = 0;
+    fw[q] = 0.0f;
+    if (q < nq) {
+      int32_t c;
+      lds_pair(pairs + (s + q) * 8u, c, fw[q]);
+      fx[q] = ldg_x(xg, feat, c);
+    }
+  }
+#pragma unroll 1
+  for (uint32_t j = s + 4; j < s + nf; ++j) {  // rows with more than 4 far sources
+    int32_t c;
+    float w;
+    lds_pair(pairs + j * 8u, c, w);
+    fma2(a1, ldg_x(xg, feat, c), w);
+  }
+  s += nf;
+  uint32_t p = pairs + s * 8u;
+  int n = static_cast<int>(e - s);
+  if (n > 0 && (s & 1u)) {  // align to a pair of pairs
+    int32_t c;
+    float w;
+    lds_pair(p, c, w);
+    fma2(a0, lds_x(xl, c), w);
+    p += 8;
+    --n;
+  }
+#pragma unroll 1
+  for (; n >= 8; n -= 8, p += 64) {
+    int32_t c[8];
+    float w[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) lds_pair2(p + 16 * q, c[2 * q], w[2 * q], c[2 * q + 1], w[2 * q + 1]);
+    uint64_t x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = lds_x(xl, c[q]);
+    fma2(a0, x[0], w[0]);
+    fma2(a1, x[1], w[1]);
+    fma2(a2, x[2], w[2]);
+    fma2(a3, x[3], w[3]);
+    fma2(a0, x[4], w[4]);
+    fma2(a1, x[5], w[5]);
+    fma2(a2, x[6], w[6]);
+    fma2(a3, x[7], w[7]);
+  }
+  if (n >= 4) {
+    int32_t c[4];
+    float w[4];
+    lds_pair2(p, c[0], w[0], c[1], w[1]);
+    lds_pair2(p + 16, c[2], w[2], c[3], w[3]);
+    uint64_t x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[q] = lds_x(xl, c[q]);
+    fma2(a0, x[0], w[0]);
+    fma2(a1, x[1], w[1]);
+    fma2(a2, x[2], w[2]);
+    fma2(a3, x[3], w[3]);
+    p += 32;
+    n -= 4;
+  }
+  if (n >= 2) {
+    int32_t c0, c1;
+    float w0, w1;
+    lds_pair2(p, c0, w0, c1, w1);
+    const uint64_t x0 = lds_x(xl, c0), x1 = lds_x(xl, c1);
+    fma2(a0, x0, w0);
+    fma2(a1, x1, w1);
+    p += 16;
+    n -= 2;
+  }
+  if (n > 0) {
+    int32_t c;
+    float w;
+    lds_pair(p, c, w);
+    fma2(a2, lds_x(xl, c), w);
+  }
+#pragma unroll
+  for (uint32_t q = 0; q < 4; ++q)
+    if (q < nq) fma2(a3, fx[q], fw[q]);
+  const uint64_t one = pk(1.0f, 1.0f);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a0) : "l"(a1), "l"(one));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a2) : "l"(a3), "l"(one));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a0) : "l"(a2), "l"(one));
+  return a0;
+}
+
+// The general band row: pairs from shared memory or (an unstaged block) from
+// the global record; a source is a ring row (code >= 0) or x[~code].
+__device__ __forceinline__ uint64_t band_row_slow(uint32_t pairs, const int2 *gpairs,
+                                                  uint32_t xl, const float *xg, uint32_t feat,
+                                                  uint32_t s, uint32_t e) {
+  uint64_t a0 = 0, a1 = 0;
+#pragma unroll 1
+  for (uint32_t j = s; j < e; ++j) {
+    int32_t c;
+    float w;
+    if (gpairs != nullptr) {
+      const int2 q = __ldg(gpairs + j);
+      c = q.x;
+      w = __int_as_float(q.y);
+    } else {
+      lds_pair(pairs + j * 8u, c, w);
+    }
+    uint64_t xv;
+    if (c >= 0) {
+      xv = lds_x(xl, c);
+    } else {
+      const float *ptr;
+      asm("mad.wide.u32 %0, %1, %2, %3;"
+          : "=l"(ptr)
+          : "r"(static_cast<uint32_t>(~c)), "r"(feat * 4u), "l"(xg));
+      asm("ld.global.nc.b64 %0, [%1];" : "=l"(xv) : "l"(ptr));
+    }
+    fma2((j & 1u) ? a1 : a0, xv, w);
+  }
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a0) : "l"(a1), "l"(pk(1.0f, 1.0f)));
+  return a0;
+}
+
+__device__ __forceinline__ void band_consume(const GArgs &a, uint32_t ring, uint32_t topo,
+                                             const BlockSync &bs, uint32_t ivalid, uint32_t kb0,
+                                             uint32_t kb1, int tile, int warp, int lane) {
+  using G = BandGeom;
+  const int64_t fcol = static_cast<int64_t>(tile) * G::T + lane * 2;
+  const bool act = fcol < a.feat;
+  const uint32_t xl = ring + lane * 8;
+  float *const ylane = a.y + (act ? fcol : 0);
+  const float *const xg = a.x + (act ? fcol : 0);
+  const uint32_t feat = static_cast<uint32_t>(a.feat);
+  const uint32_t wsel = static_cast<uint32_t>(fcol >> 5);
+  const uint32_t r0 = kb0 * kRB;
+  const uint32_t r1 = static_cast<uint32_t>(std::min<int64_t>(int64_t(kb1) * kRB, a.rows));
+  uint32_t kcur = kb0;
+  bool entered = false;
+#pragma unroll 1
+  for (uint32_t r = r0 + warp; r < r1; r += kBandCons) {
+    const uint32_t k = r / kRB;
+    const int i = static_cast<int>(r % kRB);
+    const uint32_t fi = k - kb0;
+    if (k != kcur || !entered) {  // leave the blocks before k, enter k
+      __syncwarp();
+      for (; kcur != k; ++kcur)
+        if (lane == 0) {
+          if (warp == 0) tstamp(a, kcur - kb0, 5);
+          mbar_arrive(bs.done + ((kcur - kb0) % kDone) * 8);
+        }
+      if (warp == 0 && lane == 0) tstamp(a, fi, 3);
+      mbar_wait_hint(bs.rdy(k), bs.rdy_phase(k), a.csleep);
+      if (warp == 0 && lane == 0) tstamp(a, fi, 4);
+      entered = true;
+    }
+    const uint32_t rec = topo + (k % kTopoSlots) * kRecSlot;
+    const uint32_t hw = lds_u32(rec + 4 * i);
+    const uint32_t s = i ? (lds_u32(rec + 4 * (i - 1)) & kRowEndMask) : 0u;
+    const uint32_t e = hw & kRowEndMask;
+    const uint32_t pairs = rec + kRecHdr;
+    uint64_t acc;
+    if (a.dbg & 1) {
+      acc = 0;  // development: no reduction (values garbage)
+    } else if (!(hw & (kRowGlobal | kBlkUnstaged))) {
+      acc = band_row_fast(pairs, xl, xg, feat, s, e, (hw >> 20) & 0xFFu);
+    } else {
+      const int2 *gp = (hw & kBlkUnstaged)
+                           ? reinterpret_cast<const int2 *>(a.brec + a.brec_off[k]) + kRecHdr / 8
+                           : nullptr;
+      acc = band_row_slow(pairs, gp, xl, xg, feat, s, e);
+    }
+    // the block's intra partials (dense warps)
+    mbar_wait_hint(ivalid + (fi % kISlots) * 8, (fi / kISlots) & 1u, a.csleep);
+    uint64_t iv;
+    asm volatile("ld.shared.b64 %0, [%1];"
+                 : "=l"(iv)
+                 : "r"(ring + G::kIOff + (fi % kISlots) * G::kSlotBytes + i * G::kRowBytes +
+                       lane * 8));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(iv), "l"(pk(1.0f, 1.0f)));
+    Vf<2> out;
+    upk(acc, out.v[0], out.v[1]);
+    if (a.ep.flags & AG_EPI_GIN) {
+      float x0, x1;
+      upk(lds_x(xl, static_cast<int32_t>((k % kBandSlots) * kRB + i)), x0, x1);
+      out.v[0] = __fmaf_rn(a.ep.gin_scale, x0, out.v[0]);
+      out.v[1] = __fmaf_rn(a.ep.gin_scale, x1, out.v[1]);
+    }
+    if (a.ep.flags & AG_EPI_RELU) {
+      out.v[0] = fmaxf(out.v[0], 0.0f);
+      out.v[1] = fmaxf(out.v[1], 0.0f);
+    }
+    if (a.relu && act) {
+      const uint32_t word =
+          band_relu_staged(a, k)
+              ? lds_u32(rec + kRecHdr + kBandCap * 8 + (static_cast<uint32_t>(i) * a.ldw + wsel) * 4)
+              : __ldg(a.ep.relu_bits + static_cast<int64_t>(r) * a.ldw + wsel);
+      const uint32_t rb = word >> (fcol & 31);
+      if (!(rb & 1u)) out.v[0] = 0.0f;
+      if (!(rb & 2u)) out.v[1] = 0.0f;
+    }
+    if (a.relu_out != nullptr) {
+      uint32_t *rw = a.relu_out + static_cast<int64_t>(r) * a.ldw;
+      const int64_t c0 = fcol - static_cast<int64_t>(lane) * 2;  // the tile's first column
+      const uint32_t b0 = __ballot_sync(0xffffffffu, act && out.v[0] > 0.0f);
+      const uint32_t b1 = __ballot_sync(0xffffffffu, act && out.v[1] > 0.0f);
+      const uint32_t wd = lane == 0 ? spread16(b0) | (spread16(b1) << 1)
+                                    : spread16(b0 >> 16) | (spread16(b1 >> 16) << 1);
+      if (lane < 2 && c0 + 32 * lane < a.feat) rw[(c0 >> 5) + lane] = wd;
+    }
+    if (act) {
+      float *yp;
+      asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(yp) : "r"(r), "r"(feat * 4u), "l"(ylane));
+      stv<2>(yp, out);
+    }
+  }
+  __syncwarp();
+  for (; kcur < kb1; ++kcur)  // leave the rest of the range
+    if (lane == 0) mbar_arrive(bs.done + ((kcur - kb0) % kDone) * 8);
+}
+
+__global__ void __launch_bounds__((kBandCons + kBandDense + 2) * 32, 1)
+    band_kernel(const __grid_constant__ CUtensorMap tmap, GArgs a) {
+  using G = BandGeom;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ int64_t s_kb[2];
+  const uint32_t ring = su32(smem);
+  const uint32_t ready = ring + G::kRingBytes;
+  const uint32_t done = ready + kReady * 8;
+  const uint32_t ivalid = done + kDone * 8;
+  const uint32_t topo = ring + G::kRingBytes + G::kBarBytes;
+  constexpr int kCons = kBandCons + kBandDense;  // warps arriving on done
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t H = static_cast<uint32_t>(a.H);
+  const int64_t units = static_cast<int64_t>(a.ranges) * a.ntiles;
+  if (threadIdx.x == kCons * 32) tma_prefetch_desc(&tmap);
+#pragma unroll 1
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int tile = static_cast<int>(u % a.ntiles);
+    const int range = static_cast<int>(u / a.ntiles);
+    if (threadIdx.x == 0) {
+      s_kb[0] = range_block(a, range);
+      s_kb[1] = range_block(a, range + 1);
+      for (int q = 0; q < kReady; ++q) mbar_init(ready + q * 8, 2);
+      for (int q = 0; q < kDone; ++q) mbar_init(done + q * 8, kCons);
+      for (int q = 0; q < kISlots; ++q) mbar_init(ivalid + q * 8, kBandDense);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    const uint32_t kb0 = static_cast<uint32_t>(s_kb[0]), kb1 = static_cast<uint32_t>(s_kb[1]);
+    const uint32_t Llo = kb0 > H ? kb0 - H : 0u;
+    const uint32_t Lhi = static_cast<uint32_t>(std::min<int64_t>(a.xblocks, int64_t(kb1) + H));
+    const BlockSync bs{ready, done, kb0, a.sleep};
+    if (kb0 < kb1) {
+      if (warp == kCons) produce_x<G>(a, &tmap, ring, bs, Llo, Lhi, kb0, kb1, H, tile, lane);
+      else if (warp == kCons + 1) produce_topo<G>(a, ring, bs, kb0, kb1, tile, lane);
+      else if (warp >= kBandCons) dense_intra<G, kBandDense>(a, ring, bs, ivalid, kb0, kb1, lane, warp - kBandCons);
+      else band_consume(a, ring, topo, bs, ivalid, kb0, kb1, tile, warp, lane);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int q = 0; q < kReady; ++q) mbar_inval(ready + q * 8);
+      for (int q = 0; q < kDone; ++q) mbar_inval(done + q * 8);
+      for (int q = 0; q < kISlots; ++q) mbar_inval(ivalid + q * 8);
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------- window radius (per graph) --
 constexpr int kHistBins = 64;
 
@@ -1278,6 +1722,26 @@ int env_int(const char *name, int dflt) {
 // largest window radius: >= 8 blocks of drift slack between the fastest and
 // slowest consumer warp
 constexpr int kMaxWindow = (kSlots - 9) / 2;
+
+// Development trace printer (AG_SLAB_TRACE with an -DAG_SLAB_TRACE_BUILD build).
+void print_trace(long long *trace, const char *name, const GArgs &a, cudaStream_t st) {
+  long long h[kTraceBlocks * 8];
+  if (cudaStreamSynchronize(st) != cudaSuccess ||
+      cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaFree(trace);
+    return;
+  }
+  cudaFree(trace);
+  const long long t0 = h[0] ? h[0] : h[3];
+  std::fprintf(stderr, "%s trace feat=%d H=%d (us; far/topo: done-wait start..end | X last | "
+                       "cons0 ready-wait start..end | cons0 leave | dense ivalid | last-cons leave)\n",
+               name, a.feat, a.H);
+  for (int i = 0; i < kTraceBlocks; ++i) {
+    auto f = [&](int j) { return h[i * 8 + j] ? (h[i * 8 + j] - t0) / 1e3 : -1.0; };
+    std::fprintf(stderr, "blk %2d far %7.2f..%7.2f | X %7.2f | c0 %7.2f..%7.2f leave %7.2f | dense %7.2f | "
+                         "clast leave %7.2f\n", i, f(0), f(1), f(2), f(3), f(4), f(5), f(6), f(7));
+  }
+}
 
 template <int VEC>
 int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
@@ -1351,21 +1815,7 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
   }
   k<<<grid, threads, smem, st>>>(map, a);
   AG_LAUNCH_CHECK("slab_kernel");
-  if (trace) {
-    long long h[kTraceBlocks * 8];
-    AG_CUDA(cudaStreamSynchronize(st));
-    AG_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
-    cudaFree(trace);
-    const long long t0 = h[0] ? h[0] : h[3];
-    std::fprintf(stderr, "slab trace mode=%d feat=%d H=%d (us; far: done-wait start..end | X last | "
-                         "cons0 ready-wait start..end | cons0 leave | dense ivalid | last-cons leave)\n",
-                 mode, a.feat, a.H);
-    for (int i = 0; i < kTraceBlocks; ++i) {
-      auto f = [&](int j) { return h[i * 8 + j] ? (h[i * 8 + j] - t0) / 1e3 : -1.0; };
-      std::fprintf(stderr, "blk %2d far %7.2f..%7.2f | X %7.2f | c0 %7.2f..%7.2f leave %7.2f | dense %7.2f | "
-                           "clast leave %7.2f\n", i, f(0), f(1), f(2), f(3), f(4), f(5), f(6), f(7));
-    }
-  }
+  if (trace) print_trace(trace, "slab", a, st);
   return AG_OK;
 }
 
@@ -1456,6 +1906,136 @@ __global__ void dense_block_weights_kernel(int64_t rows, const int32_t *row_ptr,
       for (int32_t e = row_ptr[r]; e < mid[r]; ++e)
         w[(r - b * kRB) * kRB + (col[e] - b * kRB)] = val ? val[e] : 1.0f;
   }
+}
+
+// Band records, pass 1: per 16-row block, its record size in 16-byte units
+// (64-byte header + 8 bytes per inter pair, padded) and the largest count.
+__global__ void band_size_kernel(int64_t rows, const int32_t *row_ptr, const int32_t *mid,
+                                 int32_t *sizes, unsigned int *max_pairs) {
+  const int64_t nb = (rows + kRB - 1) / kRB;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r1 = std::min<int64_t>(b * kRB + kRB, rows);
+    int64_t n = 0;
+    for (int64_t r = b * kRB; r < r1; ++r) n += row_ptr[r + 1] - mid[r];
+    sizes[b] = static_cast<int32_t>((kRecHdr + 8 * n + 15) / 16);
+    atomicMax(max_pairs, static_cast<unsigned int>(std::min<int64_t>(n, 0x7fffffff)));
+  }
+}
+
+// Band records, pass 2 (one thread per block): row words and the inter pairs
+// [mid[r], row_ptr[r+1]) of the role-ordered CSR as (code, weight bits), each
+// row's FAR pairs first: a source within `window` blocks of the destination's
+// block is a band-ring row, code ((src / 16) % kBandSlots) * 16 + src % 16;
+// any other source is read from global memory by the consumer, code ~src.
+// Row word i = end offset of row i's pairs | nfar << 20 (its leading far
+// pairs; more than 255: kRowGlobal, the general path) | kBlkUnstaged when the
+// block has more than kBandCap pairs.  far_cnt / far_src list up to kFarMax
+// distinct far sources per block (the producer prefetches them into L2).
+__global__ void band_record_kernel(int64_t rows, const int32_t *row_ptr, const int32_t *col,
+                                   const float *val, const int32_t *mid, int32_t window,
+                                   const int32_t *rec_off, int4 *rec, int32_t *far_cnt,
+                                   int32_t *far_src) {
+  const int64_t nb = (rows + kRB - 1) / kRB;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t *hdr = reinterpret_cast<uint32_t *>(rec + rec_off[b]);
+    int2 *pr = reinterpret_cast<int2 *>(hdr + kRecHdr / 4);
+    const int64_t r1 = std::min<int64_t>(b * kRB + kRB, rows);
+    int64_t n = 0;
+    for (int64_t r = b * kRB; r < r1; ++r) n += row_ptr[r + 1] - mid[r];
+    const uint32_t unstaged = n > kBandCap ? kBlkUnstaged : 0u;
+    int32_t staged[kFarMax];
+    int j = 0;
+    uint32_t pos = 0;
+    auto near = [&](int32_t c) {
+      const int64_t d = static_cast<int64_t>(c / kRB) - b;
+      return d >= -window && d <= window;
+    };
+    for (int i = 0; i < kRB; ++i) {
+      const int64_t r = b * kRB + i;
+      uint32_t nfar = 0;
+      if (r < rows) {
+        for (int pass = 0; pass < 2; ++pass)  // far pairs, then ring pairs
+          for (int32_t ed = mid[r]; ed < row_ptr[r + 1]; ++ed) {
+            const int32_t c = col[ed];
+            const bool nr = near(c);
+            if (nr != (pass == 1)) continue;
+            int32_t code;
+            if (nr) {
+              code = static_cast<int32_t>(((c / kRB) % kBandSlots) * kRB + c % kRB);
+            } else {
+              code = ~c;
+              ++nfar;
+              int k = 0;
+              while (k < j && staged[k] != c) ++k;
+              if (k == j && j < kFarMax) staged[j++] = c;
+            }
+            pr[pos++] = make_int2(code, __float_as_int(val ? val[ed] : 1.0f));
+          }
+      }
+      hdr[i] = pos | (nfar > 255 ? kRowGlobal : (nfar << 20)) | unstaged;
+    }
+    if (pos & 1u) pr[pos] = make_int2(0, 0);  // the 16-byte pad
+    far_cnt[b] = j;
+    for (int k = 0; k < j; ++k) far_src[b * kFarMax + k] = staged[k];
+  }
+}
+
+int launch_band(GArgs a, int window, cudaStream_t st) {
+  using G = BandGeom;
+  a.H = window;
+  a.dbg = env_int("AG_SLAB_DEBUG", 0);
+  a.sleep = env_int("AG_SLAB_SLEEP", 1);
+  a.csleep = static_cast<uint32_t>(env_int("AG_SLAB_CSLEEP", 0));
+  a.nblocks = (a.rows + kRB - 1) / kRB;
+  a.xblocks = (a.x_rows + kRB - 1) / kRB;
+  a.ntiles = static_cast<int>((a.feat + G::T - 1) / G::T);
+  a.relu = (a.ep.flags & AG_EPI_RELU_MASK) ? 1 : 0;
+  a.ldw = relu_words(a.feat);
+  const size_t smem = G::kSmem;
+  auto k = band_kernel;
+  {
+    cudaFuncAttributes fa;
+    AG_CUDA(cudaFuncGetAttributes(&fa, k));
+    int dev = 0, optin = 0;
+    AG_CUDA(cudaGetDevice(&dev));
+    AG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (smem + fa.sharedSizeBytes > static_cast<size_t>(optin))
+      return fail(AG_ERR_CUDA, "band kernel needs %zu + %zu B of shared memory, the device allows %d",
+                  smem, static_cast<size_t>(fa.sharedSizeBytes), optin);
+  }
+  AG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  const int sms = sm_count();
+  int64_t ranges = (2LL * sms + a.ntiles - 1) / a.ntiles;
+  ranges = std::max<int64_t>(1, std::min<int64_t>(ranges, a.nblocks / 4));
+  a.ranges = static_cast<int>(ranges);
+  const int64_t units = ranges * a.ntiles;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, sms)));
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  TmaEncodeFn enc = tma_encode_fn();
+  if (!enc) return fail(AG_ERR_CUDA, "band kernel: no cuTensorMapEncodeTiled");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.feat), static_cast<cuuint64_t>(a.x_rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.feat) * 4};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(G::T), static_cast<cuuint32_t>(kRB)};
+  cuuint32_t es[2] = {1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(a.x), dims, strides, box,
+          es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return fail(AG_ERR_CUDA, "band kernel: tensor map encode failed");
+  a.tma = 1;
+  long long *trace = nullptr;
+  if (std::getenv("AG_SLAB_TRACE")) {
+    AG_CUDA(cudaMalloc(&trace, kTraceBlocks * 8 * sizeof(long long)));
+    AG_CUDA(cudaMemset(trace, 0, kTraceBlocks * 8 * sizeof(long long)));
+    a.trace = trace;
+  }
+  k<<<grid, (kBandCons + kBandDense + 2) * 32, smem, st>>>(map, a);
+  AG_LAUNCH_CHECK("band_kernel");
+  if (trace) print_trace(trace, "band", a, st);
+  return AG_OK;
 }
 
 }  // namespace
@@ -1612,4 +2192,96 @@ extern "C" int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
                        : kModeAny;
   if (v2) return launch_slab<2>(a, mode, window, st);
   return launch_slab<1>(a, mode, window, st);
+}
+
+extern "C" int ag_band_max_window(void) { return kBandMaxWindow; }
+extern "C" int ag_band_capacity(void) { return kBandCap; }
+
+extern "C" int ag_band_sizes(int64_t num_rows, const int32_t *row_ptr, const int32_t *role_mid,
+                             int32_t *sizes, int64_t *max_pairs_host, void *stream) {
+  if (num_rows < 0) return fail(AG_ERR_VALUE, "negative sizes");
+  if (role_mid == nullptr || sizes == nullptr || max_pairs_host == nullptr)
+    return fail(AG_ERR_VALUE, "role_mid, sizes and max_pairs are required");
+  *max_pairs_host = 0;
+  if (num_rows == 0) return AG_OK;
+  if (num_rows > 2147483647LL) return fail(AG_ERR_VALUE, "too many rows for int32 CSR");
+  cudaStream_t st = as_stream(stream);
+  const int64_t nb = (num_rows + kRB - 1) / kRB;
+  Scratch mx;
+  AG_CUDA(mx.alloc(sizeof(unsigned int), st));
+  AG_CUDA(cudaMemsetAsync(mx.ptr, 0, sizeof(unsigned int), st));
+  band_size_kernel<<<grid_for(nb, 128), 128, 0, st>>>(num_rows, row_ptr, role_mid, sizes,
+                                                      mx.as<unsigned int>());
+  AG_LAUNCH_CHECK("band_size_kernel");
+  unsigned int h = 0;
+  AG_CUDA(cudaMemcpyAsync(&h, mx.ptr, sizeof(h), cudaMemcpyDeviceToHost, st));
+  AG_CUDA(cudaStreamSynchronize(st));
+  *max_pairs_host = h;
+  return AG_OK;
+}
+
+extern "C" int ag_band_records(int64_t num_rows, const int32_t *row_ptr, const int32_t *role_col,
+                               const float *role_val, const int32_t *role_mid, int32_t window,
+                               const int32_t *rec_off, int32_t *rec, int32_t *far_cnt,
+                               int32_t *far_src, void *stream) {
+  if (num_rows < 0) return fail(AG_ERR_VALUE, "negative sizes");
+  if (window < 0 || window > kBandMaxWindow)
+    return fail(AG_ERR_VALUE, "window must be in [0, %d]", kBandMaxWindow);
+  if (role_mid == nullptr || rec_off == nullptr || rec == nullptr)
+    return fail(AG_ERR_VALUE, "role_mid, rec_off and rec are required");
+  if (reinterpret_cast<uintptr_t>(rec) & 15) return fail(AG_ERR_VALUE, "rec must be 16-byte aligned");
+  if (num_rows == 0) return AG_OK;
+  const int64_t nb = (num_rows + kRB - 1) / kRB;
+  band_record_kernel<<<grid_for(nb, 128), 128, 0, as_stream(stream)>>>(
+      num_rows, row_ptr, role_col, role_val, role_mid, window, rec_off,
+      reinterpret_cast<int4 *>(rec), far_cnt, far_src);
+  AG_LAUNCH_CHECK("band_record_kernel");
+  return AG_OK;
+}
+
+extern "C" int ag_band_spmm(int64_t num_rows, int64_t feat, const int32_t *row_ptr,
+                            const int32_t *rec, const int32_t *rec_off, const int32_t *far_cnt,
+                            const int32_t *far_src, const float *blk_w, int64_t num_edges,
+                            const float *x, float *y, int32_t epi_flags, float gin_scale,
+                            const uint32_t *relu_bits, uint32_t *relu_out, int64_t x_rows,
+                            int32_t window, void *stream) {
+  if (num_rows < 0 || feat < 0 || num_edges < 0) return fail(AG_ERR_VALUE, "negative sizes");
+  constexpr int32_t kFlags = AG_EPI_GIN | AG_EPI_RELU_MASK | AG_EPI_RELU | AG_EPI_INTER_COO;
+  if (epi_flags & ~kFlags) return fail(AG_ERR_VALUE, "ag_band_spmm takes GIN / RELU / RELU_MASK flags");
+  if ((epi_flags & AG_EPI_RELU_MASK) && relu_bits == nullptr)
+    return fail(AG_ERR_VALUE, "AG_EPI_RELU_MASK needs relu_bits");
+  if (relu_out != nullptr && !(epi_flags & AG_EPI_RELU))
+    return fail(AG_ERR_VALUE, "relu_out is written with AG_EPI_RELU only");
+  if (window < 0 || window > kBandMaxWindow)
+    return fail(AG_ERR_VALUE, "window must be in [0, %d]", kBandMaxWindow);
+  if (x_rows < num_rows) return fail(AG_ERR_VALUE, "x_rows must be >= num_rows");
+  if (!row_ptr || !rec || !rec_off || !far_cnt || !far_src || !blk_w)
+    return fail(AG_ERR_VALUE, "row_ptr / band records / far lists / blk_w are required");
+  if (num_rows == 0 || feat == 0) return AG_OK;
+  if (feat % 4 != 0 || feat <= 32 || (reinterpret_cast<uintptr_t>(x) & 15) ||
+      (reinterpret_cast<uintptr_t>(y) & 7) || (reinterpret_cast<uintptr_t>(rec) & 15) ||
+      (relu_bits && (reinterpret_cast<uintptr_t>(relu_bits) & 15)))
+    return fail(AG_ERR_VALUE, "ag_band_spmm needs feat % 4 == 0, feat > 32, 16-byte aligned x / rec / relu_bits");
+  if (x_rows > 2147483647LL || num_edges > 2147483647LL)
+    return fail(AG_ERR_VALUE, "too many rows or edges for int32 CSR");
+  GArgs a{};
+  a.rows = num_rows;
+  a.x_rows = x_rows;
+  a.feat = static_cast<int>(feat);
+  a.mask = 3;
+  a.row_ptr = row_ptr;
+  a.far_cnt = far_cnt;
+  a.far_src = far_src;
+  a.weighted = 1;
+  a.has_mid = 1;
+  a.blk_w = blk_w;
+  a.brec = reinterpret_cast<const int4 *>(rec);
+  a.brec_off = rec_off;
+  a.x = x;
+  a.y = y;
+  a.ep = Epi{AG_OP_SUM, epi_flags, nullptr, nullptr, x, feat, gin_scale, relu_bits};
+  a.relu_out = relu_out;
+  a.cost_total = num_edges + kRowCost * num_rows;
+  a.one = 1.0f;
+  return launch_band(a, window, as_stream(stream));
 }

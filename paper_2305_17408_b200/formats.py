@@ -68,7 +68,7 @@ class CsrMatrix:
     """Compressed sparse rows over destination vertices."""
 
     __slots__ = ("num_vertices", "row_ptr", "col_idx", "_val", "_ones", "_rows", "_touched",
-                 "_off_block", "_long", "_window", "_codes", "_dense16")
+                 "_off_block", "_long", "_window", "_codes", "_dense16", "_band")
 
     def __init__(self, num_vertices: int, row_ptr: torch.Tensor, col_idx: torch.Tensor,
                  val: torch.Tensor | None, rows: torch.Tensor | None = None):
@@ -81,6 +81,7 @@ class CsrMatrix:
         self._window = None
         self._codes = {}
         self._dense16 = None
+        self._band = None
 
     @property
     def val(self) -> torch.Tensor:
@@ -170,6 +171,37 @@ class CsrMatrix:
             lay = (mid, cv, rowinfo, far_cnt, far_src, int(val is not None))
             self._codes[key] = lay
         return lay
+
+    def band_layout(self):
+        """(rec, rec_off, far_cnt, far_src, window) for ag_band_spmm, cached:
+        the inter edges of the B = 16 role layout packed into one record per
+        16-row block (ag_band_sizes / ag_band_records), window clipped to the
+        band ring's reach."""
+        if self._band is None:
+            mid, col, val = self.role_layout(16)
+            dev = self.row_ptr.device
+            V = self.num_vertices
+            nb = max((V + 15) // 16, 1)
+            sizes = torch.zeros(nb, dtype=torch.int32, device=dev)
+            mx = _lib.out_i64()
+            _lib.call("ag_band_sizes", V, _lib.ptr(self.row_ptr), _lib.ptr(mid), _lib.ptr(sizes),
+                      _lib.byref(mx), _lib.stream())
+            off = torch.zeros(nb + 1, dtype=torch.int64, device=dev)
+            torch.cumsum(sizes, 0, out=off[1:])
+            total = int(off[-1].item())
+            if total >= 2 ** 31:
+                raise ValueError("band records exceed int32 offsets")
+            off = off.to(torch.int32)
+            rec = torch.zeros(max(total, 1) * 4, dtype=torch.int32, device=dev)
+            cap = int(_lib.load().ag_slab_far_capacity())
+            far_cnt = torch.zeros(nb, dtype=torch.int32, device=dev)
+            far_src = torch.zeros(nb * cap, dtype=torch.int32, device=dev)
+            window = min(self.window(), int(_lib.load().ag_band_max_window()))
+            _lib.call("ag_band_records", V, _lib.ptr(self.row_ptr), _lib.ptr(col), _lib.ptr(val),
+                      _lib.ptr(mid), window, _lib.ptr(off), _lib.ptr(rec), _lib.ptr(far_cnt),
+                      _lib.ptr(far_src), _lib.stream())
+            self._band = (rec, off, far_cnt, far_src, window)
+        return self._band
 
     def dense_blocks16(self) -> torch.Tensor:
         """The intra runs of the B = 16 role layout as dense 16 x 16 blocks

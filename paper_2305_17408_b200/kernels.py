@@ -24,6 +24,7 @@ signature compatibility and ignored.
 from __future__ import annotations
 
 import enum
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -126,6 +127,26 @@ def _bits_for(relu_src, relu_bits_in, rows: int, feat: int):
     return relu_bits(relu_src)
 
 
+_BAND_FLAGS = None
+
+
+def _band_ok(x: torch.Tensor, y: torch.Tensor, rb, flags: int) -> bool:
+    """The band kernel (ag_band_spmm) takes this order-free dense + coo launch:
+    feat % 4 == 0 and > 32, 16-byte aligned operands, GIN / RELU / RELU_MASK
+    epilogues only.  Opt-in (AG_BAND=1): measured slower than the slab
+    kernel's dense + coo mode at every C5 width ("band kernel")."""
+    global _BAND_FLAGS
+    if _BAND_FLAGS is None:
+        _BAND_FLAGS = (_lib.AG_EPI_GIN | _lib.AG_EPI_RELU | _lib.AG_EPI_RELU_MASK
+                       | _lib.AG_EPI_INTER_COO)
+    if os.environ.get("AG_BAND", "0") != "1":
+        return False
+    F = x.shape[1]
+    return (F % 4 == 0 and F > 32 and x.stride(0) == F and y.stride(0) == F
+            and x.data_ptr() % 16 == 0 and y.data_ptr() % 8 == 0
+            and (rb is None or rb.data_ptr() % 16 == 0) and (flags & ~_BAND_FLAGS) == 0)
+
+
 def launch_fused(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp,
                  block: int = 0, mask: int = 2, flags: int = 0,
                  other_touched: torch.Tensor | None = None, deg: torch.Tensor | None = None,
@@ -143,6 +164,15 @@ def launch_fused(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp
     rb = _bits_for(relu_src, relu_bits_in, a.num_vertices, x.shape[1])
     if relu_out is not None:
         _bits_for(None, relu_out, a.num_vertices, x.shape[1])
+    if dense_intra and block == 16 and mask == 3 and op is AggregateOp.SUM \
+            and (flags & _lib.AG_EPI_INTER_COO) and _band_ok(x, y, rb, flags):
+        rec, off, far_cnt, far_src, window = a.band_layout()
+        _lib.call("ag_band_spmm", a.num_vertices, x.shape[1], _lib.ptr(a.row_ptr), _lib.ptr(rec),
+                  _lib.ptr(off), _lib.ptr(far_cnt), _lib.ptr(far_src), _lib.ptr(a.dense_blocks16()),
+                  a.num_edges, _lib.ptr(x), _lib.ptr(y),
+                  flags | (_lib.AG_EPI_RELU_MASK if rb is not None else 0), float(gin_scale),
+                  _lib.ptr(rb), _lib.ptr(relu_out), x.shape[0], window, _lib.stream())
+        return
     mid, cv, rowinfo, far_cnt, far_src, weighted = a.slab_layout(block)
     _lib.call("ag_fused_spmm", a.num_vertices, x.shape[1], int(mask), _lib.ptr(a.row_ptr),
               _lib.ptr(mid), _lib.ptr(cv), _lib.ptr(rowinfo), _lib.ptr(far_cnt),

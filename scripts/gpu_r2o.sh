@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python scripts/slab_sweep.py --feat 256 --pairs "dense_block+coo_atomic" --knob AG_SLAB_DEBUG=0,64,7,71 > gpurun_out/sweep_band2.log 2>&1
+AG_NVCC_EXTRA=-DAG_SLAB_TRACE_BUILD python -c "from paper_2305_17408_b200 import _build; _build.build(force=True)"
+AG_SLAB_TRACE=1 timeout 600 python scripts/kbench.py --feat 256 --only fused_pair --pair dense_block,coo_atomic > gpurun_out/trace_band.log 2>&1
+AG_BAND=0 AG_SLAB_TRACE=1 timeout 600 python scripts/kbench.py --feat 256 --only fused_pair --pair dense_block,coo_atomic > gpurun_out/trace_slab.log 2>&1
+echo done
