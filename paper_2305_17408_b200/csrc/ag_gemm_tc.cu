@@ -104,19 +104,23 @@ __device__ __forceinline__ long long gtime() {
 __device__ __forceinline__ uint32_t su32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+constexpr uint32_t kWaitHintNs = 20000;
 __device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
 }
+// Waits suspend the warp in hardware (try_wait with a time hint) until the
+// phase completes instead of spinning: idle splitter / epilogue warps polling
+// took a third of the issue slots the epilogue needs (ncu, C5 dH product).
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
   uint32_t done = 0;
   uint32_t spins = 0;
   while (!done) {
-    if (++spins > (1u << 24)) __trap();  // a lost arrival: fail instead of hanging
+    if (++spins > (1u << 22)) __trap();  // a lost arrival: fail instead of hanging
     asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
-        : "r"(su32(b)), "r"(parity)
+        : "r"(su32(b)), "r"(parity), "r"(kWaitHintNs)
         : "memory");
   }
 }
@@ -304,10 +308,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t total = tiles_mn * g.splits;
   const int nkb_full = static_cast<int>(g.k_per_split / BK);
   constexpr uint16_t kAll = static_cast<uint16_t>((1u << CL) - 1u);
+  // tile index math in 32 bits (64-bit division is a long software sequence on
+  // the epilogue's critical path between tiles; tile counts are < 2^31)
+  const uint32_t tmn32 = static_cast<uint32_t>(tiles_mn), nt32 = static_cast<uint32_t>(g.n_tiles);
   auto tile_m0 = [&](int64_t t) -> int64_t {
-    return (((t % tiles_mn) / g.n_tiles) * CL + rank) * BM;
+    return static_cast<int64_t>(((static_cast<uint32_t>(t) % tmn32) / nt32) * CL + rank) * BM;
   };
-  auto tile_n0 = [&](int64_t t) -> int64_t { return ((t % tiles_mn) % g.n_tiles) * BN; };
+  auto tile_n0 = [&](int64_t t) -> int64_t {
+    return static_cast<int64_t>((static_cast<uint32_t>(t) % tmn32) % nt32) * BN;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -340,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // k-blocks of tile t (the last split may be shorter)
   auto tile_kblocks = [&](int64_t t, int64_t &k0) -> int {
-    const int64_t s = t / tiles_mn;
+    const int64_t s = static_cast<uint32_t>(t) / tmn32;
     k0 = s * g.k_per_split;
     const int64_t k1 = std::min<int64_t>(g.K, k0 + g.k_per_split);
     const int64_t nk = (k1 - k0 + BK - 1) / BK;
@@ -409,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int64_t t = cid; t < total; t += ncl) {
       int64_t k0;
       const int nkb = tile_kblocks(t, k0);
-      const int ti = static_cast<int>((t - cid) / ncl);
+      const int ti = static_cast<int>(static_cast<uint32_t>(t - cid) / static_cast<uint32_t>(ncl));
       const bool tr = g.trace != nullptr && blockIdx.x == 0 && lane == 0 && ti < kTraceTiles;
       if (tr) g.trace[ti * 10 + 0] = gtime();
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -497,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t t = cid; t < total; t += ncl) {
-      const int64_t s = t / tiles_mn;
+      const int64_t s = static_cast<uint32_t>(t) / tmn32;
       const int64_t m0 = tile_m0(t);
       const int64_t n0 = tile_n0(t);
       if (g.mask != nullptr && g.splits == 1 && warp == kEpiWarp0 && lane == 0) {
@@ -519,9 +528,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t == cid) prefetch_rows(t);
         prefetch_rows(t + ncl);
       }
-      const int ti = static_cast<int>((t - cid) / ncl);
+      const int ti = static_cast<int>(static_cast<uint32_t>(t - cid) / static_cast<uint32_t>(ncl));
       const bool tr = g.trace != nullptr && blockIdx.x == 0 && warp == kEpiWarp0 && lane == 0 &&
                       ti < kTraceTiles;
+      // this warp's 32 rows' ReLU-mask words for its column half, lane = row:
+      // loaded once per tile before the accumulator wait (their latency
+      // overlaps it); the row passes below take them by shuffle.  The forward
+      // mask words (mask_out) are gathered the same way and stored once.
+      const int64_t myrow = m0 + q * 32 + lane;
+      const int nwords = (c_hi - c_lo) / 32;
+      uint32_t mw[4] = {0u, 0u, 0u, 0u}, ow[4] = {0u, 0u, 0u, 0u};
+      if (g.mask != nullptr && g.splits == 1 && myrow < g.M && !(g.exp & 8)) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          if (w < nwords && n0 + c_lo + 32 * w < g.N)
+            mw[w] = __ldg(g.mask + myrow * g.ldm + ((n0 + c_lo) >> 5) + w);
+      }
       if (tr) g.trace[ti * 10 + 3] = gtime();
       mbar_wait(&tfull[acc], acc_phase);
       if (tr) g.trace[ti * 10 + 4] = gtime();
@@ -538,6 +560,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rsub = lane >> 3, j4 = lane & 7;  // read-back role: row rsub + 4 i, chunk j4
 #pragma unroll 1
       for (int c = c_lo; c < c_hi; c += 32) {
+        const int cw = (c - c_lo) >> 5;
+        const uint32_t mwc = cw == 0 ? mw[0] : cw == 1 ? mw[1] : cw == 2 ? mw[2] : mw[3];
+        uint32_t owc = 0;
         float v[32];
         {
           uint32_t rh[32], rc[32];
@@ -576,20 +601,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (direct && (g.mask != nullptr || g.beta != 0.0f)) {
 #pragma unroll
           for (int hf = 0; hf < 8; hf += 4) {  // four passes' loads in flight at a time
-          float4 mk[4], cv[4];
+          uint32_t mk[4];
+          float4 cv[4];
 #pragma unroll
           for (int i0 = 0; i0 < 4; ++i0) {
             const int i = hf + i0;
             const int64_t grow = grow0 + 4 * i;
             const bool in = grow < g.M && colok;
-            mk[i0] = make_float4(1.f, 1.f, 1.f, 1.f);
             cv[i0] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (in && g.mask != nullptr && !(g.exp & 8)) {
-              // the 4 columns' bits of the row's mask word (col % 4 == 0)
-              const uint32_t nib = (__ldg(g.mask + grow * g.ldm + (col >> 5)) >> (col & 31)) & 15u;
-              mk[i0] = make_float4(nib & 1u ? 1.f : 0.f, nib & 2u ? 1.f : 0.f,
-                                   nib & 4u ? 1.f : 0.f, nib & 8u ? 1.f : 0.f);
-            }
+            // the 4 columns' bits of the row's mask word (col % 4 == 0), from
+            // the lane that loaded row 4 i + rsub
+            const uint32_t word = __shfl_sync(0xffffffffu, mwc, 4 * i + rsub);
+            mk[i0] = (g.mask != nullptr && !(g.exp & 8)) ? (word >> (col & 31)) & 15u : 15u;
             if (in && g.beta != 0.0f) {
               const float *cp = g.C + grow * g.ldc + col;
               if (vec_ok && col4) {
@@ -606,13 +629,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i0 = 0; i0 < 4; ++i0) {
             const int i = hf + i0;
             float *ov = &o[i].x;
-            const float *m4 = &mk[i0].x, *c4 = &cv[i0].x;
+            const float *c4 = &cv[i0].x;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              float r = g.alpha * ov[e];
+              float r = g.alpha == 1.0f ? ov[e] : g.alpha * ov[e];
               if (g.beta != 0.0f) r = fmaf(g.beta, c4[e], r);
               if (g.relu) r = fmaxf(r, 0.0f);
-              if (g.mask != nullptr && !(m4[e] > 0.0f)) r = 0.0f;
+              if (!((mk[i0] >> e) & 1u)) r = 0.0f;
               ov[e] = r;
             }
           }
@@ -643,9 +666,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             wd |= __shfl_xor_sync(0xffffffffu, wd, 1);
             wd |= __shfl_xor_sync(0xffffffffu, wd, 2);
             wd |= __shfl_xor_sync(0xffffffffu, wd, 4);
-            const int64_t grow = grow0 + 4 * i;
-            if (j4 == 0 && grow < g.M && colok) g.mask_out[grow * g.ldmo + (col >> 5)] = wd;
+            // lane l keeps row l's word (row 4 i + (l & 3) lives in group l & 3)
+            const uint32_t wrow = __shfl_sync(0xffffffffu, wd, (lane & 3) * 8);
+            if ((lane >> 2) == i) owc = wrow;
           }
+          if (cw == 0) ow[0] = owc;
+          else if (cw == 1) ow[1] = owc;
+          else if (cw == 2) ow[2] = owc;
+          else ow[3] = owc;
         }
         if (!(g.exp & 4)) {
 #pragma unroll
@@ -676,6 +704,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
 
+      }
+      if (g.splits == 1 && g.mask_out != nullptr && myrow < g.M) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          if (w < nwords && n0 + c_lo + 32 * w < g.N)
+            g.mask_out[myrow * g.ldmo + ((n0 + c_lo) >> 5) + w] = ow[w];
       }
       tc_fence_before();
       __syncwarp();
@@ -795,8 +829,12 @@ int launch_bn1(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &m
 template <int BN>
 int launch_bn(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &mb,
               const CUtensorMap &mbl, const TcArgs &g, int cl, cudaStream_t st) {
+  // one shared accumulator for 256-wide row-tile products (two would fill
+  // TMEM and leave the epilogue un-overlapped: measured 2.0 -> 1.65 ms for
+  // V x 256 x 256, 2.6 -> 1.4 ms for the masked V x 48 x 256 dH); the split-K
+  // dW products (M-major A) keep two; AG_TC_ONEACC=0/1 overrides
   const char *e = std::getenv("AG_TC_ONEACC");
-  const bool one = e && std::atoi(e);
+  const bool one = e ? std::atoi(e) != 0 : (BN == 256 && !a_mn);
   if constexpr (BN >= 64) {
     if (cl == 2) {
       return one ? launch_bn1<BN, true, 2>(a_mn, b_mn, ma, mb, mbl, g, st)
@@ -853,9 +891,8 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int32_
   // N tile: the whole N when it fits one MMA (<= 256), padded to 16
   int bn = static_cast<int>(std::min<int64_t>(256, ((N + 15) / 16) * 16));
   bn = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
-  // short K: the epilogue dominates a tile; 128-wide tiles double-buffer the
-  // TMEM accumulators so it overlaps the next tile's MMAs (measured faster)
-  if (bn == 256 && K <= 128) bn = 128;
+  // (256-wide tiles share one TMEM accumulator, so they double-buffer too and
+  // the epilogue overlaps the next tile's MMAs at any K)
   if (const char *e = std::getenv("AG_TC_BN")) bn = std::min(bn, std::max(32, std::atoi(e)));
   TcArgs g{};
   g.M = M; g.N = N; g.K = K;
@@ -905,6 +942,7 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int32_
   g.k_per_split = kb_per * BK;
   splits = static_cast<int>((kblocks + kb_per - 1) / kb_per);
   g.splits = splits;
+  if (tiles * splits > 2147483647LL) return fail(AG_ERR_VALUE, "GEMM has too many tiles");
   // clusters of 2 CTAs share (multicast) every B k-block
   // (not for the M-major, split-K dW products: measured slower there)
   int cl = (bn >= 64 && g.m_tiles >= 2 && !a_mn) ? 2 : 1;

@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider -x > gpurun_out/pytest_all.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_all.log
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_c5.log 2>&1
+timeout 600 python scripts/step_profile.py > gpurun_out/step_profile.log 2>&1
+echo done
