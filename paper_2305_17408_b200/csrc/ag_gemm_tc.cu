@@ -45,7 +45,10 @@ constexpr int BM = 128;
 // fp32 elements per k-block: one 128-byte swizzle row (SWIZZLE_128B).  BK = 16
 // (SWIZZLE_64B, 4 stages of 48 KB) also works and was measured: no faster for
 // K = 256 and slower for short K (twice the per-k-block barrier round trips).
-constexpr int BK = 32;
+#ifndef AG_TC_BK
+#define AG_TC_BK 32
+#endif
+constexpr int BK = AG_TC_BK;
 constexpr int kKRow = BK * 4;                       // bytes per K-major row
 constexpr uint64_t kKLayout = BK == 32 ? 2ull : 4ull;  // SWIZZLE_128B / SWIZZLE_64B
 constexpr uint32_t kKSbo = 8 * kKRow;               // 8-row swizzle atom
@@ -121,6 +124,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
         : "r"(su32(b)), "r"(parity), "r"(kWaitHintNs)
+        : "memory");
+  }
+}
+// Spin wait for the single-thread critical path (TMA producer, MMA issuer).
+__device__ __forceinline__ void mbar_wait_spin(uint64_t *b, uint32_t parity) {
+  uint32_t done = 0;
+  uint32_t spins = 0;
+  while (!done) {
+    if (++spins > (1u << 26)) __trap();
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(su32(b)), "r"(parity)
         : "memory");
   }
 }
@@ -367,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int64_t k0;
         const int nkb = tile_kblocks(t, k0);
         for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_spin(&empty[stage], phase ^ 1);
           unsigned char *st = smem + stage * C::STAGE;
           unsigned char *sa = st, *sb = st + 2 * C::A_BYTES;
           if (g.exp & 32) {  // experiment: no operand traffic, handoffs only
@@ -421,14 +438,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ti = static_cast<int>(static_cast<uint32_t>(t - cid) / static_cast<uint32_t>(ncl));
       const bool tr = g.trace != nullptr && blockIdx.x == 0 && lane == 0 && ti < kTraceTiles;
       if (tr) g.trace[ti * 10 + 0] = gtime();
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      mbar_wait_spin(&tempty[acc], acc_phase ^ 1);
       if (tr) g.trace[ti * 10 + 1] = gtime();
       tc_fence_after();
       const uint32_t d = tmem_base + static_cast<uint32_t>(acc * C::NACC * BN);  // hi*hi
       const uint32_t dc = ONE ? d : d + BN;                                     // correction
       for (int kb = 0; kb < nkb; ++kb) {
         if (tr && kb < 2) g.trace[ti * 10 + 6 + 2 * kb] = gtime();
-        mbar_wait(&conv[stage], phase);
+        mbar_wait_spin(&conv[stage], phase);
         if (tr && kb < 2) g.trace[ti * 10 + 7 + 2 * kb] = gtime();
         tc_fence_after();
         if (lane == 0) {
@@ -909,8 +926,11 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int32_
   g.bdiag = bdiag;
   if (const char *e = std::getenv("AG_TC_EXP")) g.exp = std::atoi(e);
   {
+    // raw hi by default: the MMA reads only an fp32 operand's top 19 bits, so
+    // the splitters need not write the masked hi half back (a third less
+    // shared-memory traffic in the split; bitwise equal, tests/test_slab_gpu.py)
     const char *rh = std::getenv("AG_TC_RAWHI");
-    g.raw_hi = rh ? std::atoi(rh) : 0;
+    g.raw_hi = rh ? std::atoi(rh) : 1;
   }
   g.m_tiles = static_cast<int>((M + BM - 1) / BM);
   g.n_tiles = static_cast<int>((N + bn - 1) / bn);

@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gemm_gpu.py tests/test_slab_gpu.py -k "gemm" -q -m gpu -p no:cacheprovider -x > gpurun_out/pytest_gemm.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gemm.log
+timeout 300 python scripts/gemm_epi.py > gpurun_out/gemm_epi4.log 2>&1
+timeout 300 python scripts/gemm_kerr.py > gpurun_out/gemm_kerr4.log 2>&1
+echo done

@@ -127,6 +127,14 @@ def test_gemm_raw_hi_is_bitwise_masked_split(monkeypatch):
     want = K.gemm(a, b)
     monkeypatch.setenv("AG_TC_RAWHI", "1")
     assert torch.equal(K.gemm(a, b), want)
+    # a dW-shaped product (both operands split in shared memory, split K)
+    h = torch.from_numpy(rng.standard_normal((300000, 64)).astype(np.float32)).cuda()
+    g = torch.from_numpy(rng.standard_normal((300000, 48)).astype(np.float32)).cuda()
+    assert g.numel() > K.PRESPLIT_MAX_ELEMS
+    monkeypatch.setenv("AG_TC_RAWHI", "0")
+    want = K.gemm(h, g, trans_a=True)
+    monkeypatch.setenv("AG_TC_RAWHI", "1")
+    assert torch.equal(K.gemm(h, g, trans_a=True), want)
 
 
 @pytest.mark.parametrize("F", [64, 100, 256])
