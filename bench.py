@@ -217,7 +217,9 @@ def run_ours(args, cfg):
         dnet = D.DistGNN.build(cfg["model"], dims, dec, rank, world, seed=0,
                                subject_t=net.subject_t)
         r0, r1 = dnet.bounds[rank], dnet.bounds[rank + 1]
-        choices = {("fwd", 0): (ag.KernelKind.CSR_INTRA_BLOCKED, ag.KernelKind.CSR_INTER)}
+        names = {"csr": (ag.KernelKind.CSR_INTRA_BLOCKED, ag.KernelKind.CSR_INTER),
+                 "dense_coo": (ag.KernelKind.DENSE_BLOCK, ag.KernelKind.COO_ATOMIC)}
+        choices = {k: names[v] for k, v in dnet.autotune().items()}
         x_local = x[r0:r1].contiguous()
         labels = torch.from_numpy(labels_np[r0:r1]).cuda()
         mask = torch.from_numpy(mask_np[r0:r1]).cuda()
@@ -231,8 +233,11 @@ def run_ours(args, cfg):
             return dnet.train_step(dnet.input_ext(xd), ld, md, n_mask, lr)
         timed = dnet
         host_x = x_local
-        halo = {"fwd_halo_rows_per_rank": dnet.fwd.plan.max_send,
-                "bwd_halo_rows_per_rank": dnet.bwd.plan.max_send,
+        fst, bst = dnet.fwd.plan.stats(), dnet.bwd.plan.stats()
+        halo = {"fwd_halo_rows": fst["halo_rows"], "bwd_halo_rows": bst["halo_rows"],
+                "fwd_allgather_rows_avoided": fst["allgather_rows"],
+                "exchange": "per-peer uneven all-to-all (exact halo), backward exchange "
+                            "overlapped with the dW GEMM",
                 "rows_per_rank": r1 - r0}
     else:
         labels = torch.from_numpy(labels_np).cuda()
@@ -416,7 +421,7 @@ def run_ours(args, cfg):
             "launch": "each timed step replays the training step as one CUDA graph "
                       "(GraphedTrainStep); per-aggregation timings from an eager pass"
                       if use_graph else "eager launches, per-aggregation CUDA events in-step",
-            "parallelism": f"row-partition x{world} (NCCL halo all-gather + dW all-reduce)"
+            "parallelism": f"row-partition x{world} (NCCL per-peer halo all-to-all + dW all-reduce)"
                            if world > 1 else "single GPU",
             **({"halo": halo} if halo else {}),
         },

@@ -1,5 +1,5 @@
-"""Multi-GPU host logic on CPU: world-size-2 gloo processes run the real
-partition / send-set / remap / all-gather code of paper_2305_17408_b200.dist
+"""Multi-GPU host logic on CPU: world-size-2 and -4 gloo processes run the real
+partition / peer-set / remap / all-to-all code of paper_2305_17408_b200.dist
 on CPU tensors, with the oracle's numpy CSR aggregation standing in for the
 device kernel.  Every rank's local aggregation over its halo-extended features
 must be BITWISE equal to its rows of the global aggregation,
@@ -85,9 +85,15 @@ def _worker(rank, world, port, out):
                                     role_val=torch.from_numpy(rval))
         ext_to_global = np.full(plan.ext_rows, -1, np.int64)
         ext_to_global[:plan.n_local] = np.arange(r0, r1)
-        for j, S in enumerate(plan.sets):
-            base = plan.halo_base + j * plan.max_send
+        for j, S in enumerate(plan.recv_sets):
+            base = plan.halo_base + plan.recv_offsets[j]
             ext_to_global[base:base + S.numel()] = S.numpy()
+        # exact halo: every received row is referenced by this rank's edges
+        lcol = op.col.numpy().astype(np.int64)
+        used = np.unique(lcol[lcol >= plan.halo_base])
+        exact = bool(used.size == plan.ext_rows - plan.halo_base
+                     and np.array_equal(x_ext.numpy()[plan.halo_base:],
+                                        x[ext_to_global[plan.halo_base:]]))
         e0, e1 = rp[r0], rp[r1]
         role_ok = bool(np.array_equal(ext_to_global[rop.col.numpy()], rcol[e0:e1])
                        and np.array_equal(rop.mid.numpy() + e0, mid[r0:r1]))
@@ -97,20 +103,24 @@ def _worker(rank, world, port, out):
         dist.all_reduce(part)
         dw_ok = bool(np.allclose(part.numpy(), x.T.astype(np.float64) @ g.astype(np.float64),
                                  rtol=1e-12, atol=1e-12))
-        halo_frac = plan.max_send / max(1, plan.n_local)
-        out[rank] = (bitwise, role_ok, dw_ok, plan.n_local, halo_frac)
+        st = plan.stats()
+        halo_frac = st["halo_rows"] / max(1, plan.n_local)
+        out[rank] = (bitwise, role_ok, dw_ok, plan.n_local, halo_frac, exact,
+                     st["halo_rows"] <= st["allgather_rows"])
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 4])
 def test_row_partition_halo_exchange_gloo(world):
     out = mp.Manager().dict()
     mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     assert sorted(out.keys()) == list(range(world))
     for rank in range(world):
-        bitwise, role_ok, dw_ok, n_local, halo_frac = out[rank]
+        bitwise, role_ok, dw_ok, n_local, halo_frac, exact, leq = out[rank]
         assert bitwise, f"rank {rank}: local aggregation differs from the global rows"
+        assert exact, f"rank {rank}: the halo holds rows nobody references, or wrong rows"
+        assert leq, f"rank {rank}: per-peer halo larger than the padded all-gather"
         assert role_ok, f"rank {rank}: role-ordered remap"
         assert dw_ok, f"rank {rank}: dW all-reduce"
         assert n_local > 0 and halo_frac < 0.5
