@@ -91,6 +91,7 @@ struct TcArgs {
   // block-diagonal product (ag_block_diag_gemm_tf32x3): the B operand's K rows
   // of output tile m0 start at the panel base (m0 / bdiag) * bdiag; 0 = plain GEMM
   int64_t bdiag;
+  int c_tma;            // 1: tmC maps C (direct products): the epilogue stores by TMA
   long long *trace;     // AG_TC_TRACE: per-tile clock stamps of CTA 0 (development only)
 };
 constexpr int kTraceTiles = 48;
@@ -160,6 +161,25 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
       : "memory");
+}
+// TMA tensor store of a 32 x 32 fp32 box from shared memory (bulk group)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 // the same load delivered to the same shared-memory offset (and mbarrier) of
 // every CTA in `mask` of the cluster
@@ -303,18 +323,21 @@ template <int BN, bool A_MN, bool B_MN, bool ONE, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmBl, TcArgs g) {
+                   const __grid_constant__ CUtensorMap tmBl,
+                   const __grid_constant__ CUtensorMap tmC, TcArgs g) {
   using C = Cfg<BN, ONE>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE);
+  // epilogue staging buffers first (1024-byte aligned: the TMA store's 128B
+  // swizzle is a function of the absolute shared address), then the barriers
+  unsigned char *epi_buf = smem + C::STAGES * C::STAGE;  // C::EPI bytes
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE + C::EPI);
   uint64_t *conv = full + C::STAGES;
   uint64_t *empty = conv + C::STAGES;
   uint64_t *tfull = empty + C::STAGES;  // [2]
   uint64_t *tempty = tfull + 2;         // [2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-  unsigned char *epi_buf = smem + C::STAGES * C::STAGE + 256;  // C::EPI bytes
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // cluster tiles: CL consecutive M tiles x one N tile x one K split
@@ -575,6 +598,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // reads and stores).
       const uint32_t xb = su32(epi_buf) + static_cast<uint32_t>(warp - kEpiWarp0) * (32 * 32 * 4);
       const int rsub = lane >> 3, j4 = lane & 7;  // read-back role: row rsub + 4 i, chunk j4
+      // TMA-store epilogue: direct products without a C read (beta = 0)
+      const bool fast = g.c_tma && direct && g.beta == 0.0f && !(g.exp & 12);
 #pragma unroll 1
       for (int c = c_lo; c < c_hi; c += 32) {
         const int cw = (c - c_lo) >> 5;
@@ -592,6 +617,42 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 32; ++i)
             v[i] = ONE ? __uint_as_float(rh[i])
                        : __fadd_rn(__uint_as_float(rh[i]), __uint_as_float(rc[i]));
+        }
+        if (fast) {
+          // lane = row: alpha / ReLU / the row's backward-mask bits and its
+          // forward-mask word in registers, then the 32 x 32 chunk goes out
+          // as one TMA tensor store from the (128B-swizzled) shared buffer
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            float r = g.alpha == 1.0f ? v[i] : g.alpha * v[i];
+            if (g.relu) r = fmaxf(r, 0.0f);
+            if (g.mask != nullptr && !((mwc >> i) & 1u)) r = 0.0f;
+            v[i] = r;
+          }
+          if (g.mask_out != nullptr) {
+            uint32_t wd = 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) wd |= (v[i] > 0.0f ? 1u : 0u) << i;
+            if (cw == 0) ow[0] = wd;
+            else if (cw == 1) ow[1] = wd;
+            else if (cw == 2) ow[2] = wd;
+            else ow[3] = wd;
+          }
+          if (lane == 0) bulk_wait_read0();  // the previous chunk's store has read xb
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             xb + lane * 128 + ((j ^ (lane & 7)) * 16)),
+                         "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                         : "memory");
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, xb, static_cast<int>(n0 + c), static_cast<int>(m0 + q * 32));
+            bulk_commit();
+          }
+          continue;
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -736,6 +797,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (warp >= kEpiWarp0 && lane == 0) bulk_wait0();  // the TMA stores have completed
   tc_fence_before();
   __syncthreads();
   if (CL > 1) cluster_sync();  // no CTA leaves while a peer may still signal / write it
@@ -806,8 +868,8 @@ int make_map(CUtensorMap *m, const float *base, int64_t inner, int64_t outer, in
 }
 
 template <int BN, bool A_MN, bool B_MN, bool ONE, int CL>
-int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbl, TcArgs g,
-              cudaStream_t st) {
+int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbl,
+              const CUtensorMap &mc, TcArgs g, cudaStream_t st) {
   using C = Cfg<BN, ONE>;
   auto k = tc_gemm_kernel<BN, A_MN, B_MN, ONE, CL>;
   AG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -815,7 +877,7 @@ int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &m
   const int64_t total = msup * g.n_tiles * g.splits;
   const int grid = static_cast<int>(std::min<int64_t>(total, sm_count() / CL)) * CL;
   if (CL == 1) {
-    k<<<grid, kThreads, C::SMEM, st>>>(ma, mb, mbl, g);
+    k<<<grid, kThreads, C::SMEM, st>>>(ma, mb, mbl, mc, g);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -829,7 +891,7 @@ int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &m
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    AG_CUDA(cudaLaunchKernelEx(&cfg, k, ma, mb, mbl, g));
+    AG_CUDA(cudaLaunchKernelEx(&cfg, k, ma, mb, mbl, mc, g));
   }
   AG_LAUNCH_CHECK("tc_gemm_kernel");
   return AG_OK;
@@ -837,15 +899,16 @@ int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &m
 
 template <int BN, bool ONE, int CL>
 int launch_bn1(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &mb,
-               const CUtensorMap &mbl, const TcArgs &g, cudaStream_t st) {
-  if (!a_mn && b_mn) return launch_tc<BN, false, true, ONE, CL>(ma, mb, mbl, g, st);
-  if (!a_mn && !b_mn) return launch_tc<BN, false, false, ONE, CL>(ma, mb, mbl, g, st);
-  if (a_mn && b_mn) return launch_tc<BN, true, true, ONE, CL>(ma, mb, mbl, g, st);
-  return launch_tc<BN, true, false, ONE, CL>(ma, mb, mbl, g, st);
+               const CUtensorMap &mbl, const CUtensorMap &mc, const TcArgs &g, cudaStream_t st) {
+  if (!a_mn && b_mn) return launch_tc<BN, false, true, ONE, CL>(ma, mb, mbl, mc, g, st);
+  if (!a_mn && !b_mn) return launch_tc<BN, false, false, ONE, CL>(ma, mb, mbl, mc, g, st);
+  if (a_mn && b_mn) return launch_tc<BN, true, true, ONE, CL>(ma, mb, mbl, mc, g, st);
+  return launch_tc<BN, true, false, ONE, CL>(ma, mb, mbl, mc, g, st);
 }
 template <int BN>
 int launch_bn(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &mb,
-              const CUtensorMap &mbl, const TcArgs &g, int cl, cudaStream_t st) {
+              const CUtensorMap &mbl, const CUtensorMap &mc, const TcArgs &g, int cl,
+              cudaStream_t st) {
   // one shared accumulator for 256-wide row-tile products (two would fill
   // TMEM and leave the epilogue un-overlapped: measured 2.0 -> 1.65 ms for
   // V x 256 x 256, 2.6 -> 1.4 ms for the masked V x 48 x 256 dH); the split-K
@@ -854,12 +917,12 @@ int launch_bn(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &mb
   const bool one = e ? std::atoi(e) != 0 : (BN == 256 && !a_mn);
   if constexpr (BN >= 64) {
     if (cl == 2) {
-      return one ? launch_bn1<BN, true, 2>(a_mn, b_mn, ma, mb, mbl, g, st)
-                 : launch_bn1<BN, false, 2>(a_mn, b_mn, ma, mb, mbl, g, st);
+      return one ? launch_bn1<BN, true, 2>(a_mn, b_mn, ma, mb, mbl, mc, g, st)
+                 : launch_bn1<BN, false, 2>(a_mn, b_mn, ma, mb, mbl, mc, g, st);
     }
   }
-  return one ? launch_bn1<BN, true, 1>(a_mn, b_mn, ma, mb, mbl, g, st)
-             : launch_bn1<BN, false, 1>(a_mn, b_mn, ma, mb, mbl, g, st);
+  return one ? launch_bn1<BN, true, 1>(a_mn, b_mn, ma, mb, mbl, mc, g, st)
+             : launch_bn1<BN, false, 1>(a_mn, b_mn, ma, mb, mbl, mc, g, st);
 }
 
 __global__ void tf32_split_lo_kernel(int64_t n, const float *src, float *lo) {
@@ -1002,6 +1065,23 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int32_
     g.C = C;
     g.ldc = ldc;
   }
+  // C as a TMA tensor (box 32 x 32, 128-byte swizzle = the epilogue's staging
+  // layout) for direct products: the epilogue stores its chunks by TMA
+  CUtensorMap mc = mb;
+  g.c_tma = 0;
+  if (g.split_mode == 0 && splits == 1 && (reinterpret_cast<uintptr_t>(C) & 15) == 0 &&
+      ldc % 4 == 0 && std::getenv("AG_TC_NO_CTMA") == nullptr) {
+    EncodeFn enc = encode_fn();
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldc) * 4};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t es[2] = {1, 1};
+    if (enc && enc(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      g.c_tma = 1;
+  }
   long long *trace = nullptr;
   if (std::getenv("AG_TC_TRACE")) {
     AG_CUDA(cudaMalloc(&trace, kTraceTiles * 10 * sizeof(long long)));
@@ -1009,10 +1089,10 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int32_
     g.trace = trace;
   }
   switch (bn) {
-    case 32: rc = launch_bn<32>(a_mn, b_mn, ma, mb, mbl, g, cl, st); break;
-    case 64: rc = launch_bn<64>(a_mn, b_mn, ma, mb, mbl, g, cl, st); break;
-    case 128: rc = launch_bn<128>(a_mn, b_mn, ma, mb, mbl, g, cl, st); break;
-    default: rc = launch_bn<256>(a_mn, b_mn, ma, mb, mbl, g, cl, st); break;
+    case 32: rc = launch_bn<32>(a_mn, b_mn, ma, mb, mbl, mc, g, cl, st); break;
+    case 64: rc = launch_bn<64>(a_mn, b_mn, ma, mb, mbl, mc, g, cl, st); break;
+    case 128: rc = launch_bn<128>(a_mn, b_mn, ma, mb, mbl, mc, g, cl, st); break;
+    default: rc = launch_bn<256>(a_mn, b_mn, ma, mb, mbl, mc, g, cl, st); break;
   }
   if (rc) return rc;
   if (trace) {
