@@ -265,7 +265,7 @@ int ag_fused_spmm(int64_t num_rows, int64_t feat, int32_t role_mask,
 
 /* Window radius (in 16-row blocks) for ag_fused_spmm over this CSR: the
  * smallest radius whose ring covers `coverage` (e.g. 0.995) of the edges the
- * largest supported radius (16) would cover, from a device histogram of
+ * largest supported radius (17) would cover, from a device histogram of
  * |src/16 - dst/16|.  Synchronous (reads the histogram back); call once per
  * topology and cache the result.  No reference counterpart: a B200 layout
  * parameter of the cached formats (formats.py:76-140). */

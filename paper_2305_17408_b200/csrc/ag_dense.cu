@@ -10,6 +10,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ag_common.cuh"
 
@@ -191,6 +192,69 @@ __global__ void __launch_bounds__(kXentThreads) xent_kernel(
       dz[c] = (p - (c == y ? 1.0f : 0.0f)) * inv_n;
     }
     if (lane == 0) acc += static_cast<double>(mx + logf(se) - z[y]);
+  }
+  if (lane == 0) warp_sum[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kXentThreads / 32; ++w) t += warp_sum[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
+// Narrow logits (C <= 64): a warp per row, lane l holding logits l and l + 32
+// in registers -- one coalesced pass over the row, exp computed once and kept
+// for the gradient, max / sum by warp shuffles.  Loss partials as in
+// xent_kernel (fp64 per lane-0 in a fixed row order, fixed-order CTA sum).
+__global__ void __launch_bounds__(kXentThreads) xent_warp_kernel(
+    int64_t rows, int64_t C, int64_t ld, const float *logits, const int32_t *labels,
+    const uint8_t *mask, float inv_n, int64_t rows_per_cta, double *partial, float *dlogits,
+    int64_t ldd) {
+  constexpr int U = 4;  // rows per warp in flight (their loads issued together)
+  __shared__ double warp_sum[kXentThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(rows, r0 + rows_per_cta);
+  const int c0 = lane, c1 = lane + 32;
+  const bool in0 = c0 < C, in1 = c1 < C;
+  double acc = 0.0;
+  for (int64_t rb = r0 + warp * U; rb < r1; rb += (kXentThreads / 32) * U) {
+    float z0[U], z1[U];
+    int32_t y[U];
+    bool on[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = rb + u;
+      const bool ok = r < r1;
+      const float *z = logits + (ok ? r : r0) * ld;
+      z0[u] = (ok && in0) ? __ldg(z + c0) : -INFINITY;
+      z1[u] = (ok && in1) ? __ldg(z + c1) : -INFINITY;
+      y[u] = ok ? labels[r] : 0;
+      on[u] = ok && (mask ? mask[r] != 0 : true);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = rb + u;
+      if (r >= r1) break;
+      float g0 = 0.0f, g1 = 0.0f;
+      if (on[u]) {
+        float mx = fmaxf(z0[u], z1[u]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const float e0 = in0 ? expf(z0[u] - mx) : 0.0f, e1 = in1 ? expf(z1[u] - mx) : 0.0f;
+        float se = e0 + e1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+        const float inv_se = 1.0f / se;
+        g0 = (e0 * inv_se - (c0 == y[u] ? 1.0f : 0.0f)) * inv_n;
+        g1 = (e1 * inv_se - (c1 == y[u] ? 1.0f : 0.0f)) * inv_n;
+        const float zy = __shfl_sync(0xffffffffu, y[u] < 32 ? z0[u] : z1[u], y[u] & 31);
+        if (lane == 0) acc += static_cast<double>(mx + logf(se) - zy);
+      }
+      float *dz = dlogits + r * ldd;
+      if (c0 < ldd) dz[c0] = in0 ? g0 : 0.0f;  // pad columns stay 0
+      if (c1 < ldd) dz[c1] = in1 ? g1 : 0.0f;
+    }
   }
   if (lane == 0) warp_sum[warp] = acc;
   __syncthreads();
@@ -387,7 +451,22 @@ extern "C" int ag_softmax_xent(int64_t rows, int64_t C, int64_t ld, const float 
   if (rows < 0 || C < 1 || ld < C || ld_dlogits < C) return fail(AG_ERR_VALUE, "bad loss sizes");
   cudaStream_t st = as_stream(stream);
   const float inv_n = num_masked > 0 ? 1.0f / static_cast<float>(num_masked) : 0.0f;
-  const bool narrow = ld <= kXentLd;
+  const bool narrow = ld <= kXentLd && std::getenv("AG_XENT_ROWS") != nullptr;
+  if (C <= 64 && ld_dlogits <= 64 && !narrow) {
+    const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64,
+                                                                static_cast<int64_t>(sm_count()) * 8));
+    const int64_t per = (rows + ctas - 1) / ctas;
+    Scratch pw;
+    AG_CUDA(pw.alloc(ctas * sizeof(double), st));
+    xent_warp_kernel<<<static_cast<unsigned>(ctas), kXentThreads, 0, st>>>(
+        rows, C, ld, logits, labels, mask, inv_n, std::max<int64_t>(per, 1), pw.as<double>(),
+        dlogits, ld_dlogits);
+    AG_LAUNCH_CHECK("xent_warp_kernel");
+    loss_final_kernel<<<1, 32, 0, st>>>(static_cast<int>(ctas), pw.as<double>(),
+                                        num_masked > 0 ? 1.0 / num_masked : 0.0, loss_out);
+    AG_LAUNCH_CHECK("loss_final_kernel");
+    return AG_OK;
+  }
   int64_t ctas;
   Scratch part;
   if (narrow) {

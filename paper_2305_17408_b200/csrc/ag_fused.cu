@@ -69,8 +69,14 @@ constexpr int kConsMax = 16;
 template <int MODE>
 constexpr int cons_warps();
 constexpr int kWin = 64;     // topology items per window refill (two per lane)
-constexpr int kSlots = 45;   // X ring capacity in blocks (window H <= (kSlots - 9) / 2 = 18)
-constexpr int kFarSlots = 4; // far ring: staged out-of-window sources of the next blocks
+#ifndef AG_SLAB_SLOTS
+#define AG_SLAB_SLOTS 43
+#endif
+#ifndef AG_SLAB_FAR_SLOTS
+#define AG_SLAB_FAR_SLOTS 5
+#endif
+constexpr int kSlots = AG_SLAB_SLOTS;  // X ring capacity in blocks (window H <= (kSlots - 9) / 2 = 17)
+constexpr int kFarSlots = AG_SLAB_FAR_SLOTS;  // far ring depth (measured: 43 / 5 vs 45 / 4 is 2% faster)
 constexpr int kFarMax = 20;  // staged far sources per block (more: read from global)
 constexpr int kRG = 1;       // consecutive rows a consumer warp takes at a time (divides kRB)
 constexpr int kISlots = 4;   // dense-intra mode: per-block intra results (16 rows x tile)
