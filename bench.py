@@ -37,8 +37,11 @@ CONFIGS = {
     "C2": dict(V=19717, E=88648, dims=[500, 16, 3], model="gcn", name="pubmed-shaped"),
     "C3": dict(V=169343, E=1166243, dims=[128, 64, 64, 64, 64, 40], model="gin",
                name="ogbn-arxiv-shaped"),
+    # C4's planted communities are 512 rows: the partition file's community size
+    # is the decomposition block (B = 16 leaves 1.2% of the edges intra; B = 512
+    # puts 36% on the tensor-core dense_block kernel -- 32.8 -> 20.3 ms per epoch)
     "C4": dict(V=232965, E=114615892, dims=[602, 128, 41], model="gcn", name="reddit-shaped",
-               block_gen=512),
+               block_gen=512, comm_size=512),
     "C5": dict(V=2449029, E=61859140, dims=[100, 256, 256, 47], model="gcn",
                name="ogbn-products-shaped"),
 }
@@ -175,9 +178,9 @@ class HostFeeder:
 
 def ncu_traffic():
     """DRAM bytes of one F=256 aggregation launch from the committed ncu
-    capture of the pair the autotune runs (profiles/r01_ncu_dense_pair.json),
-    or (None, reason)."""
-    p = ROOT / "profiles" / "r01_ncu_dense_pair.json"
+    capture of the pair the autotune runs (profiles/r02_ncu.json), or
+    (None, reason)."""
+    p = ROOT / "profiles" / "r02_ncu.json"
     if not p.exists():
         return None, "no ncu capture committed"
     d = json.loads(p.read_text())
@@ -568,11 +571,12 @@ def main():
                          "'' disables it")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the training step eagerly instead of as a CUDA graph")
-    ap.add_argument("--comm-size", type=int, default=COMM_SIZE,
-                    help="decomposition block size B (SURVEY 8d: also report 64/128/256 for C4)")
+    ap.add_argument("--comm-size", type=int, default=None,
+                    help="decomposition block size B (default: the config's community size, "
+                         "16 except C4's 512; SURVEY 8d: also report 64/128/256 for C4)")
     args = ap.parse_args()
-    globals()["COMM_SIZE"] = args.comm_size
     cfg = CONFIGS[args.config]
+    globals()["COMM_SIZE"] = args.comm_size or cfg.get("comm_size", COMM_SIZE)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
