@@ -66,6 +66,14 @@ constexpr int kRB = 16;      // rows per ring block
 // registers: with the intra role on the dense warps (kModeDense3Coo) the consumers run
 // 16 + 2 warps at 96 registers (measured faster; the exact-order code spills there)
 constexpr int kConsMax = 16;
+#ifndef AG_SLAB_COO_CONS
+#define AG_SLAB_COO_CONS 14
+#endif
+// dense + coo: consumer warps (+ 2 dense warps), rows round-robin.  Measured at
+// C5 F = 256: 8 / 10 / 12 / 14 warps 6.13 / 5.35 / 4.74 / 4.56 ms; 16 warps each
+// owning one row of every block (no per-row block bookkeeping) 4.92 ms
+constexpr int kCooCons = AG_SLAB_COO_CONS;
+static_assert(kCooCons <= kConsMax, "consumer windows");
 template <int MODE>
 constexpr int cons_warps();
 constexpr int kWin = 64;     // topology items per window refill (two per lane)
@@ -651,7 +659,7 @@ constexpr int kModeDense3Coo = 5;
 __host__ __device__ constexpr bool mode_dense(int m) { return m == kModeDense3 || m == kModeDense3Coo; }
 __host__ __device__ constexpr bool mode_coo(int m) { return m == kModeSum3Coo || m == kModeDense3Coo; }
 template <int MODE>
-constexpr int cons_warps() { return MODE == kModeDense3Coo ? kConsMax : 14; }
+constexpr int cons_warps() { return MODE == kModeDense3Coo ? kCooCons + 2 : 14; }
 __host__ __device__ constexpr bool mode_sum3(int m) {
   return m == kModeSum3 || m == kModeDense3 || mode_coo(m);
 }
@@ -1812,7 +1820,7 @@ int launch_slab(GArgs a, int mode, int window, cudaStream_t st) {
   };
   if (a.feat % 4 == 0 && env_int("AG_SLAB_NO_TMA", 0) == 0 && encode(&map, a.x, a.x_rows))
     a.tma = 1;
-  const int threads = (mode == kModeDense3Coo ? kConsMax : 14) * 32 + 64;
+  const int threads = (mode == kModeDense3Coo ? kCooCons + 2 : 14) * 32 + 64;
   long long *trace = nullptr;
   if (std::getenv("AG_SLAB_TRACE")) {
     AG_CUDA(cudaMalloc(&trace, kTraceBlocks * 8 * sizeof(long long)));
