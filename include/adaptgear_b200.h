@@ -187,6 +187,15 @@ int ag_csr_intra_spmm(int64_t num_rows, int64_t feat, int64_t block_size,
 int ag_coo_spmm(int64_t num_rows, int64_t feat, int64_t num_edges,
                 const int32_t *row, const int32_t *col, const float *val,
                 const float *x, float *y, int32_t op, void *stream);
+/* coo_atomic (kernels.py:192-225) for sum / mean partials as a row gather:
+ * the COO is dst-sorted, so row_ptr[num_rows + 1] (ag_build_row_ptr of its
+ * rows) delimits each destination's edge run; a sub-warp per row gathers the
+ * sources (8 loads in flight) and writes y[r] = sum of val * x[col] in an
+ * unspecified order (the reference's order is open too; tested at 1e-4), with
+ * no atomics.  y rows without edges are written 0.  val NULL: weights 1.0. */
+int ag_coo_gather_spmm(int64_t num_rows, int64_t feat, const int32_t *row_ptr,
+                       const int32_t *col, const float *val, const float *x, float *y,
+                       void *stream);
 
 /* K4 aggregate_dense_block (kernels.py:228-250): for every B-row community c
  * with slot k = comm_slot[c] >= 0: Y[cB:cB+B] = blocks[k] @ X[cB:cB+B]

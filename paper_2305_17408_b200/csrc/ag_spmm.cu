@@ -365,6 +365,67 @@ __global__ void __launch_bounds__(kBlock) coo_spmm_kernel(CooArgs a) {
   }
 }
 
+// ------------------------------------- K3 as a row gather (sum / mean) -----
+// coo_atomic leaves the summation order open (the reference accumulates in
+// fp64 bincount over scrambled edges, kernels.py:192-225, tested at 1e-4), and
+// its COO is dst-sorted, so each destination's edges are one contiguous run.
+// LANES lanes own a row (VEC columns each), load its (col, val) run LANES at a
+// time coalesced, and gather 8 source rows per step with all 8 loads in flight,
+// accumulating in registers: no atomics, one store per row.  For graphs whose
+// sources are far apart (C4: every row reads ~300 rows spread over 16k) this is
+// an L2 gather; the atomic kernel below stays for max.
+template <int VEC, int LANES>
+__global__ void __launch_bounds__(kBlock) coo_gather_kernel(int64_t rows, int64_t feat,
+                                                            const int32_t *row_ptr,
+                                                            const int32_t *col, const float *val,
+                                                            const float *x, float *y) {
+  const int sub = threadIdx.x & 31;
+  const int lane = sub % LANES;
+  const unsigned gmask =
+      LANES == 32 ? 0xffffffffu : (((1u << LANES) - 1u) << (sub / LANES * LANES));
+  const int64_t grp = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / LANES;
+  const int64_t ngrp = static_cast<int64_t>(gridDim.x) * (kBlock / LANES);
+  const int tile = LANES * VEC;
+  for (int64_t r = grp; r < rows; r += ngrp) {
+    const int32_t s = __ldg(row_ptr + r), e = __ldg(row_ptr + r + 1);
+    for (int f0 = 0; f0 < feat; f0 += tile) {
+      const int64_t f = f0 + lane * VEC;
+      const bool act = f < feat;
+      Vf<VEC> a0 = splat<VEC>(0.0f), a1 = a0;
+      for (int32_t b = s; b < e; b += LANES) {
+        int32_t mc = 0;
+        float mv = 0.0f;
+        if (b + lane < e) {
+          mc = __ldg(col + b + lane);
+          mv = val ? __ldg(val + b + lane) : 1.0f;
+        }
+        const int n = e - b < LANES ? e - b : LANES;
+        for (int j = 0; j < n; j += 8) {
+          Vf<VEC> xv[8];
+          float w[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int jj = j + u;
+            const int32_t c = __shfl_sync(gmask, mc, jj, LANES);
+            w[u] = __shfl_sync(gmask, mv, jj, LANES);
+            xv[u] = (jj < n && act) ? ldv<VEC>(x + static_cast<int64_t>(c) * feat + f)
+                                    : splat<VEC>(0.0f);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (j + u < n) {
+              Vf<VEC> &acc = (u & 1) ? a1 : a0;
+#pragma unroll
+              for (int i = 0; i < VEC; ++i) acc.v[i] = fmaf(xv[u].v[i], w[u], acc.v[i]);
+            }
+          }
+        }
+      }
+      if (act) stv<VEC>(y + r * feat + f, vadd<VEC>(a0, a1));
+    }
+  }
+}
+
 // ---------------------------------------------------- K4: dense blocks -----
 struct DenseArgs {
   int64_t rows;
@@ -467,6 +528,28 @@ int resident_grid(K kernel, size_t smem, int64_t work_blocks) {
   if (work_blocks < g) g = work_blocks;
   if (g < 1) g = 1;
   return static_cast<int>(g);
+}
+
+template <int VEC, int LANES>
+int launch_coo_gather(int64_t rows, int64_t feat, const int32_t *row_ptr, const int32_t *col,
+                      const float *val, const float *x, float *y, cudaStream_t st) {
+  auto k = coo_gather_kernel<VEC, LANES>;
+  const int64_t work = (rows * LANES + kBlock - 1) / kBlock;
+  k<<<resident_grid(k, 0, work), kBlock, 0, st>>>(rows, feat, row_ptr, col, val, x, y);
+  AG_LAUNCH_CHECK("coo_gather_kernel");
+  return AG_OK;
+}
+
+template <int VEC>
+int launch_coo_gather_vec(int64_t rows, int64_t feat, const int32_t *row_ptr,
+                          const int32_t *col, const float *val, const float *x, float *y,
+                          cudaStream_t st) {
+  switch (pick_lanes((feat + VEC - 1) / VEC)) {
+    case 4: return launch_coo_gather<VEC, 4>(rows, feat, row_ptr, col, val, x, y, st);
+    case 8: return launch_coo_gather<VEC, 8>(rows, feat, row_ptr, col, val, x, y, st);
+    case 16: return launch_coo_gather<VEC, 16>(rows, feat, row_ptr, col, val, x, y, st);
+    default: return launch_coo_gather<VEC, 32>(rows, feat, row_ptr, col, val, x, y, st);
+  }
 }
 
 template <int VEC, int LANES>
@@ -664,4 +747,18 @@ extern "C" int ag_combine(int64_t num_rows, int64_t feat, const float *a, const 
       num_rows, feat, a, touched_a, b, touched_b, deg, op, out);
   AG_LAUNCH_CHECK("combine_kernel");
   return AG_OK;
+}
+
+extern "C" int ag_coo_gather_spmm(int64_t num_rows, int64_t feat, const int32_t *row_ptr,
+                                  const int32_t *col, const float *val, const float *x, float *y,
+                                  void *stream) {
+  if (int rc = check_common(num_rows, feat, AG_OP_SUM, 0, nullptr)) return rc;
+  if (num_rows == 0 || feat == 0) return AG_OK;
+  if (row_ptr == nullptr) return fail(AG_ERR_VALUE, "row_ptr is required");
+  cudaStream_t st = as_stream(stream);
+  switch (pick_vec(feat, x, y)) {
+    case 4: return launch_coo_gather_vec<4>(num_rows, feat, row_ptr, col, val, x, y, st);
+    case 2: return launch_coo_gather_vec<2>(num_rows, feat, row_ptr, col, val, x, y, st);
+    default: return launch_coo_gather_vec<1>(num_rows, feat, row_ptr, col, val, x, y, st);
+  }
 }

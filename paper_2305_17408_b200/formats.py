@@ -23,12 +23,23 @@ SLAB_COVERAGE = 0.995
 class CooMatrix:
     """Coordinate-format adjacency sorted by (row, col)."""
 
-    __slots__ = ("num_vertices", "row", "col", "_val", "_ones")
+    __slots__ = ("num_vertices", "row", "col", "_val", "_ones", "_row_ptr")
 
     def __init__(self, num_vertices: int, row: torch.Tensor, col: torch.Tensor,
                  val: torch.Tensor | None):
         self.num_vertices = int(num_vertices)
         self.row, self.col, self._val, self._ones = row, col, val, None
+        self._row_ptr = None
+
+    @property
+    def row_ptr(self) -> torch.Tensor:
+        """Offsets of each destination's run (the rows are sorted), built once."""
+        if self._row_ptr is None:
+            rp = torch.empty(self.num_vertices + 1, dtype=torch.int32, device=self.row.device)
+            _lib.call("ag_build_row_ptr", self.num_vertices, self.num_edges, _lib.ptr(self.row),
+                      _lib.ptr(rp), _lib.stream())
+            self._row_ptr = rp
+        return self._row_ptr
 
     @property
     def val(self) -> torch.Tensor:

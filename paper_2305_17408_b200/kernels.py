@@ -297,11 +297,20 @@ def aggregate_csr_intra_blocked(a: CsrMatrix, x, op: AggregateOp, block_size: in
 
 
 def aggregate_coo_atomic(a: CooMatrix, x, op: AggregateOp) -> PartialResult:
-    """Edge-parallel aggregation with atomic accumulation, kernels.py:192-225."""
+    """Edge-parallel aggregation with atomic accumulation, kernels.py:192-225.
+
+    Sum / mean partials run as a row gather over the dst-sorted COO
+    (ag_coo_gather_spmm: same order-free semantics, no atomics); max keeps the
+    atomic compare-exchange kernel."""
     x = _check_features(a.num_vertices, x)
     y = torch.empty((a.num_vertices, x.shape[1]), dtype=torch.float32, device=x.device)
-    coo_init(y, op)
-    launch_coo(a, x, y, op)
+    if op is not AggregateOp.MAX and os.environ.get("AG_COO_ATOMIC") != "1":
+        _lib.call("ag_coo_gather_spmm", a.num_vertices, x.shape[1], _lib.ptr(a.row_ptr),
+                  _lib.ptr(a.col), _lib.ptr(a.kernel_val), _lib.ptr(x), _lib.ptr(y),
+                  _lib.stream())
+    else:
+        coo_init(y, op)
+        launch_coo(a, x, y, op)
     touched = _coo_touched(a)
     note = None
     if op is AggregateOp.MAX:
@@ -483,8 +492,13 @@ class SubgraphExec:
         if kind in (KernelKind.CSR_INTER, KernelKind.CSR_INTRA_BLOCKED):
             launch_fused(self.csr, x, y, op)
         elif kind is KernelKind.COO_ATOMIC:
-            coo_init(y, op)
-            launch_coo(self.coo, x, y, op)
+            if op is not AggregateOp.MAX and os.environ.get("AG_COO_ATOMIC") != "1":
+                _lib.call("ag_coo_gather_spmm", self.coo.num_vertices, x.shape[1],
+                          _lib.ptr(self.coo.row_ptr), _lib.ptr(self.coo.col),
+                          _lib.ptr(self.coo.kernel_val), _lib.ptr(x), _lib.ptr(y), _lib.stream())
+            else:
+                coo_init(y, op)
+                launch_coo(self.coo, x, y, op)
         else:
             y.copy_(self.run(kind, x, op, tile_budget_bytes).values)
 
