@@ -337,12 +337,16 @@ __global__ void __launch_bounds__(kXentThreads) xent_rows_kernel(
   }
 }
 
+// One warp: lane l sums partials l, l + 32, ... in order, then a fixed
+// shuffle tree -- deterministic for a given partial count, ~30x shorter than
+// one thread walking every partial.
 __global__ void loss_final_kernel(int n, const double *partial, double inv_n, float *out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < n; ++i) t += partial[i];
-    *out = static_cast<float>(t * inv_n);
-  }
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  double t = 0.0;
+  for (int i = threadIdx.x; i < n; i += 32) t += partial[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (threadIdx.x == 0) *out = static_cast<float>(t * inv_n);
 }
 
 // bits[r][w] of a [rows][feat] (row stride ld) activation: a warp per
