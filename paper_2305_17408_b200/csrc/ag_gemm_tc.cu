@@ -198,6 +198,46 @@ __device__ __forceinline__ void tc_commit_mc(uint64_t *bar, uint16_t mask) {
       "h"(mask)
       : "memory");
 }
+// ---- 2-SM (cta_group::2) pair helpers: the leader (cluster rank 0) issues the
+// M = 256 MMAs over both CTAs' shared memory; barrier arrivals from the peer
+// target the leader's barriers through their cluster addresses
+__device__ __forceinline__ uint32_t mapa_rank(const void *p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(su32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *b, uint32_t parity) {
+  uint32_t done = 0;
+  uint32_t spins = 0;
+  while (!done) {
+    if (++spins > (1u << 26)) __trap();
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tc_mma_tf32_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_2sm(uint64_t *bar) {  // arrives on both CTAs' barrier
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(su32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
                ::: "memory");
@@ -254,16 +294,17 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
 }
 
 // Instruction descriptor: D f32, A/B tf32, majors, N, M = 128.
-__host__ __device__ constexpr uint32_t instr_desc(bool a_mn, bool b_mn, int n) {
+__host__ __device__ constexpr uint32_t instr_desc(bool a_mn, bool b_mn, int n, int m = BM) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
          (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
-         (static_cast<uint32_t>(BM >> 4) << 24);
+         (static_cast<uint32_t>(m >> 4) << 24);
 }
 
-template <int BN, bool ONE = false>
+template <int BN, bool ONE = false, bool P2 = false>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;   // 16 KB
-  static constexpr int B_BYTES = BN * BK * 4;   // BN * 128 B
+  // P2 (2-SM pair): each CTA holds half of the B tile's columns
+  static constexpr int B_BYTES = (P2 ? BN / 2 : BN) * BK * 4;
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES =
       STAGE * 4 <= 200 * 1024 ? 4 : STAGE * 3 <= 200 * 1024 ? 3 : 2;
@@ -319,13 +360,14 @@ __device__ __forceinline__ void split_tile(uint32_t hi, uint32_t lo, int n4, int
 // of the same N tile in lockstep; each CTA TMA-loads 1/CL of every B k-block
 // and multicasts it to all of them, so B crosses L2 once per cluster, and the
 // MMA completions free the stage in every CTA (multicast commit).
-template <int BN, bool A_MN, bool B_MN, bool ONE, int CL>
+template <int BN, bool A_MN, bool B_MN, bool ONE, int CL, bool P2 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmBl,
                    const __grid_constant__ CUtensorMap tmC, TcArgs g) {
-  using C = Cfg<BN, ONE>;
+  using C = Cfg<BN, ONE, P2>;
+  static_assert(!P2 || CL == 2, "a 2-SM pair is a cluster of two");
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -361,12 +403,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 4);
-      mbar_init(&empty[s], CL);
+      mbar_init(&conv[s], P2 ? 8 : 4);     // P2: both CTAs' splitters arrive on the leader's
+      mbar_init(&empty[s], P2 ? 1 : CL);   // P2: the leader's multicast commit
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], kEpiWarps);
+      mbar_init(&tempty[b], P2 ? 2 * kEpiWarps : kEpiWarps);  // P2: both CTAs' epilogues
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -375,11 +417,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmB);
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     su32(tmem_slot)),
-                 "n"(C::TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (P2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tmem_slot)),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tmem_slot)),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -428,6 +478,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           // block-diagonal mode: this tile's B rows start at its panel base
           const int kb_row = kk + (g.bdiag ? static_cast<int>((m0 / g.bdiag) * g.bdiag) : 0);
           auto load_b = [&](unsigned char *dst, const CUtensorMap *map) {
+            if constexpr (P2) {  // this CTA's half of the columns, no multicast
+              if (B_MN) {
+#pragma unroll
+                for (int c = 0; c < BN / 64; ++c)
+                  tma_load_2d(dst + c * kMnBox, map, &full[stage],
+                              n0 + rank * (BN / 2) + 32 * c, kb_row);
+              } else {
+                tma_load_2d(dst, map, &full[stage], kb_row, n0 + rank * (BN / 2));
+              }
+              return;
+            }
             if (B_MN) {  // BN/32 boxes {32 (n), 32 (k)}: box c from CTA c % CL
 #pragma unroll
               for (int c = 0; c < BN / 32; ++c) {
@@ -450,7 +511,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ----------------------------------------------------- MMA issuer ----
-    constexpr uint32_t idesc = instr_desc(A_MN, B_MN, BN);
+    // P2: the leader issues M = 256 MMAs over both CTAs; the peer's warp idles
+    if (P2 && rank != 0) {
+    } else {
+    constexpr uint32_t idesc = instr_desc(A_MN, B_MN, BN, P2 ? 2 * BM : BM);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -461,14 +525,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ti = static_cast<int>(static_cast<uint32_t>(t - cid) / static_cast<uint32_t>(ncl));
       const bool tr = g.trace != nullptr && blockIdx.x == 0 && lane == 0 && ti < kTraceTiles;
       if (tr) g.trace[ti * 10 + 0] = gtime();
-      mbar_wait_spin(&tempty[acc], acc_phase ^ 1);
+      if (P2) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+      else mbar_wait_spin(&tempty[acc], acc_phase ^ 1);
       if (tr) g.trace[ti * 10 + 1] = gtime();
       tc_fence_after();
       const uint32_t d = tmem_base + static_cast<uint32_t>(acc * C::NACC * BN);  // hi*hi
       const uint32_t dc = ONE ? d : d + BN;                                     // correction
       for (int kb = 0; kb < nkb; ++kb) {
         if (tr && kb < 2) g.trace[ti * 10 + 6 + 2 * kb] = gtime();
-        mbar_wait_spin(&conv[stage], phase);
+        if (P2) mbar_wait_cluster(&conv[stage], phase);
+        else mbar_wait_spin(&conv[stage], phase);
         if (tr && kb < 2) g.trace[ti * 10 + 7 + 2 * kb] = gtime();
         tc_fence_after();
         if (lane == 0) {
@@ -491,22 +557,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t dbh = smem_desc(b_hi + bo, blbo, bsbo, B_MN);
             const uint64_t dbl = smem_desc(b_lo + bo, blbo, bsbo, B_MN);
             const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
-            if (!(g.exp & 18)) {
-              tc_mma_tf32(dc, dal, dbh, idesc, first);
-              tc_mma_tf32(dc, dah, dbl, idesc, 1u);
+            if constexpr (P2) {
+              tc_mma_tf32_2sm(dc, dal, dbh, idesc, first);
+              tc_mma_tf32_2sm(dc, dah, dbl, idesc, 1u);
+              tc_mma_tf32_2sm(d, dah, dbh, idesc, ONE ? 1u : first);
+            } else {
+              if (!(g.exp & 18)) {
+                tc_mma_tf32(dc, dal, dbh, idesc, first);
+                tc_mma_tf32(dc, dah, dbl, idesc, 1u);
+              }
+              if (!(g.exp & 16)) tc_mma_tf32(d, dah, dbh, idesc, ONE ? 1u : first);
             }
-            if (!(g.exp & 16)) tc_mma_tf32(d, dah, dbh, idesc, ONE ? 1u : first);
           }
-          if (CL == 1) tc_commit(&empty[stage]);
-          else tc_commit_mc(&empty[stage], kAll);  // the stage is free in every CTA's view
-          if (kb == nkb - 1) tc_commit(&tfull[acc]);
+          if constexpr (P2) {
+            tc_commit_2sm(&empty[stage]);  // the stage is free in both CTAs
+            if (kb == nkb - 1) tc_commit_2sm(&tfull[acc]);
+          } else {
+            if (CL == 1) tc_commit(&empty[stage]);
+            else tc_commit_mc(&empty[stage], kAll);  // the stage is free in every CTA's view
+            if (kb == nkb - 1) tc_commit(&tfull[acc]);
+          }
         }
         __syncwarp();
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
-      if (nkb == 0 && lane == 0) tc_commit(&tfull[acc]);  // (K == 0: nothing to do)
+      if (nkb == 0 && lane == 0) {  // (K == 0: nothing to do)
+        if constexpr (P2) tc_commit_2sm(&tfull[acc]);
+        else tc_commit(&tfull[acc]);
+      }
       __syncwarp();
       if (++acc == C::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
+    }
     }
   } else if (warp < kEpiWarp0) {
     // ------------------------------------------------------- splitters ---
@@ -533,7 +614,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_proxy_async();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[stage]);
+        if (lane == 0) {
+          if constexpr (P2) mbar_arrive_cluster(mapa_rank(&conv[stage], 0));
+          else mbar_arrive(&conv[stage]);
+        }
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -792,7 +876,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (tr) g.trace[ti * 10 + 5] = gtime();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (P2) mbar_arrive_cluster(mapa_rank(&tempty[acc], 0));
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == C::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
     }
   }
@@ -803,9 +890,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (CL > 1) cluster_sync();  // no CTA leaves while a peer may still signal / write it
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "n"(C::TMEM_COLS)
-                 : "memory");
+    if constexpr (P2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -867,11 +959,11 @@ int make_map(CUtensorMap *m, const float *base, int64_t inner, int64_t outer, in
   return AG_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool ONE, int CL>
+template <int BN, bool A_MN, bool B_MN, bool ONE, int CL, bool P2 = false>
 int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbl,
               const CUtensorMap &mc, TcArgs g, cudaStream_t st) {
-  using C = Cfg<BN, ONE>;
-  auto k = tc_gemm_kernel<BN, A_MN, B_MN, ONE, CL>;
+  using C = Cfg<BN, ONE, P2>;
+  auto k = tc_gemm_kernel<BN, A_MN, B_MN, ONE, CL, P2>;
   AG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   const int64_t msup = (g.m_tiles + CL - 1) / CL;
   const int64_t total = msup * g.n_tiles * g.splits;
@@ -905,6 +997,22 @@ int launch_bn1(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &m
   if (a_mn && b_mn) return launch_tc<BN, true, true, ONE, CL>(ma, mb, mbl, mc, g, st);
   return launch_tc<BN, true, false, ONE, CL>(ma, mb, mbl, mc, g, st);
 }
+// 2-SM pairs (cta_group::2, M = 256 per MMA, each CTA holding half of B):
+// 256-wide tiles only
+int launch_2sm(bool a_mn, bool b_mn, bool one, const CUtensorMap &ma, const CUtensorMap &mb,
+               const CUtensorMap &mbl, const CUtensorMap &mc, const TcArgs &g, cudaStream_t st) {
+  if (one) {
+    if (!a_mn && b_mn) return launch_tc<256, false, true, true, 2, true>(ma, mb, mbl, mc, g, st);
+    if (!a_mn && !b_mn) return launch_tc<256, false, false, true, 2, true>(ma, mb, mbl, mc, g, st);
+    if (a_mn && b_mn) return launch_tc<256, true, true, true, 2, true>(ma, mb, mbl, mc, g, st);
+    return launch_tc<256, true, false, true, 2, true>(ma, mb, mbl, mc, g, st);
+  }
+  if (!a_mn && b_mn) return launch_tc<256, false, true, false, 2, true>(ma, mb, mbl, mc, g, st);
+  if (!a_mn && !b_mn) return launch_tc<256, false, false, false, 2, true>(ma, mb, mbl, mc, g, st);
+  if (a_mn && b_mn) return launch_tc<256, true, true, false, 2, true>(ma, mb, mbl, mc, g, st);
+  return launch_tc<256, true, false, false, 2, true>(ma, mb, mbl, mc, g, st);
+}
+
 template <int BN>
 int launch_bn(bool a_mn, bool b_mn, const CUtensorMap &ma, const CUtensorMap &mb,
               const CUtensorMap &mbl, const CUtensorMap &mc, const TcArgs &g, int cl,
@@ -1031,6 +1139,10 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int32_
   int cl = (bn >= 64 && g.m_tiles >= 2 && !a_mn) ? 2 : 1;
   if (const char *e = std::getenv("AG_TC_CL")) cl = std::atoi(e) == 2 && bn >= 64 ? 2 : 1;
   if (bdiag) cl = 1;  // neighbouring tiles read different B panels: no multicast
+  // 2-SM pairs for 256-wide tiles (AG_TC_2SM=1; development until measured)
+  const char *e2 = std::getenv("AG_TC_2SM");
+  const bool p2 = bn == 256 && bdiag == 0 && g.m_tiles >= 2 && e2 && std::atoi(e2) == 1;
+  if (p2) cl = 2;
   CUtensorMap ma, mb;
   int rc;
   // A: K-major [M][K] (inner K) or M-major [K][M] (inner M)
@@ -1038,7 +1150,7 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int32_
   else rc = make_map(&ma, A, K, M, lda, BM, false);
   if (rc) return rc;
   if (b_mn) rc = make_map(&mb, B, N, bdiag ? b_rows : K, ldb, BK, true);
-  else rc = make_map(&mb, B, K, N, ldb, bn / cl, false);
+  else rc = make_map(&mb, B, K, N, ldb, bn / cl, false);  // (p2: cl = 2, each CTA's half)
   if (rc) return rc;
   CUtensorMap mbl = mb;
   if (B_lo) {
@@ -1088,7 +1200,10 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int32_
     AG_CUDA(cudaMemset(trace, 0, kTraceTiles * 10 * sizeof(long long)));
     g.trace = trace;
   }
-  switch (bn) {
+  if (p2) {
+    const char *eo = std::getenv("AG_TC_ONEACC");
+    rc = launch_2sm(a_mn, b_mn, eo ? std::atoi(eo) != 0 : !a_mn, ma, mb, mbl, mc, g, st);
+  } else switch (bn) {
     case 32: rc = launch_bn<32>(a_mn, b_mn, ma, mb, mbl, mc, g, cl, st); break;
     case 64: rc = launch_bn<64>(a_mn, b_mn, ma, mb, mbl, mc, g, cl, st); break;
     case 128: rc = launch_bn<128>(a_mn, b_mn, ma, mb, mbl, mc, g, cl, st); break;

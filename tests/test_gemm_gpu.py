@@ -76,3 +76,19 @@ def test_auto_engine_picks_simt_for_unaligned_strides():
     w = torch.randn((47, 7), device="cuda")
     got = K.gemm(a, w)
     assert rel_error(to_np(got), to_np(a.double() @ w.double())) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,Kd,ta,tb", [(1000, 256, 256, False, False), (5000, 256, 48, False, True),
+                                         (777, 200, 100, False, False), (256, 256, 70000, True, False)])
+def test_tc_gemm_2sm_pairs_equal_single_sm(M, N, Kd, ta, tb, monkeypatch):
+    """The opt-in 2-SM path (AG_TC_2SM=1: cta_group::2 MMAs, M = 256 over a CTA
+    pair, each CTA holding half of the B tile) accumulates in the same order as
+    the single-SM path: bitwise equal results, including partial tiles and
+    the split-K dW shape."""
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    a = torch.randn((Kd, M) if ta else (M, Kd), device="cuda", generator=g)
+    b = torch.randn((N, Kd) if tb else (Kd, N), device="cuda", generator=g)
+    base = K.gemm(a, b, trans_a=ta, trans_b=tb, engine="tc")
+    monkeypatch.setenv("AG_TC_2SM", "1")
+    got = K.gemm(a, b, trans_a=ta, trans_b=tb, engine="tc")
+    assert torch.equal(got, base)
