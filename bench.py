@@ -202,7 +202,14 @@ def run_ours(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    # the row-partitioned (DistGNN) path: world > 1, or --force-dist on one GPU
+    # (NCCL group of one: exercises the multi-GPU code path end to end)
+    dpath = world > 1 or args.force_dist
+    if dpath:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl")
     g, rg, dec, net, prep_s = build_workload(cfg, rank, world)
     V = cfg["V"]
@@ -214,7 +221,7 @@ def run_ours(args, cfg):
     lr = 0.01
     t_tune = time.perf_counter()
     cache_info = None
-    if world > 1:
+    if dpath:
         # row partition: each rank owns a B-aligned, nnz-balanced row range
         from paper_2305_17408_b200 import dist as D
         dnet = D.DistGNN.build(cfg["model"], dims, dec, rank, world, seed=0,
@@ -263,9 +270,9 @@ def run_ours(args, cfg):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if dpath:
         dist.barrier()
-    use_graph = world == 1 and not args.no_graph
+    use_graph = not dpath and not args.no_graph
     timed.events = []
     launches0 = _lib.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -281,7 +288,7 @@ def run_ours(args, cfg):
         graphed_v = ag.GraphedTrainStep(timed, [(x, labels, mask)], n_mask, lr)
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
-        if world > 1:
+        if dpath:
             dist.barrier()
         start.record()
         for _ in range(args.steps):
@@ -291,7 +298,7 @@ def run_ours(args, cfg):
                 loss, _ = step()
         end.record()
         torch.cuda.synchronize()
-        if world > 1:
+        if dpath:
             dist.barrier()
     if use_graph:
         launches = launches_per_step * args.steps  # the graph holds one step's launches
@@ -308,11 +315,11 @@ def run_ours(args, cfg):
     E_full = rg.num_edges
     weighted = rg.weights is not None
     # algorithmic bytes of the aggregations THIS rank ran (its rows' share)
-    frac_rows = 1.0 if world == 1 else halo["rows_per_rank"] / V
+    frac_rows = 1.0 if not dpath else halo["rows_per_rank"] / V
     agg_bytes = sum(bytes_alg(V, E_full, f, weighted) for _, _, f, _ in timed.events) * frac_rows
     n_agg = len(timed.events)
     timed.events = None
-    if world > 1:
+    if dpath:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -350,13 +357,13 @@ def run_ours(args, cfg):
     # single GPU: the step replays as one CUDA graph per feeder buffer
     # (models.GraphedTrainStep); the buffers hold real inputs while capturing
     graphed = None
-    if world == 1 and not args.no_graph:
+    if not dpath and not args.no_graph:
         for bufs in feeder.bufs:
             for d, h in zip(bufs, feeder.host):
                 d.copy_(h)
         graphed = ag.GraphedTrainStep(timed, [tuple(b) for b in feeder.bufs], n_mask, lr)
     feeder.reset()
-    if world > 1:
+    if dpath:
         dist.barrier()
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps + 1)]
     e_start.record()
@@ -380,14 +387,14 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     e2e_ms = e_start.elapsed_time(e_end) / e2e_steps
     e2e_each = [round(step_ev[i].elapsed_time(step_ev[i + 1]), 2) for i in range(e2e_steps)]
-    if world > 1:
+    if dpath:
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     h2d = x_host.numel() * 4 + lab_host.numel() * 4 + mask_host.numel()
 
     peak, peak_src = peaks()
-    frac_local = 1.0 if world == 1 else halo["rows_per_rank"] / V
+    frac_local = 1.0 if not dpath else halo["rows_per_rank"] / V
     widths = {str(f): {"launches_per_step": n // args.steps, "ms_per_launch": round(t / n, 4),
                        "alg_GBps": round(bytes_alg(V, E_full, f, weighted) * frac_local
                                          / (t / n / 1e3) / 1e9, 1)}
@@ -425,7 +432,7 @@ def run_ours(args, cfg):
                       "(GraphedTrainStep); per-aggregation timings from an eager pass"
                       if use_graph else "eager launches, per-aggregation CUDA events in-step",
             "parallelism": f"row-partition x{world} (NCCL per-peer halo all-to-all + dW all-reduce)"
-                           if world > 1 else "single GPU",
+                           if dpath else "single GPU",
             **({"halo": halo} if halo else {}),
         },
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms/epoch", "h2d_bytes_per_step": h2d,
@@ -458,11 +465,11 @@ def run_ours(args, cfg):
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not dpath and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(rg, cfg)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dpath:
         dist.destroy_process_group()
 
 
@@ -569,6 +576,8 @@ def main():
     ap.add_argument("--choice-cache", default=str(ROOT / ".choice_cache.json"),
                     help="ChoiceCache file (selector + autotuned pairs per graph/width/direction); "
                          "'' disables it")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the row-partitioned multi-GPU path even on one GPU (testing)")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the training step eagerly instead of as a CUDA graph")
     ap.add_argument("--comm-size", type=int, default=None,
