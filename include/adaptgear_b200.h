@@ -196,6 +196,16 @@ int ag_coo_spmm(int64_t num_rows, int64_t feat, int64_t num_edges,
 int ag_coo_gather_spmm(int64_t num_rows, int64_t feat, const int32_t *row_ptr,
                        const int32_t *col, const float *val, const float *x, float *y,
                        void *stream);
+/* The (dense_block, coo_atomic) selector pair on a small graph (features that
+ * fit L2) as ONE order-free row gather over the full CSR (both roles' edges),
+ * with ag_fused_spmm's epilogues: y = sum [+ gin_scale * x] [relu, bits to
+ * relu_out] [* relu_bits].  feat % 4 == 0, x / y 16-byte aligned, row stride
+ * feat; relu masks [rows][ceil(feat / 32)] words.  Order-free like the pair
+ * (kernels.py:228-250 matmul, :192-225 scrambled bincount; tested at 1e-5). */
+int ag_gather_pair_spmm(int64_t num_rows, int64_t feat, const int32_t *row_ptr,
+                        const int32_t *col, const float *val, const float *x, float *y,
+                        int32_t epi_flags, float gin_scale, const uint32_t *relu_bits,
+                        uint32_t *relu_out, void *stream);
 
 /* K4 aggregate_dense_block (kernels.py:228-250): for every B-row community c
  * with slot k = comm_slot[c] >= 0: Y[cB:cB+B] = blocks[k] @ X[cB:cB+B]

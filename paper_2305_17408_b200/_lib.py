@@ -53,6 +53,7 @@ SIGNATURES: dict[str, list] = {
     "ag_csr_intra_spmm": [I64, I64, I64, I64, P, P, P, P, P, I32, I32, P, P, F32, P],
     "ag_coo_spmm": [I64, I64, I64, P, P, P, P, P, I32, P],
     "ag_coo_gather_spmm": [I64, I64, P, P, P, P, P, P],
+    "ag_gather_pair_spmm": [I64, I64, P, P, P, P, P, I32, F32, P, P, P],
     "ag_dense_block_spmm": [I64, I64, I64, P, P, P, P, P, I32, I32, P, P, F32, P],
     "ag_role_csr_build": [I64, P, P, P, I64, P, P, P, P],
     "ag_fused_spmm": [I64, I64, I32, P, P, P, P, P, P, I32, P, I64, P, P, I32, I32, P, P, F32,

@@ -426,6 +426,99 @@ __global__ void __launch_bounds__(kBlock) coo_gather_kernel(int64_t rows, int64_
   }
 }
 
+// ------------------- small graphs: the (dense_block, coo_atomic) pair as a gather --
+// Both roles of that selector pair are order-free (the dense block product is a
+// BLAS matmul, kernels.py:247; coo_atomic a scrambled bincount), so on a graph
+// whose features fit L2 the pair runs as ONE row gather over the full CSR: a
+// LANES-lane group per row (4 columns per lane), 8 source loads in flight,
+// then the fused epilogue -- GIN (1 + eps) x, ReLU (+ its bit mask), or the
+// ReLU-backward mask -- and one store.  The slab kernel's pipeline start-up
+// (tens of microseconds filling the X ring) dominates such graphs.
+template <int LANES>
+__global__ void __launch_bounds__(kBlock) gather_pair_kernel(
+    int64_t rows, int64_t feat, const int32_t *row_ptr, const int32_t *col, const float *val,
+    const float *x, float *y, int32_t flags, float gin_scale, const uint32_t *relu_bits,
+    uint32_t *relu_out, int64_t ldw) {
+  constexpr int VEC = 4;
+  const int sub = threadIdx.x & 31;
+  const int lane = sub % LANES;
+  const unsigned gmask =
+      LANES == 32 ? 0xffffffffu : (((1u << LANES) - 1u) << (sub / LANES * LANES));
+  const int64_t grp = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / LANES;
+  const int64_t ngrp = static_cast<int64_t>(gridDim.x) * (kBlock / LANES);
+  const int tile = LANES * VEC;
+  for (int64_t r = grp; r < rows; r += ngrp) {
+    const int32_t s = __ldg(row_ptr + r), e = __ldg(row_ptr + r + 1);
+    for (int f0 = 0; f0 < feat; f0 += tile) {
+      const int64_t f = f0 + lane * VEC;
+      const bool act = f < feat;
+      Vf<VEC> a0 = splat<VEC>(0.0f), a1 = a0;
+      for (int32_t b = s; b < e; b += LANES) {
+        int32_t mc = 0;
+        float mv = 0.0f;
+        if (b + lane < e) {
+          mc = __ldg(col + b + lane);
+          mv = val ? __ldg(val + b + lane) : 1.0f;
+        }
+        const int n = e - b < LANES ? e - b : LANES;
+        for (int j = 0; j < n; j += 8) {
+          Vf<VEC> xv[8];
+          float w[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int jj = j + u;
+            const int32_t c = __shfl_sync(gmask, mc, jj, LANES);
+            w[u] = __shfl_sync(gmask, mv, jj, LANES);
+            xv[u] = (jj < n && act) ? ldv<VEC>(x + static_cast<int64_t>(c) * feat + f)
+                                    : splat<VEC>(0.0f);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (j + u < n) {
+              Vf<VEC> &acc = (u & 1) ? a1 : a0;
+#pragma unroll
+              for (int i = 0; i < VEC; ++i) acc.v[i] = fmaf(xv[u].v[i], w[u], acc.v[i]);
+            }
+          }
+        }
+      }
+      Vf<VEC> o = vadd<VEC>(a0, a1);
+      if ((flags & AG_EPI_GIN) && act) {
+        const Vf<VEC> xr = ldv<VEC>(x + r * feat + f);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) o.v[i] = fmaf(gin_scale, xr.v[i], o.v[i]);
+      }
+      if (flags & AG_EPI_RELU) {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) o.v[i] = fmaxf(o.v[i], 0.0f);
+      }
+      if ((flags & AG_EPI_RELU_MASK) && act) {
+        const uint32_t nib = (__ldg(relu_bits + r * ldw + (f >> 5)) >> (f & 31)) & 15u;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i)
+          if (!((nib >> i) & 1u)) o.v[i] = 0.0f;
+      }
+      if (relu_out != nullptr) {  // 8 lanes x 4 columns = one mask word
+        uint32_t wd = 0;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i)
+          if (act && f + i < feat && o.v[i] > 0.0f) wd |= 1u << (4 * (lane & 7) + i);
+        if constexpr (LANES >= 8) {
+          wd |= __shfl_xor_sync(gmask, wd, 1, LANES);
+          wd |= __shfl_xor_sync(gmask, wd, 2, LANES);
+          wd |= __shfl_xor_sync(gmask, wd, 4, LANES);
+          if ((lane & 7) == 0 && act) relu_out[r * ldw + (f >> 5)] = wd;
+        } else {  // fewer than 8 lanes: the group's lanes share one word
+#pragma unroll
+          for (int o2 = 1; o2 < LANES; o2 <<= 1) wd |= __shfl_xor_sync(gmask, wd, o2, LANES);
+          if (lane == 0) relu_out[r * ldw + (f0 >> 5)] = wd;
+        }
+      }
+      if (act) stv<VEC>(y + r * feat + f, o);
+    }
+  }
+}
+
 // ---------------------------------------------------- K4: dense blocks -----
 struct DenseArgs {
   int64_t rows;
@@ -550,6 +643,18 @@ int launch_coo_gather_vec(int64_t rows, int64_t feat, const int32_t *row_ptr,
     case 16: return launch_coo_gather<VEC, 16>(rows, feat, row_ptr, col, val, x, y, st);
     default: return launch_coo_gather<VEC, 32>(rows, feat, row_ptr, col, val, x, y, st);
   }
+}
+
+template <int LANES>
+int launch_gather_pair(int64_t rows, int64_t feat, const int32_t *row_ptr, const int32_t *col,
+                       const float *val, const float *x, float *y, int32_t flags, float gin,
+                       const uint32_t *rb, uint32_t *ro, cudaStream_t st) {
+  auto k = gather_pair_kernel<LANES>;
+  const int64_t work = (rows * LANES + kBlock - 1) / kBlock;
+  k<<<resident_grid(k, 0, work), kBlock, 0, st>>>(rows, feat, row_ptr, col, val, x, y, flags, gin,
+                                                   rb, ro, relu_words(feat));
+  AG_LAUNCH_CHECK("gather_pair_kernel");
+  return AG_OK;
 }
 
 template <int VEC, int LANES>
@@ -760,5 +865,32 @@ extern "C" int ag_coo_gather_spmm(int64_t num_rows, int64_t feat, const int32_t 
     case 4: return launch_coo_gather_vec<4>(num_rows, feat, row_ptr, col, val, x, y, st);
     case 2: return launch_coo_gather_vec<2>(num_rows, feat, row_ptr, col, val, x, y, st);
     default: return launch_coo_gather_vec<1>(num_rows, feat, row_ptr, col, val, x, y, st);
+  }
+}
+
+extern "C" int ag_gather_pair_spmm(int64_t num_rows, int64_t feat, const int32_t *row_ptr,
+                                   const int32_t *col, const float *val, const float *x,
+                                   float *y, int32_t epi_flags, float gin_scale,
+                                   const uint32_t *relu_bits, uint32_t *relu_out, void *stream) {
+  if (num_rows < 0 || feat < 0) return fail(AG_ERR_VALUE, "negative sizes");
+  constexpr int32_t kFlags = AG_EPI_GIN | AG_EPI_RELU | AG_EPI_RELU_MASK;
+  if (epi_flags & ~kFlags) return fail(AG_ERR_VALUE, "ag_gather_pair_spmm takes GIN / RELU / RELU_MASK");
+  if ((epi_flags & AG_EPI_RELU_MASK) && relu_bits == nullptr)
+    return fail(AG_ERR_VALUE, "AG_EPI_RELU_MASK needs relu_bits");
+  if (relu_out != nullptr && !(epi_flags & AG_EPI_RELU))
+    return fail(AG_ERR_VALUE, "relu_out is written with AG_EPI_RELU only");
+  if (num_rows == 0 || feat == 0) return AG_OK;
+  if (feat % 4 || (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(y) & 15))
+    return fail(AG_ERR_VALUE, "ag_gather_pair_spmm needs feat % 4 == 0 and 16-byte aligned x / y");
+  cudaStream_t st = as_stream(stream);
+  switch (pick_lanes(feat / 4)) {
+    case 4: return launch_gather_pair<4>(num_rows, feat, row_ptr, col, val, x, y, epi_flags,
+                                         gin_scale, relu_bits, relu_out, st);
+    case 8: return launch_gather_pair<8>(num_rows, feat, row_ptr, col, val, x, y, epi_flags,
+                                         gin_scale, relu_bits, relu_out, st);
+    case 16: return launch_gather_pair<16>(num_rows, feat, row_ptr, col, val, x, y, epi_flags,
+                                           gin_scale, relu_bits, relu_out, st);
+    default: return launch_gather_pair<32>(num_rows, feat, row_ptr, col, val, x, y, epi_flags,
+                                           gin_scale, relu_bits, relu_out, st);
   }
 }

@@ -128,6 +128,20 @@ def _bits_for(relu_src, relu_bits_in, rows: int, feat: int):
 
 
 _BAND_FLAGS = None
+GATHER_MAX_BYTES = 64 << 20  # features up to this size take the gather pair (they stay in L2)
+
+
+def _gather_ok(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, flags: int) -> bool:
+    """The order-free (dense_block, coo_atomic) pair runs as one row gather
+    (ag_gather_pair_spmm) when the features fit L2 (AG_GATHER=0 disables)."""
+    if os.environ.get("AG_GATHER", "1") == "0":
+        return False
+    F = x.shape[1]
+    allowed = (_lib.AG_EPI_GIN | _lib.AG_EPI_RELU | _lib.AG_EPI_RELU_MASK
+               | _lib.AG_EPI_INTER_COO)
+    return (x.shape[0] * F * 4 <= GATHER_MAX_BYTES and F % 4 == 0 and x.stride(0) == F
+            and y.stride(0) == F and x.data_ptr() % 16 == 0 and y.data_ptr() % 16 == 0
+            and (flags & ~allowed) == 0 and x.shape[0] == a.num_vertices)
 
 
 def _band_ok(x: torch.Tensor, y: torch.Tensor, rb, flags: int) -> bool:
@@ -164,6 +178,14 @@ def launch_fused(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, op: AggregateOp
     rb = _bits_for(relu_src, relu_bits_in, a.num_vertices, x.shape[1])
     if relu_out is not None:
         _bits_for(None, relu_out, a.num_vertices, x.shape[1])
+    if dense_intra and block == 16 and mask == 3 and op is AggregateOp.SUM \
+            and (flags & _lib.AG_EPI_INTER_COO) and _gather_ok(a, x, y, flags):
+        # a small graph: the order-free pair as one row gather (no ring start-up)
+        _lib.call("ag_gather_pair_spmm", a.num_vertices, x.shape[1], _lib.ptr(a.row_ptr),
+                  _lib.ptr(a.col_idx), _lib.ptr(a.kernel_val), _lib.ptr(x), _lib.ptr(y),
+                  flags & ~_lib.AG_EPI_INTER_COO | (_lib.AG_EPI_RELU_MASK if rb is not None else 0),
+                  float(gin_scale), _lib.ptr(rb), _lib.ptr(relu_out), _lib.stream())
+        return
     if dense_intra and block == 16 and mask == 3 and op is AggregateOp.SUM \
             and (flags & _lib.AG_EPI_INTER_COO) and _band_ok(x, y, rb, flags):
         rec, off, far_cnt, far_src, window = a.band_layout()

@@ -22,6 +22,13 @@ from oracle import ref_numpy as R  # noqa: E402
 from conftest import same_float, to_np  # noqa: E402
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _slab_only(monkeypatch):
+    """These graphs are small enough for the gather pair (ag_gather_pair_spmm,
+    tests/test_gather_gpu.py); here the slab kernel's own modes are tested."""
+    monkeypatch.setenv("AG_GATHER", "0")
 OPS = (ag.AggregateOp.SUM, ag.AggregateOp.MEAN, ag.AggregateOp.MAX)
 
 
