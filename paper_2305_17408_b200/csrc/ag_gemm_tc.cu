@@ -901,20 +901,38 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-__global__ void splitk_sum_kernel(int64_t M, int64_t N, int splits, const float *part, float *C,
-                                  int64_t ldc, float alpha, float beta, int relu,
-                                  const uint32_t *mask, int64_t ldm) {
+// Sum of the split-K partials: a 32 x 8 block takes 32 consecutive outputs;
+// thread (o, g) adds partials g, g + 8, ... of output o in fp64 (loads
+// coalesced across o), then the 8 group sums are added in a fixed order --
+// deterministic, and 8x the memory parallelism of one thread per output
+// walking all ~150 partials.
+constexpr int kSumGroups = 8;
+__global__ void __launch_bounds__(32 * kSumGroups) splitk_sum_kernel(
+    int64_t M, int64_t N, int splits, const float *part, float *C, int64_t ldc, float alpha,
+    float beta, int relu, const uint32_t *mask, int64_t ldm) {
+  __shared__ double acc[kSumGroups][32];
   const int64_t n = M * N;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32; i0 < n;
+       i0 += static_cast<int64_t>(gridDim.x) * 32) {
+    const int64_t i = i0 + tx;
     double s = 0.0;
-    for (int p = 0; p < splits; ++p) s += part[p * n + i];  // fixed order: deterministic
-    const int64_t m = i / N, c = i % N;
-    float v = alpha * static_cast<float>(s);
-    if (beta != 0.0f) v = fmaf(beta, C[m * ldc + c], v);
-    if (relu) v = fmaxf(v, 0.0f);
-    if (mask && !relu_bit(mask, ldm, m, c)) v = 0.0f;
-    C[m * ldc + c] = v;
+    if (i < n)
+      for (int p = ty; p < splits; p += kSumGroups) s += part[p * n + i];
+    acc[ty][tx] = s;
+    __syncthreads();
+    if (ty == 0 && i < n) {
+      s = 0.0;
+#pragma unroll
+      for (int q = 0; q < kSumGroups; ++q) s += acc[q][tx];
+      const int64_t m = i / N, c = i % N;
+      float v = alpha * static_cast<float>(s);
+      if (beta != 0.0f) v = fmaf(beta, C[m * ldc + c], v);
+      if (relu) v = fmaxf(v, 0.0f);
+      if (mask && !relu_bit(mask, ldm, m, c)) v = 0.0f;
+      C[m * ldc + c] = v;
+    }
+    __syncthreads();
   }
 }
 
@@ -1228,7 +1246,7 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int32_
     }
   }
   if (splits > 1) {
-    splitk_sum_kernel<<<grid_for(M * N, 256), 256, 0, st>>>(M, N, nparts, g.C, C, ldc, alpha,
+    splitk_sum_kernel<<<grid_for((M * N + 31) / 32, 1), 32 * kSumGroups, 0, st>>>(M, N, nparts, g.C, C, ldc, alpha,
                                                             beta, g.relu, mask, ldm);
     AG_LAUNCH_CHECK("splitk_sum_kernel");
     if (mask_out != nullptr) {
