@@ -139,9 +139,9 @@ def test_world1_distgnn_equals_gnn(model, pair):
         assert rel_error(to_np(b), to_np(a)) < tol
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world,pair", [(2, "csr"), (4, "csr"), (2, "dense_coo")])
 @pytest.mark.parametrize("model", ["gcn", "gin"])
-def test_virtual_ranks_distgnn_step(world, model):
+def test_virtual_ranks_distgnn_step(world, pair, model):
     """G ranks as threads on one GPU (in-process all-to-all / all-reduce):
     the row-partitioned, reassociated step with the halo exchange and the
     overlapped backward equals the 1-GPU GNN step -- loss and every dW
@@ -158,7 +158,7 @@ def test_virtual_ranks_distgnn_step(world, model):
     loss_r, grads_r = ref.train_step(x, labels, mask, n, lr=0.0)
     torch.cuda.synchronize()
     nets = [D.DistGNN.build(model, dims, dec, rank=r, world=world, seed=2, gin_eps=0.2,
-                            subject_t=ref.subject_t, pair="csr") for r in range(world)]
+                            subject_t=ref.subject_t, pair=pair) for r in range(world)]
     shared, barrier = {}, threading.Barrier(world)
     results, errors = {}, []
     for r, net in enumerate(nets):
