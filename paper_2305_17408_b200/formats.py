@@ -79,7 +79,7 @@ class CsrMatrix:
     """Compressed sparse rows over destination vertices."""
 
     __slots__ = ("num_vertices", "row_ptr", "col_idx", "_val", "_ones", "_rows", "_touched",
-                 "_off_block", "_long", "_window", "_codes", "_dense16", "_band")
+                 "_off_block", "_long", "_window", "_codes", "_dense16", "_band", "_ring_cov")
 
     def __init__(self, num_vertices: int, row_ptr: torch.Tensor, col_idx: torch.Tensor,
                  val: torch.Tensor | None, rows: torch.Tensor | None = None):
@@ -93,6 +93,7 @@ class CsrMatrix:
         self._codes = {}
         self._dense16 = None
         self._band = None
+        self._ring_cov = None
 
     @property
     def val(self) -> torch.Tensor:
@@ -120,6 +121,19 @@ class CsrMatrix:
                       _lib.ptr(self.col_idx), SLAB_COVERAGE, _lib.byref(w), _lib.stream())
             self._window = int(w.value)
         return self._window
+
+    def ring_coverage(self) -> float:
+        """Fraction of the edges whose source lies within window() 16-row blocks
+        of the destination's block: what the slab kernel's shared-memory ring
+        serves (the rest are far / global loads).  Computed once."""
+        if self._ring_cov is None:
+            E = self.num_edges
+            if E == 0:
+                self._ring_cov = 1.0
+            else:
+                d = (self.col_idx.to(torch.int64) // 16 - self.rows().to(torch.int64) // 16).abs()
+                self._ring_cov = float((d <= self.window()).sum().item()) / E
+        return self._ring_cov
 
     def touched(self) -> torch.Tensor:
         """bool[V]: row has >= 1 edge (kernels.py:121)."""

@@ -129,19 +129,27 @@ def _bits_for(relu_src, relu_bits_in, rows: int, feat: int):
 
 _BAND_FLAGS = None
 GATHER_MAX_BYTES = 64 << 20  # features up to this size take the gather pair (they stay in L2)
+GATHER_MIN_COVERAGE = 0.9     # below this ring coverage the slab kernel's general path dominates
 
 
 def _gather_ok(a: CsrMatrix, x: torch.Tensor, y: torch.Tensor, flags: int) -> bool:
     """The order-free (dense_block, coo_atomic) pair runs as one row gather
-    (ag_gather_pair_spmm) when the features fit L2 (AG_GATHER=0 disables)."""
-    if os.environ.get("AG_GATHER", "1") == "0":
+    (ag_gather_pair_spmm) when the features fit L2, or when the slab kernel's
+    ring would serve under 90% of the edges (wide windows, many global
+    edges: its general path's per-edge global loads cost more than a plain
+    L2 gather).  AG_GATHER=0 disables it, AG_GATHER=2 forces it."""
+    mode = os.environ.get("AG_GATHER", "1")
+    if mode == "0":
         return False
     F = x.shape[1]
     allowed = (_lib.AG_EPI_GIN | _lib.AG_EPI_RELU | _lib.AG_EPI_RELU_MASK
                | _lib.AG_EPI_INTER_COO)
-    return (x.shape[0] * F * 4 <= GATHER_MAX_BYTES and F % 4 == 0 and x.stride(0) == F
-            and y.stride(0) == F and x.data_ptr() % 16 == 0 and y.data_ptr() % 16 == 0
-            and (flags & ~allowed) == 0 and x.shape[0] == a.num_vertices)
+    if not (F % 4 == 0 and x.stride(0) == F and y.stride(0) == F and x.data_ptr() % 16 == 0
+            and y.data_ptr() % 16 == 0 and (flags & ~allowed) == 0
+            and x.shape[0] == a.num_vertices):
+        return False
+    return (mode == "2" or x.shape[0] * F * 4 <= GATHER_MAX_BYTES
+            or a.ring_coverage() < GATHER_MIN_COVERAGE)
 
 
 def _band_ok(x: torch.Tensor, y: torch.Tensor, rb, flags: int) -> bool:

@@ -50,7 +50,7 @@ def measure(name, dec, rg, feats, peak, extra):
     row = {"variant": name, **extra, "edges": rg.num_edges,
            "intra_fraction": round(dec.intra.num_edges / rg.num_edges, 4),
            "deg_max": int(lens.max().item()), "rows_over_64": int((lens > 64).sum().item()),
-           "window": csr.window()}
+           "window": csr.window(), "ring_coverage": round(csr.ring_coverage(), 4)}
     for F in feats:
         x = torch.randn((V, F), device="cuda")
         y = torch.empty_like(x)
@@ -62,8 +62,10 @@ def measure(name, dec, rg, feats, peak, extra):
             if best is None or t < best[0]:
                 best = (t, f"{ki.value}+{ke.value}")
         gbs = ba / best[0] / 1e6
-        row[f"F{F}"] = {"ms": round(best[0], 4), "pair": best[1], "alg_GBps": round(gbs, 1),
-                        "frac": round(gbs / peak, 4)}
+        eng = "gather" if (best[1] == "dense_block+coo_atomic"
+                           and K._gather_ok(csr, x, y, 32)) else "slab"
+        row[f"F{F}"] = {"ms": round(best[0], 4), "pair": best[1], "engine": eng,
+                        "alg_GBps": round(gbs, 1), "frac": round(gbs / peak, 4)}
         del x, y
     print(json.dumps(row), file=sys.stderr, flush=True)
     return row
