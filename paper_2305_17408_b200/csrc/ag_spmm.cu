@@ -434,11 +434,12 @@ __global__ void __launch_bounds__(kBlock) coo_gather_kernel(int64_t rows, int64_
 // then the fused epilogue -- GIN (1 + eps) x, ReLU (+ its bit mask), or the
 // ReLU-backward mask -- and one store.  The slab kernel's pipeline start-up
 // (tens of microseconds filling the X ring) dominates such graphs.
-template <int LANES>
+template <int LANES, int NV>
 __global__ void __launch_bounds__(kBlock) gather_pair_kernel(
     int64_t rows, int64_t feat, const int32_t *row_ptr, const int32_t *col, const float *val,
     const float *x, float *y, int32_t flags, float gin_scale, const uint32_t *relu_bits,
     uint32_t *relu_out, int64_t ldw) {
+  // NV float4 chunks per lane per pass (chunk k covers columns f0 + 4 (lane + k LANES))
   constexpr int VEC = 4;
   const int sub = threadIdx.x & 31;
   const int lane = sub % LANES;
@@ -446,13 +447,20 @@ __global__ void __launch_bounds__(kBlock) gather_pair_kernel(
       LANES == 32 ? 0xffffffffu : (((1u << LANES) - 1u) << (sub / LANES * LANES));
   const int64_t grp = (static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x) / LANES;
   const int64_t ngrp = static_cast<int64_t>(gridDim.x) * (kBlock / LANES);
-  const int tile = LANES * VEC;
+  const int tile = LANES * VEC * NV;
   for (int64_t r = grp; r < rows; r += ngrp) {
     const int32_t s = __ldg(row_ptr + r), e = __ldg(row_ptr + r + 1);
     for (int f0 = 0; f0 < feat; f0 += tile) {
-      const int64_t f = f0 + lane * VEC;
-      const bool act = f < feat;
-      Vf<VEC> a0 = splat<VEC>(0.0f), a1 = a0;
+      int64_t f[NV];
+      bool act[NV];
+      Vf<VEC> a0[NV], a1[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        f[k] = f0 + (lane + k * LANES) * VEC;
+        act[k] = f[k] < feat;
+        a0[k] = splat<VEC>(0.0f);
+        a1[k] = a0[k];
+      }
       for (int32_t b = s; b < e; b += LANES) {
         int32_t mc = 0;
         float mv = 0.0f;
@@ -462,59 +470,67 @@ __global__ void __launch_bounds__(kBlock) gather_pair_kernel(
         }
         const int n = e - b < LANES ? e - b : LANES;
         for (int j = 0; j < n; j += 8) {
-          Vf<VEC> xv[8];
+          Vf<VEC> xv[8][NV];
           float w[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int jj = j + u;
             const int32_t c = __shfl_sync(gmask, mc, jj, LANES);
             w[u] = __shfl_sync(gmask, mv, jj, LANES);
-            xv[u] = (jj < n && act) ? ldv<VEC>(x + static_cast<int64_t>(c) * feat + f)
-                                    : splat<VEC>(0.0f);
+            const float *xr = x + static_cast<int64_t>(c) * feat;
+#pragma unroll
+            for (int k = 0; k < NV; ++k)
+              xv[u][k] = (jj < n && act[k]) ? ldv<VEC>(xr + f[k]) : splat<VEC>(0.0f);
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             if (j + u < n) {
-              Vf<VEC> &acc = (u & 1) ? a1 : a0;
 #pragma unroll
-              for (int i = 0; i < VEC; ++i) acc.v[i] = fmaf(xv[u].v[i], w[u], acc.v[i]);
+              for (int k = 0; k < NV; ++k) {
+                Vf<VEC> &acc = (u & 1) ? a1[k] : a0[k];
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) acc.v[i] = fmaf(xv[u][k].v[i], w[u], acc.v[i]);
+              }
             }
           }
         }
       }
-      Vf<VEC> o = vadd<VEC>(a0, a1);
-      if ((flags & AG_EPI_GIN) && act) {
-        const Vf<VEC> xr = ldv<VEC>(x + r * feat + f);
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) o.v[i] = fmaf(gin_scale, xr.v[i], o.v[i]);
-      }
-      if (flags & AG_EPI_RELU) {
+      for (int k = 0; k < NV; ++k) {
+        Vf<VEC> o = vadd<VEC>(a0[k], a1[k]);
+        if ((flags & AG_EPI_GIN) && act[k]) {
+          const Vf<VEC> xr = ldv<VEC>(x + r * feat + f[k]);
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) o.v[i] = fmaxf(o.v[i], 0.0f);
-      }
-      if ((flags & AG_EPI_RELU_MASK) && act) {
-        const uint32_t nib = (__ldg(relu_bits + r * ldw + (f >> 5)) >> (f & 31)) & 15u;
-#pragma unroll
-        for (int i = 0; i < VEC; ++i)
-          if (!((nib >> i) & 1u)) o.v[i] = 0.0f;
-      }
-      if (relu_out != nullptr) {  // 8 lanes x 4 columns = one mask word
-        uint32_t wd = 0;
-#pragma unroll
-        for (int i = 0; i < VEC; ++i)
-          if (act && f + i < feat && o.v[i] > 0.0f) wd |= 1u << (4 * (lane & 7) + i);
-        if constexpr (LANES >= 8) {
-          wd |= __shfl_xor_sync(gmask, wd, 1, LANES);
-          wd |= __shfl_xor_sync(gmask, wd, 2, LANES);
-          wd |= __shfl_xor_sync(gmask, wd, 4, LANES);
-          if ((lane & 7) == 0 && act) relu_out[r * ldw + (f >> 5)] = wd;
-        } else {  // fewer than 8 lanes: the group's lanes share one word
-#pragma unroll
-          for (int o2 = 1; o2 < LANES; o2 <<= 1) wd |= __shfl_xor_sync(gmask, wd, o2, LANES);
-          if (lane == 0) relu_out[r * ldw + (f0 >> 5)] = wd;
+          for (int i = 0; i < VEC; ++i) o.v[i] = fmaf(gin_scale, xr.v[i], o.v[i]);
         }
+        if (flags & AG_EPI_RELU) {
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) o.v[i] = fmaxf(o.v[i], 0.0f);
+        }
+        if ((flags & AG_EPI_RELU_MASK) && act[k]) {
+          const uint32_t nib = (__ldg(relu_bits + r * ldw + (f[k] >> 5)) >> (f[k] & 31)) & 15u;
+#pragma unroll
+          for (int i = 0; i < VEC; ++i)
+            if (!((nib >> i) & 1u)) o.v[i] = 0.0f;
+        }
+        if (relu_out != nullptr) {  // 8 lanes x 4 columns = one mask word
+          uint32_t wd = 0;
+#pragma unroll
+          for (int i = 0; i < VEC; ++i)
+            if (act[k] && f[k] + i < feat && o.v[i] > 0.0f) wd |= 1u << (4 * (lane & 7) + i);
+          if constexpr (LANES >= 8) {
+            wd |= __shfl_xor_sync(gmask, wd, 1, LANES);
+            wd |= __shfl_xor_sync(gmask, wd, 2, LANES);
+            wd |= __shfl_xor_sync(gmask, wd, 4, LANES);
+            if ((lane & 7) == 0 && act[k]) relu_out[r * ldw + (f[k] >> 5)] = wd;
+          } else {  // fewer than 8 lanes (NV = 1): the group's lanes share one word
+#pragma unroll
+            for (int o2 = 1; o2 < LANES; o2 <<= 1) wd |= __shfl_xor_sync(gmask, wd, o2, LANES);
+            if (lane == 0) relu_out[r * ldw + (f0 >> 5)] = wd;
+          }
+        }
+        if (act[k]) stv<VEC>(y + r * feat + f[k], o);
       }
-      if (act) stv<VEC>(y + r * feat + f, o);
     }
   }
 }
@@ -645,11 +661,11 @@ int launch_coo_gather_vec(int64_t rows, int64_t feat, const int32_t *row_ptr,
   }
 }
 
-template <int LANES>
+template <int LANES, int NV = 1>
 int launch_gather_pair(int64_t rows, int64_t feat, const int32_t *row_ptr, const int32_t *col,
                        const float *val, const float *x, float *y, int32_t flags, float gin,
                        const uint32_t *rb, uint32_t *ro, cudaStream_t st) {
-  auto k = gather_pair_kernel<LANES>;
+  auto k = gather_pair_kernel<LANES, NV>;
   const int64_t work = (rows * LANES + kBlock - 1) / kBlock;
   k<<<resident_grid(k, 0, work), kBlock, 0, st>>>(rows, feat, row_ptr, col, val, x, y, flags, gin,
                                                    rb, ro, relu_words(feat));
@@ -890,7 +906,12 @@ extern "C" int ag_gather_pair_spmm(int64_t num_rows, int64_t feat, const int32_t
                                          gin_scale, relu_bits, relu_out, st);
     case 16: return launch_gather_pair<16>(num_rows, feat, row_ptr, col, val, x, y, epi_flags,
                                            gin_scale, relu_bits, relu_out, st);
-    default: return launch_gather_pair<32>(num_rows, feat, row_ptr, col, val, x, y, epi_flags,
-                                           gin_scale, relu_bits, relu_out, st);
+    default:
+      // wider than 128 columns: two float4 chunks per lane per pass (256 columns)
+      if (feat > 128)
+        return launch_gather_pair<32, 2>(num_rows, feat, row_ptr, col, val, x, y, epi_flags,
+                                         gin_scale, relu_bits, relu_out, st);
+      return launch_gather_pair<32>(num_rows, feat, row_ptr, col, val, x, y, epi_flags,
+                                    gin_scale, relu_bits, relu_out, st);
   }
 }

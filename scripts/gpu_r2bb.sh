@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gather_gpu.py -q -m gpu -p no:cacheprovider -x > gpurun_out/pytest_g5.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_g5.log
+timeout 1200 python scripts/sensitivity.py > gpurun_out/sens5.json 2> gpurun_out/sens5.log
+echo done
