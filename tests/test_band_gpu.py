@@ -28,6 +28,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True)
 def _band_on(monkeypatch):
     monkeypatch.setenv("AG_BAND", "1")
+    monkeypatch.setenv("AG_GATHER", "0")  # these small graphs would take the gather pair
 DENSE_COO = dict(kernel_intra=ag.KernelKind.DENSE_BLOCK, kernel_inter=ag.KernelKind.COO_ATOMIC)
 
 
