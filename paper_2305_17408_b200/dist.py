@@ -498,7 +498,7 @@ class DistGNN:
             h_ext, width = h_next, dout
         logits = h_ext[:n, :width]
         loss = torch.empty(1, dtype=torch.float32, device=dev)
-        g = torch.zeros((n, models._pad4(width)), dtype=torch.float32, device=dev)[:, :width]
+        g = torch.empty((n, models._pad4(width)), dtype=torch.float32, device=dev)[:, :width]  # xent writes the pad
         _lib.call("ag_softmax_xent", n, logits.shape[1], logits.stride(0), _lib.ptr(logits),
                   _lib.ptr(labels), _lib.ptr(mask), int(num_masked), _lib.ptr(loss),
                   _lib.ptr(g), g.stride(0), _lib.stream())

@@ -449,8 +449,9 @@ class GNN:
 
     def loss_and_grad(self, logits, labels, mask, num_masked: int):
         loss = torch.empty(1, dtype=torch.float32, device=logits.device)
-        # zero pad columns: a gemm-first last layer aggregates the padded width
-        d_logits = torch.zeros((logits.shape[0], _pad4(logits.shape[1])), dtype=torch.float32,
+        # the kernel writes every column up to the padded width (pad columns 0: a
+        # gemm-first last layer aggregates the padded width), so no fill is needed
+        d_logits = torch.empty((logits.shape[0], _pad4(logits.shape[1])), dtype=torch.float32,
                                device=logits.device)[:, :logits.shape[1]]
         _lib.call("ag_softmax_xent", logits.shape[0], logits.shape[1], logits.stride(0),
                   _lib.ptr(logits), _lib.ptr(labels), _lib.ptr(mask), int(num_masked),
