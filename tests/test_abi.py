@@ -119,3 +119,24 @@ def test_edge_list_errors(tmp_path):
     f.write_text("0 -3\n")
     with pytest.raises(EdgeListError):
         load_edge_list(f)
+
+
+def test_cluster_bfs_host_bit_exact_at_config_scale():
+    """cluster_bfs at BASELINE scale (C2 pubmed-shaped, C3 ogbn-arxiv-shaped
+    graphs from the numpy generator twin): the host C++ partition's digests
+    equal the unmodified reference's (tests/golden/make_bfs_golden.py)."""
+    import hashlib
+    import json
+    import pathlib
+    from oracle import synth
+    gold = json.loads((pathlib.Path(__file__).parent / "golden" / "bfs_scale.json").read_text())
+
+    def digest(a):
+        return hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()
+
+    for case in gold["cases"]:
+        (dst, src), _ = synth.community_graph(case["V"], case["E"], seed=0, **case["generator"])
+        assert dst.size == case["edges_canonical"], case["name"]
+        comm, perm = _bfs(case["V"], dst, src, case["comm_size"])
+        assert digest(comm) == case["community_sha256"], case["name"]
+        assert digest(perm) == case["perm_sha256"], case["name"]
