@@ -3,10 +3,11 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/final
 O=gpurun_out/final
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
 timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
 timeout 1200 python bench.py --steps 10 --warmup 3 > $O/bench_C5.log 2>&1
 for c in C1 C2 C3 C4; do
-  timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > $O/bench_$c.log 2>&1
+  timeout 1500 python bench.py --config $c --steps 10 --warmup 3 > $O/bench_$c.log 2>&1
 done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.log 2>&1
 timeout 600 python scripts/step_profile.py > $O/step_profile.log 2>&1
